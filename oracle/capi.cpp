@@ -438,3 +438,42 @@ void or_raycast_depth(void* scene, const or_pose* T, const or_intrinsics* k, flo
 uint64_t or_stage_seed(uint64_t seed, int stage) { return stage_seed(seed, stage); }
 
 }  // extern "C"
+
+extern "C" {
+// Eq. 5 energy of pose H over grid-sample indices (KAT hook).
+int or_energy(void* fp, void* sp, const float* depth, const uint8_t* rgb, const or_intrinsics* k, const or_pose* H,
+              const int32_t* samples, int n, float* out) {
+  return guarded([&] {
+    const Frame fr = mk_frame(depth, rgb, *k, 1);
+    FrameCtx c;
+    build_frame_ctx(c, *static_cast<Forest*>(fp), *static_cast<AdaptState*>(sp), fr);
+    std::vector<int> s(samples, samples + n);
+    *out = energy(c, *static_cast<AdaptState*>(sp), to_pose(H->R, H->t), s);
+    return 0;
+  });
+}
+// lm_refine of pose H over grid-sample indices (KAT hook); returns the final surrogate.
+int or_lm(void* fp, void* sp, const float* depth, const uint8_t* rgb, const or_intrinsics* k, or_pose* H,
+          const int32_t* samples, int n, int use_cov, double* surrogate) {
+  return guarded([&] {
+    const Frame fr = mk_frame(depth, rgb, *k, 1);
+    FrameCtx c;
+    build_frame_ctx(c, *static_cast<Forest*>(fp), *static_cast<AdaptState*>(sp), fr);
+    std::vector<int> s(samples, samples + n);
+    Pose P = to_pose(H->R, H->t);
+    lm_refine(c, *static_cast<AdaptState*>(sp), P, s, use_cov != 0, surrogate);
+    std::memcpy(H, &P, sizeof(or_pose));
+    return 0;
+  });
+}
+int or_grid_count(void* fp, void* sp, const float* depth, const uint8_t* rgb, const or_intrinsics* k, int32_t* nmodes,
+                  int cap) {
+  return guarded([&] {
+    const Frame fr = mk_frame(depth, rgb, *k, 1);
+    FrameCtx c;
+    build_frame_ctx(c, *static_cast<Forest*>(fp), *static_cast<AdaptState*>(sp), fr);
+    for (size_t i = 0; i < c.nmodes.size() && static_cast<int>(i) < cap; ++i) nmodes[i] = c.nmodes[i];
+    return static_cast<int>(c.nmodes.size()) > cap ? -1 : 0;
+  });
+}
+}

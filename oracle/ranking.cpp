@@ -173,7 +173,13 @@ IcpResult icp_refine(const Scene& s, const Pose& init, const Frame& fr) {
           M[6 * a + b] = tot[kk];
           M[6 * b + a] = tot[kk];
         }
-      for (int a = 0; a < 6; ++a) rhs[a] = -tot[21 + a];
+      // damping mu = 1e-6 tr(A)/6 keeps directions the view does not constrain (e.g. height
+      // in front of a bare wall) at their current value instead of failing the solve
+      const double mu = 1e-6 * ((((((tot[0] + tot[6]) + tot[11]) + tot[15]) + tot[18]) + tot[20]) / 6.0);
+      for (int a = 0; a < 6; ++a) {
+        rhs[a] = -tot[21 + a];
+        M[6 * a + a] = M[6 * a + a] + mu;
+      }
       if (!chol6_solve(M, rhs, delta)) break;
       T = compose(exp_se3(delta), T);
     }

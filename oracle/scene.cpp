@@ -57,24 +57,28 @@ Scene generate_synthetic_scene(uint64_t seed, int complexity) {
         p.b[k] = walls[i][3 + k];
       }
     } else {
-      // objects spread round-robin over the four walls (even slots + jitter) so every
-      // view direction sees asymmetric geometry (breaks the room's 180-degree symmetry)
+      // objects evenly spaced by perimeter arc length (+ jitter) so every view direction
+      // sees non-planar, asymmetric geometry (breaks the room's symmetries)
       const int j = i - 6, nobj = n - 6;
-      const int wall = j % 4;  // 0: x=0, 1: x=X, 2: y=0, 3: y=Y
-      const int per_wall = (nobj + 3 - wall) / 4;
-      const int slot = j / 4;
+      const double perim = 2.0 * (X + Y);
+      const double s = (j + 0.5 + 0.3 * (rng.uniform() - 0.5)) * perim / nobj;
+      int wall;  // 0: x=0, 1: x=X, 2: y=0, 3: y=Y
+      double centre;
+      if (s < X) { wall = 2; centre = s; }
+      else if (s < X + Y) { wall = 1; centre = s - X; }
+      else if (s < 2.0 * X + Y) { wall = 3; centre = X - (s - X - Y); }
+      else { wall = 0; centre = Y - (s - 2.0 * X - Y); }
       const int along_axis = wall < 2 ? 1 : 0;
       const int nrm = wall < 2 ? 0 : 1;
       const double along_len = wall < 2 ? Y : X;
       const double wall_pos = (wall == 0 || wall == 2) ? 0.0 : (wall == 1 ? X : Y);
       const bool lowside = (wall == 0 || wall == 2);
-      const double centre = (slot + 0.5 + 0.3 * (rng.uniform() - 0.5)) * along_len / per_wall;
       if (rng.uniform() < 0.55) {  // box: floor-standing cabinet or wall shelf
-        const double w = 0.25 + 0.45 * rng.uniform();
+        const double w = 0.4 + 0.5 * rng.uniform();
         const double depth = 0.2 + 0.5 * rng.uniform();
         const double gap = 0.02 + 0.15 * rng.uniform();
         const bool floor = rng.bernoulli(0.7);
-        const double z0 = floor ? 0.0 : 0.6 + 0.8 * rng.uniform();
+        const double z0 = floor ? 0.0 : 0.5 + 0.6 * rng.uniform();
         const double h = floor ? 0.4 + 1.2 * rng.uniform() : 0.15 + 0.4 * rng.uniform();
         double mn[3], mx[3];
         if (lowside) { mn[nrm] = wall_pos + gap; mx[nrm] = mn[nrm] + std::min(depth, 0.9 - gap); }
@@ -86,9 +90,9 @@ Scene generate_synthetic_scene(uint64_t seed, int complexity) {
         p.type = 0;
         for (int k = 0; k < 3; ++k) { p.a[k] = static_cast<float>(mn[k]); p.b[k] = static_cast<float>(mx[k]); }
       } else {  // sphere
-        const double r = 0.12 + 0.23 * rng.uniform();
+        const double r = 0.2 + 0.2 * rng.uniform();
         const double gap = 0.05 + 0.25 * rng.uniform();
-        const double z = r + 0.1 + (1.9 - 2 * r) * rng.uniform();
+        const double z = r + 0.1 + (1.2 - r) * rng.uniform();
         double c[3];
         c[nrm] = lowside ? wall_pos + gap + r : wall_pos - gap - r;
         c[along_axis] = std::min(std::max(centre, r + 0.05), along_len - r - 0.05);
@@ -255,10 +259,10 @@ void generate_trajectory(uint64_t seed, int n, int kind, Pose* out) {
     double a, b, c, d;
     det_sincos(twopi * s + ph0, &a, &b);
     det_sincos(2 * twopi * s + ph1, &c, &d);
-    double px = 2.0 + 0.55 * b, py = 1.5 + 0.35 * a, pz = 1.4 + 0.15 * c;
+    double px = 2.0 + 0.5 * b, py = 1.5 + 0.2 * a, pz = 1.4 + 0.15 * c;
     double e, g;
     det_sincos(3 * twopi * s + ph3, &e, &g);
-    double yaw = ph2 + twopi * s, pitch = -0.2 + 0.12 * e, roll = 0.0;
+    double yaw = ph2 + twopi * s, pitch = -0.35 + 0.12 * e, roll = 0.0;
     if (kind == 1) {
       px += 0.06 * (2 * pert.uniform() - 1);
       py += 0.06 * (2 * pert.uniform() - 1);

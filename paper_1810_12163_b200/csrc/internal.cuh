@@ -1,0 +1,140 @@
+// Host/device internal state of the screloc B200 library (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace scr {
+
+void set_error(const std::string& msg);
+scr_status cuda_fail(cudaError_t e, const char* what);
+
+#define SCR_CUDA(expr)                                           \
+  do {                                                           \
+    cudaError_t _e = (expr);                                     \
+    if (_e != cudaSuccess) return ::scr::cuda_fail(_e, #expr);   \
+  } while (0)
+
+struct ForestView {
+  const int4* nodes;     // {left, right|leaf_id, feature, threshold bits}; left < 0 marks a leaf
+  const short4* specs;   // {dx, dy, kind, channel}
+  int T;
+  int node_base[kMaxTrees];
+  int leaf_base[kMaxTrees];
+};
+
+struct FrameGeom {
+  int W, H;
+  float fx, fy, cx, cy;     // f32 copies (feature/raycast arithmetic)
+  double dfx, dfy, dcx, dcy;  // f64 (backproject, geometry.hpp:198)
+};
+
+struct PredView {
+  const int* count;
+  const ModeGeom* geom;
+  const float4* col;
+};
+
+// Per-batch device workspace (frames are addressed by workspace slot f in [0, cap)).
+struct Workspace {
+  int cap = 0;    // frames
+  int gmax = 0;   // grid pixels per frame
+  float* depth = nullptr;     // staging for host uploads [cap * WH]
+  uint8_t* rgb = nullptr;     // [cap * WH * 3]
+  uint2* tex = nullptr;       // packed texels [cap * WH]: {depth or 0, rgb|valid<<24}
+  int* gcount = nullptr;      // [cap]
+  int* gpx = nullptr;         // [cap * gmax] packed x | y << 16
+  float4* gcam = nullptr;     // [cap * gmax] camera point (f32 of the f64 backprojection)
+  int* gslot = nullptr;       // [cap * gmax * T]
+  int* gnm = nullptr;         // [cap * gmax] number of modes (union over trees)
+  // RANSAC (grown on demand)
+  int nmax_cap = 0, ncull_cap = 0, samples_cap = 0;
+  Pose* hyp = nullptr;        // [cap * nmax]
+  float* henergy = nullptr;   // [cap * nmax]
+  int* hok = nullptr;         // [cap * nmax]
+  int* hiters = nullptr;      // [cap * nmax]
+  Pose* cand = nullptr;       // [cap * ncull]
+  float* cenergy = nullptr;   // [cap * ncull]
+  int* cslot = nullptr;       // [cap * ncull]
+  int* ncand = nullptr;       // [cap]
+  int* samples = nullptr;     // [cap * samples_cap]
+  int* assoc = nullptr;       // [cap * ncull * samples_cap]
+  // ranking / ICP
+  int icp_cap = 0;            // (frame, candidate) jobs resident at once
+  uint2* icp_map = nullptr;   // [icp_cap * WH] {t bits, prim | face << 16}
+  Pose* icp_pose = nullptr;   // [cap * ncull] refined poses
+  double* icp_score = nullptr;  // [cap * ncull]
+  int* icp_conv = nullptr;    // [cap * ncull]
+  double* icp_rms = nullptr;
+  double* icp_inl = nullptr;
+  int* fidx = nullptr;        // active frame list [cap]
+  uint64_t* seeds = nullptr;  // [cap]
+  int* status = nullptr;      // [cap]
+  // reservoir insertion scratch (one frame)
+  unsigned* ins_cnt = nullptr;  // [L]
+  unsigned* ins_off = nullptr;  // [L + 1]
+  unsigned* ins_cur = nullptr;  // [L]
+  int* ins_item = nullptr;      // [gmax * T] packed g * T + t
+  int* ins_tgt = nullptr;       // [gmax * T]
+  int* ins_rank = nullptr;      // [gmax * T]
+  unsigned* ins_total = nullptr;
+};
+
+}  // namespace scr
+
+struct scr_device_s {
+  int ordinal = 0;
+  int sm_count = 148;
+};
+
+struct scr_scene_s {
+  scr_device dev = nullptr;
+  cudaStream_t stream = nullptr;
+  scr_intrinsics k{};
+  scr::FrameGeom geom{};
+  scr_forest_params fp{};
+  uint64_t adapt_seed = 0;
+  int T = 0;
+  int64_t L = 0;
+  int64_t cursor = 0;
+  std::vector<int> node_base, leaf_base;
+  int4* d_nodes = nullptr;
+  short4* d_specs = nullptr;
+  scr_entry* d_entries = nullptr;
+  uint32_t* d_seen = nullptr;
+  int* d_count = nullptr;
+  scr::ModeGeom* d_geom = nullptr;
+  float4* d_col = nullptr;
+  float* d_cov = nullptr;   // 6 per mode (dumps only)
+  scr::Prim* d_prims = nullptr;
+  int n_prims = 0;
+  scr::Workspace ws;
+  int64_t launches = 0;
+  scr::ForestView forest_view() const;
+  scr::PredView pred_view() const { return {d_count, d_geom, d_col}; }
+};
+
+struct scr_frameset_s {
+  scr_scene scene = nullptr;
+  int cap = 0;
+  float* depth = nullptr;
+  uint8_t* rgb = nullptr;
+};
+
+namespace scr {
+// scene.cu
+scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_base, const int* d_idx, int n);
+scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int samples);
+scr_status ensure_icp_ws(scr_scene s, int jobs);
+// reloc.cu
+scr_status run_cascade(scr_scene s, int n, const scr_ransac_params* stages, const int32_t* modes,
+                       const double* thr, int nstages, const uint64_t* seeds, scr_result* out);
+scr_status run_ransac_debug(scr_scene s, const scr_ransac_params* p, uint64_t seed, int32_t* gen_slots,
+                            scr_pose* gen_poses, int* n_gen, int32_t* surv_slots, scr_pose* surv_poses,
+                            float* surv_energy, int* n_surv);
+scr_status run_icp_debug(scr_scene s, const scr_pose* init, scr_pose* out, int* conv, double* rms, double* inl,
+                         double* score);
+}  // namespace scr

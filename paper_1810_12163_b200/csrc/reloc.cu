@@ -1,0 +1,1109 @@
+// Per-frame relocalisation on the GPU: preemptive RANSAC (K4 generation, K5 energy,
+// K6 Levenberg-Marquardt, K7 cull/halving), ICP + depth-raycast ranking (K8-K10) and
+// the cascade controller (K11), for a batch of independent frames.
+//
+// Reference behaviour restated here (SPEC.md; the reference sources are missing):
+//   generate_hypothesis / generate_initial_hypotheses
+//   energy (Eq. 5)
+//   initial_cull
+//   lm_refine
+//   preemptive_ransac
+//   raycast_depth / icp_refine
+//   depth_diff_score (Eqs. 6-7)
+//   rank_hypotheses / relocalise / run_cascade
+// Geometry in f64 restates proj/include/screloc/geometry.hpp:83-191.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace scr {
+
+struct GenParams {
+  int max_iters, nmax;
+  double min_sq_dist;
+  float colour_thresh;
+  double rigidity_tol;
+};
+
+struct FrameRefs {  // per-batch views of the packed frames
+  const int* fidx;       // active index -> workspace slot
+  const int* gcount;
+  const int* gpx;
+  const float4* gcam;
+  const int* gslot;
+  const int* gnm;
+  const uint2* tex;
+  int gmax, T;
+};
+
+SCR_DEV int mode_index(const FrameRefs& fr, const int* pcount, size_t gbase, int m) {
+  for (int t = 0; t < fr.T; ++t) {
+    const int slot = fr.gslot[gbase * fr.T + t];
+    const int cnt = pcount[slot];
+    if (m < cnt) return slot * kMaxModes + m;
+    m -= cnt;
+  }
+  return -1;
+}
+
+// ================================ K4: hypothesis generation ================================
+// One thread per (frame, slot); slot s draws from Rng::stream(seed, s) and retries up to
+// max_iters. Draw order and checks follow DESIGN.md A1/A7.
+__global__ void __launch_bounds__(128) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
+                                                const uint64_t* __restrict__ seeds, Pose* __restrict__ hyp,
+                                                int* __restrict__ hok, int* __restrict__ hiters) {
+  const int a = blockIdx.y;
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= gp.nmax) return;
+  const int f = fr.fidx[a];
+  const uint64_t G = static_cast<uint64_t>(fr.gcount[f]);
+  const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
+  Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(slot));
+  int ok = 0, it = 0;
+  Pose T;
+  if (G > 0) {
+    const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+    const uint2* tex = fr.tex + static_cast<size_t>(f) * g.W * g.H;
+    for (it = 0; it < gp.max_iters; ++it) {
+      int gi[3], mi[3];
+      bool good = true;
+#pragma unroll 1
+      for (int k = 0; k < 3; ++k) {
+        gi[k] = static_cast<int>(rng_uniform_int(rng, G));
+        const int nm = fr.gnm[fbase + gi[k]];
+        if (nm == 0) {
+          good = false;
+          break;
+        }
+        mi[k] = mode_index(fr, pv.count, fbase + gi[k], static_cast<int>(rng_uniform_int(rng, static_cast<uint64_t>(nm))));
+      }
+      if (!good) continue;
+      const int cc = static_cast<int>(rng_uniform_int(rng, 3));
+      {
+        const int px = fr.gpx[fbase + gi[cc]];
+        const uint32_t col = tex[(px >> 16) * g.W + (px & 0xffff)].y;
+        const float4 mc = pv.col[mi[cc]];
+        float linf = 0.0f;
+        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
+        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 8) & 255u), mc.y)));
+        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 16) & 255u), mc.z)));
+        if (linf > gp.colour_thresh) continue;
+      }
+      double w[9], cm[9];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float4 q0 = pv.geom[mi[k]].q0;
+        w[3 * k + 0] = static_cast<double>(q0.x);
+        w[3 * k + 1] = static_cast<double>(q0.y);
+        w[3 * k + 2] = static_cast<double>(q0.z);
+        const int px = fr.gpx[fbase + gi[k]];
+        const int x = px & 0xffff, y = px >> 16;
+        const double dd = static_cast<double>(__uint_as_float(tex[y * g.W + x].x));
+        cm[3 * k + 0] = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
+        cm[3 * k + 1] = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
+        cm[3 * k + 2] = dd;
+      }
+      double dw2[3], dc2[3];
+      bool close = false;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
+        const double ax = w[3 * pa] - w[3 * pb], ay = w[3 * pa + 1] - w[3 * pb + 1], az = w[3 * pa + 2] - w[3 * pb + 2];
+        dw2[q] = (ax * ax + ay * ay) + az * az;
+        const double bx = cm[3 * pa] - cm[3 * pb], by = cm[3 * pa + 1] - cm[3 * pb + 1],
+                     bz = cm[3 * pa + 2] - cm[3 * pb + 2];
+        dc2[q] = (bx * bx + by * by) + bz * bz;
+        if (dw2[q] < gp.min_sq_dist) close = true;
+      }
+      if (close) continue;
+      bool nonrigid = false;
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > gp.rigidity_tol) nonrigid = true;
+      if (nonrigid) continue;
+      if (!kabsch3(cm, w, T)) continue;
+      ok = 1;
+      break;
+    }
+  }
+  if (ok) hyp[out] = T;
+  hok[out] = ok;
+  hiters[out] = ok ? it + 1 : gp.max_iters;
+}
+
+// Sample batch k of frame a: eta draws of uniform_int(G) from Rng::stream(seed, nmax + k).
+__global__ void k_draw_samples(FrameRefs fr, const uint64_t* __restrict__ seeds, int nA, int nmax, int eta, int batch,
+                               int scap, int* __restrict__ samples) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nA) return;
+  const uint64_t G = static_cast<uint64_t>(fr.gcount[fr.fidx[a]]);
+  int* out = samples + static_cast<size_t>(a) * scap + static_cast<size_t>(batch) * eta;
+  if (G == 0) {
+    for (int i = 0; i < eta; ++i) out[i] = 0;
+    return;
+  }
+  Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(nmax) + static_cast<uint64_t>(batch));
+  for (int i = 0; i < eta; ++i) out[i] = static_cast<int>(rng_uniform_int(rng, G));
+}
+
+// ================================ K5: Eq. 5 energy =========================================
+// One thread per (frame, hypothesis); a warp holds 32 hypotheses of one frame walking the
+// same samples, so every mode load is warp-uniform (one broadcast transaction).
+__global__ void __launch_bounds__(128) k_energy(FrameRefs fr, PredView pv, const Pose* __restrict__ poses,
+                                                const int* __restrict__ ok, int stride,
+                                                const int* __restrict__ nper, int min_n,
+                                                const int* __restrict__ samples, int scap, int ns,
+                                                float* __restrict__ out) {
+  const int a = blockIdx.y;
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = nper ? nper[a] : stride;
+  if (h >= n || n <= min_n) return;
+  const size_t idx = static_cast<size_t>(a) * stride + h;
+  if (ok && !ok[idx]) {
+    out[idx] = __int_as_float(0x7f800000);
+    return;
+  }
+  float R[9], t[3];
+  const Pose& P = poses[idx];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(P.R[i]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(P.t[i]);
+  const int f = fr.fidx[a];
+  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  const int* smp = samples + static_cast<size_t>(a) * scap;
+  float E = 0.0f;
+  for (int s = 0; s < ns; ++s) {
+    const int gi = smp[s];
+    const size_t gb = fbase + gi;
+    if (fr.gnm[gb] == 0) continue;
+    const float4 c = fr.gcam[gb];
+    float y[3];
+    xform_f32(R, t, c.x, c.y, c.z, y);
+    float qmin = __int_as_float(0x7f800000);
+    for (int tt = 0; tt < fr.T; ++tt) {
+      const int slot = fr.gslot[gb * fr.T + tt];
+      const int cnt = pv.count[slot];
+      const ModeGeom* mg = pv.geom + static_cast<size_t>(slot) * kMaxModes;
+      for (int m = 0; m < cnt; ++m) {
+        const float4 q0 = mg[m].q0, q1 = mg[m].q1, q2 = mg[m].q2;
+        const float q = quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(y[0], q0.x), __fsub_rn(y[1], q0.y),
+                                  __fsub_rn(y[2], q0.z));
+        qmin = fminf(qmin, q);
+      }
+    }
+    E = __fadd_rn(E, __fsqrt_rn(fmaxf(qmin, 0.0f)));
+  }
+  out[idx] = E;
+}
+
+// ================================ K7: cull / halving ========================================
+// One CTA per frame: bitonic sort of keys (energy bits << 32 | slot << 12 | position),
+// i.e. ascending energy with ties to the lower generation slot, then the
+// first `keep` entries become the candidate list.
+__global__ void __launch_bounds__(1024) k_select(const Pose* __restrict__ src_pose, const float* __restrict__ src_e,
+                                                 const int* __restrict__ src_ok, const int* __restrict__ src_slot,
+                                                 int src_stride, const int* __restrict__ src_n, int n_fixed,
+                                                 int keep_cap, int n_out, int halving, Pose* __restrict__ cand,
+                                                 float* __restrict__ cenergy, int* __restrict__ cslot,
+                                                 int* __restrict__ ncand, int cand_stride) {
+  extern __shared__ unsigned long long keys[];
+  const int a = blockIdx.x;
+  const int n = src_n ? src_n[a] : n_fixed;
+  if (halving && n <= n_out) return;
+  int P = 1;
+  while (P < n) P <<= 1;
+  const size_t base = static_cast<size_t>(a) * src_stride;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    unsigned long long k = ~0ull;
+    if (i < n && (!src_ok || src_ok[base + i])) {
+      const float e = src_e[base + i];
+      const uint32_t eb = isnan(e) ? 0x7f800000u : __float_as_uint(e);
+      const uint32_t sl = src_slot ? static_cast<uint32_t>(src_slot[base + i]) : static_cast<uint32_t>(i);
+      k = (static_cast<unsigned long long>(eb) << 32) | (static_cast<unsigned long long>(sl) << 12) |
+          static_cast<unsigned long long>(i);
+    }
+    keys[i] = k;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long x = keys[i], y = keys[ixj];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            keys[i] = y;
+            keys[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int valid = 0;
+  if (src_ok) {
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    int local = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) local += src_ok[base + i] ? 1 : 0;
+    atomicAdd(&cnt, local);
+    __syncthreads();
+    valid = cnt;
+  } else {
+    valid = n;
+  }
+  const int keep = halving ? (n + 1) / 2 : min(valid, keep_cap);
+  // gather into registers first: for halving the source and destination alias
+  Pose p;
+  float e = 0.0f;
+  int sl = 0;
+  const bool mine = threadIdx.x < keep;
+  if (mine) {
+    const int pos = static_cast<int>(keys[threadIdx.x] & 0xfffull);
+    p = src_pose[base + pos];
+    e = src_e[base + pos];
+    sl = src_slot ? src_slot[base + pos] : pos;
+  }
+  __syncthreads();
+  if (mine) {
+    const size_t o = static_cast<size_t>(a) * cand_stride + threadIdx.x;
+    cand[o] = p;
+    cenergy[o] = e;
+    cslot[o] = sl;
+  }
+  if (threadIdx.x == 0) ncand[a] = keep;
+}
+
+// ================================ K6: Levenberg-Marquardt ===================================
+// One warp per (frame, candidate). Lanes own samples i = lane (mod 32); association
+// (nearest mode, frozen per step) in f32, normal equations in f64 reduced with the xor
+// butterfly (identical on every lane, so every lane takes the same accept/reject path).
+struct LmArgs {
+  int ns, scap, cand_stride, n_out, use_cov;
+};
+
+SCR_DEV void lm_accum(const Pose& H, const double x[3], const ModeGeom& mg, bool use_cov, double acc[28], bool jac) {
+  double y[3];
+  pose_apply(H, x, y);
+  const double d0 = y[0] - static_cast<double>(mg.q0.x), d1 = y[1] - static_cast<double>(mg.q0.y),
+               d2 = y[2] - static_cast<double>(mg.q0.z);
+  double S[9];
+  if (use_cov) {
+    S[0] = mg.q2.y; S[1] = mg.q2.z; S[2] = mg.q2.w;
+    S[3] = mg.q2.z; S[4] = mg.q3.x; S[5] = mg.q3.y;
+    S[6] = mg.q2.w; S[7] = mg.q3.y; S[8] = mg.q3.z;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) S[i] = (i % 4 == 0) ? 1.0 : 0.0;
+  }
+  double r[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[i] = (S[3 * i + 0] * d0 + S[3 * i + 1] * d1) + S[3 * i + 2] * d2;
+  acc[27] = acc[27] + ((r[0] * r[0] + r[1] * r[1]) + r[2] * r[2]);
+  if (!jac) return;
+  double J[3][6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    J[i][0] = S[3 * i + 1] * (-y[2]) + S[3 * i + 2] * y[1];
+    J[i][1] = S[3 * i + 0] * y[2] + S[3 * i + 2] * (-y[0]);
+    J[i][2] = S[3 * i + 0] * (-y[1]) + S[3 * i + 1] * y[0];
+    J[i][3] = S[3 * i + 0];
+    J[i][4] = S[3 * i + 1];
+    J[i][5] = S[3 * i + 2];
+  }
+  int k = 0;
+#pragma unroll
+  for (int a = 0; a < 6; ++a)
+#pragma unroll
+    for (int b = a; b < 6; ++b, ++k) acc[k] = acc[k] + ((J[0][a] * J[0][b] + J[1][a] * J[1][b]) + J[2][a] * J[2][b]);
+#pragma unroll
+  for (int a = 0; a < 6; ++a) acc[21 + a] = acc[21 + a] + ((J[0][a] * r[0] + J[1][a] * r[1]) + J[2][a] * r[2]);
+}
+
+__global__ void __launch_bounds__(128) k_lm(FrameRefs fr, PredView pv, LmArgs la, const int* __restrict__ samples,
+                                            Pose* __restrict__ cand, const int* __restrict__ ncand,
+                                            int* __restrict__ assoc) {
+  const int a = blockIdx.y;
+  const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int n = ncand[a];
+  if (n <= la.n_out || h >= n) return;
+  const int f = fr.fidx[a];
+  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  const int* smp = samples + static_cast<size_t>(a) * la.scap;
+  int* as = assoc + (static_cast<size_t>(a) * la.cand_stride + h) * la.scap;
+  Pose H = cand[static_cast<size_t>(a) * la.cand_stride + h];
+  double lambda = 1e-3;
+  bool need_assoc = true;
+  for (int it = 0; it < 10; ++it) {
+    if (need_assoc) {
+      float R[9], t[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(H.R[i]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(H.t[i]);
+      for (int i = lane; i < la.ns; i += 32) {
+        const size_t gb = fbase + smp[i];
+        int best_m = -1;
+        if (fr.gnm[gb] > 0) {
+          const float4 c = fr.gcam[gb];
+          float y[3];
+          xform_f32(R, t, c.x, c.y, c.z, y);
+          float best = 0.0f;
+          for (int tt = 0; tt < fr.T; ++tt) {
+            const int slot = fr.gslot[gb * fr.T + tt];
+            const int cnt = pv.count[slot];
+            for (int m = 0; m < cnt; ++m) {
+              const int mi = slot * kMaxModes + m;
+              const float4 q0 = pv.geom[mi].q0;
+              const float d0 = __fsub_rn(y[0], q0.x), d1 = __fsub_rn(y[1], q0.y), d2 = __fsub_rn(y[2], q0.z);
+              float q;
+              if (la.use_cov) {
+                const float4 q1 = pv.geom[mi].q1, q2 = pv.geom[mi].q2;
+                q = quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, d0, d1, d2);
+              } else {
+                q = quad_eucl(d0, d1, d2);
+              }
+              if (best_m < 0 || q < best) {
+                best = q;
+                best_m = mi;
+              }
+            }
+          }
+        }
+        as[i] = best_m;
+      }
+      __syncwarp();
+      need_assoc = false;
+    }
+    double acc[28];
+#pragma unroll
+    for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+    for (int i = lane; i < la.ns; i += 32) {
+      const int mi = as[i];
+      if (mi < 0) continue;
+      const float4 c = fr.gcam[fbase + smp[i]];
+      const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
+      lm_accum(H, x, pv.geom[mi], la.use_cov != 0, acc, true);
+    }
+#pragma unroll
+    for (int k = 0; k < 28; ++k) acc[k] = warp_sum_xor(acc[k]);
+    const double E = acc[27];
+    if (!(E > 0.0)) break;
+    double M[36], rhs[6], delta[6];
+    int k = 0;
+#pragma unroll
+    for (int p = 0; p < 6; ++p)
+#pragma unroll
+      for (int q = p; q < 6; ++q, ++k) {
+        M[6 * p + q] = acc[k];
+        M[6 * q + p] = acc[k];
+      }
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      M[6 * p + p] = M[6 * p + p] + lambda * M[6 * p + p];
+      rhs[p] = -acc[21 + p];
+    }
+    if (!chol6(M, rhs, delta)) {
+      lambda = lambda * 10.0;
+      continue;
+    }
+    Pose D, Hn;
+    exp_se3(delta, D);
+    pose_compose(D, H, Hn);
+    double accn[28];
+    accn[27] = 0.0;
+    for (int i = lane; i < la.ns; i += 32) {
+      const int mi = as[i];
+      if (mi < 0) continue;
+      const float4 c = fr.gcam[fbase + smp[i]];
+      const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
+      lm_accum(Hn, x, pv.geom[mi], la.use_cov != 0, accn, false);
+    }
+    const double En = warp_sum_xor(accn[27]);
+    if (En < E) {
+      H = Hn;
+      lambda = lambda * 0.1;
+      need_assoc = true;
+      if ((E - En) / E < 1e-6) break;
+    } else {
+      lambda = lambda * 10.0;
+    }
+  }
+  if (lane == 0) cand[static_cast<size_t>(a) * la.cand_stride + h] = H;
+}
+
+// ================================ K8-K10: ICP + raycast + depth-difference score ============
+// One 256-thread CTA per (frame, candidate) job. Thread l owns pixels p = l (mod 256) of
+// each pass (the canonical reduction order of DESIGN.md); per-thread partials are f32,
+// combined in f64 by a warp xor butterfly and then sequentially over the 8 warps.
+struct IcpArgs {
+  int cand_stride, n_cand_jobs;  // jobs per frame (1 for icp/raw, n_out for ranked)
+  int do_icp;
+  int job0;                      // first job of this chunk
+  size_t map_stride;
+};
+
+template <int NV>
+__device__ __forceinline__ void block_reduce_f32(const float* v, double (*red)[32], double* out) {
+  constexpr int nv = NV;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < nv; ++k) {
+    const double s = warp_sum_xor(static_cast<double>(v[k]));
+    if (lane == 0) red[wid][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double s = red[0][threadIdx.x];
+    for (int w = 1; w < (kLanes / 32); ++w) s = s + red[w][threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int block_isum(int v, int* ired) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_isum(v);
+  if (lane == 0) ired[wid] = v;
+  __syncthreads();
+  int s = 0;
+  for (int w = 0; w < kLanes / 32; ++w) s += ired[w];
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, FrameRefs fr, const Prim* __restrict__ prims,
+                                                   int nprims, const Pose* __restrict__ cand,
+                                                   const int* __restrict__ ncand, uint2* __restrict__ maps,
+                                                   Pose* __restrict__ out_pose, int* __restrict__ out_conv,
+                                                   double* __restrict__ out_rms, double* __restrict__ out_inl,
+                                                   double* __restrict__ out_score) {
+  __shared__ double red[kLanes / 32][32];
+  __shared__ double tot[32];
+  __shared__ int ired[kLanes / 32];
+  __shared__ Pose Ts;
+  __shared__ int stop_level;
+  const int job = ia.job0 + blockIdx.x;
+  const int a = job / ia.n_cand_jobs, c = job % ia.n_cand_jobs;
+  if (c >= ncand[a]) return;
+  const int f = fr.fidx[a];
+  const size_t cidx = static_cast<size_t>(a) * ia.cand_stride + c;
+  const uint2* tex = fr.tex + static_cast<size_t>(f) * g.W * g.H;
+  uint2* map = maps + static_cast<size_t>(blockIdx.x) * ia.map_stride;
+  if (threadIdx.x == 0) Ts = cand[cidx];
+  __syncthreads();
+  int last_inl = 0, last_valid = 0;
+  double last_r2 = 0.0;
+  bool have_stats = false;
+  if (ia.do_icp) {
+    for (int level = 2; level >= 0; --level) {
+      const int fs = 1 << level;
+      const int Wl = g.W / fs, Hl = g.H / fs;
+      const float fxl = static_cast<float>(g.dfx / fs), fyl = static_cast<float>(g.dfy / fs);
+      const float cxl = static_cast<float>(g.dcx / fs), cyl = static_cast<float>(g.dcy / fs);
+      const Pose Tref = Ts;
+      Pose Tinv;
+      pose_invert(Tref, Tinv);
+      float Rr[9], tr[3], Ri[9], ti[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        Rr[i] = static_cast<float>(Tref.R[i]);
+        Ri[i] = static_cast<float>(Tinv.R[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        tr[i] = static_cast<float>(Tref.t[i]);
+        ti[i] = static_cast<float>(Tinv.t[i]);
+      }
+      // K8: model map of this level at the reference pose
+      for (int p = threadIdx.x; p < Wl * Hl; p += blockDim.x) {
+        float d[3];
+        ray_dir(Rr, fxl, fyl, cxl, cyl, p % Wl, p / Wl, d);
+        const Hit h = raycast(prims, nprims, tr, d);
+        uint2 v = make_uint2(0u, 0xffffffffu);
+        if (h.prim >= 0 && h.t <= kRenderMaxDepth) v = make_uint2(__float_as_uint(h.t), h.prim | (h.face << 16));
+        map[p] = v;
+      }
+      if (threadIdx.x == 0) stop_level = 0;
+      __syncthreads();
+      const int iters = level == 2 ? 10 : (level == 1 ? 5 : 4);
+      for (int it = 0; it < iters; ++it) {
+        const Pose T = Ts;
+        float R[9], t[3];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(T.R[i]);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(T.t[i]);
+        float acc[28];
+#pragma unroll
+        for (int k = 0; k < 28; ++k) acc[k] = 0.0f;
+        int inl = 0, valid = 0;
+        // K9: projective point-to-plane association + normal equations
+        for (int p = threadIdx.x; p < Wl * Hl; p += blockDim.x) {
+          const int x = p % Wl, y = p / Wl;
+          const float dl = __uint_as_float(tex[(y * fs) * g.W + x * fs].x);
+          if (!depth_valid(dl)) continue;
+          ++valid;
+          const float dcx = __fdiv_rn(__fsub_rn(static_cast<float>(x), cxl), fxl);
+          const float dcy = __fdiv_rn(__fsub_rn(static_cast<float>(y), cyl), fyl);
+          const float pc0 = __fmul_rn(dcx, dl), pc1 = __fmul_rn(dcy, dl);
+          float pw[3], pr[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            pw[i] = __fmaf_rn(R[3 * i + 0], pc0, __fmaf_rn(R[3 * i + 1], pc1, __fmaf_rn(R[3 * i + 2], dl, t[i])));
+#pragma unroll
+          for (int i = 0; i < 3; ++i)
+            pr[i] = __fmaf_rn(Ri[3 * i + 0], pw[0], __fmaf_rn(Ri[3 * i + 1], pw[1], __fmaf_rn(Ri[3 * i + 2], pw[2], ti[i])));
+          if (!(pr[2] > 0.0f)) continue;
+          const float uf = __fmaf_rn(fxl, __fdiv_rn(pr[0], pr[2]), cxl);
+          const float vf = __fmaf_rn(fyl, __fdiv_rn(pr[1], pr[2]), cyl);
+          if (!(uf > -0.5f && vf > -0.5f && uf < __fsub_rn(static_cast<float>(Wl), 0.5f) &&
+                vf < __fsub_rn(static_cast<float>(Hl), 0.5f)))
+            continue;
+          const int ui = static_cast<int>(floorf(__fadd_rn(uf, 0.5f)));
+          const int vi = static_cast<int>(floorf(__fadd_rn(vf, 0.5f)));
+          if (ui < 0 || vi < 0 || ui >= Wl || vi >= Hl) continue;
+          const uint2 mv = map[vi * Wl + ui];
+          if (mv.y == 0xffffffffu) continue;
+          const float th = __uint_as_float(mv.x);
+          float dm[3], m[3], nn[3];
+          ray_dir(Rr, fxl, fyl, cxl, cyl, ui, vi, dm);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) m[i] = __fmaf_rn(th, dm[i], tr[i]);
+          hit_normal(prims, static_cast<int>(mv.y & 0xffffu), static_cast<int>(mv.y >> 16), m, nn);
+          const float df0 = __fsub_rn(pw[0], m[0]), df1 = __fsub_rn(pw[1], m[1]), df2 = __fsub_rn(pw[2], m[2]);
+          const float dist2 = __fmaf_rn(df0, df0, __fmaf_rn(df1, df1, __fmul_rn(df2, df2)));
+          if (!(dist2 <= 0.01f)) continue;
+          const float r = __fmaf_rn(nn[0], df0, __fmaf_rn(nn[1], df1, __fmul_rn(nn[2], df2)));
+          const float J[6] = {__fmaf_rn(pw[1], nn[2], -__fmul_rn(pw[2], nn[1])),
+                              __fmaf_rn(pw[2], nn[0], -__fmul_rn(pw[0], nn[2])),
+                              __fmaf_rn(pw[0], nn[1], -__fmul_rn(pw[1], nn[0])), nn[0], nn[1], nn[2]};
+          int k = 0;
+#pragma unroll
+          for (int aa = 0; aa < 6; ++aa)
+#pragma unroll
+            for (int bb = aa; bb < 6; ++bb, ++k) acc[k] = __fmaf_rn(J[aa], J[bb], acc[k]);
+#pragma unroll
+          for (int aa = 0; aa < 6; ++aa) acc[21 + aa] = __fmaf_rn(J[aa], r, acc[21 + aa]);
+          acc[27] = __fmaf_rn(r, r, acc[27]);
+          ++inl;
+        }
+        block_reduce_f32<28>(acc, red, tot);
+        const int inl_t = block_isum(inl, ired);
+        const int valid_t = block_isum(valid, ired);
+        if (level == 0) {
+          last_inl = inl_t;
+          last_valid = valid_t;
+          last_r2 = tot[27];
+          have_stats = true;
+        }
+        if (threadIdx.x == 0) {
+          bool stop = inl_t < 6;
+          if (!stop) {
+            double M[36], rhs[6], delta[6];
+            int k = 0;
+            for (int p = 0; p < 6; ++p)
+              for (int q = p; q < 6; ++q, ++k) {
+                M[6 * p + q] = tot[k];
+                M[6 * q + p] = tot[k];
+              }
+            const double mu = 1e-6 * ((((((tot[0] + tot[6]) + tot[11]) + tot[15]) + tot[18]) + tot[20]) / 6.0);
+            for (int p = 0; p < 6; ++p) {
+              rhs[p] = -tot[21 + p];
+              M[6 * p + p] = M[6 * p + p] + mu;
+            }
+            if (!chol6(M, rhs, delta)) {
+              stop = true;
+            } else {
+              Pose D, Tn;
+              exp_se3(delta, D);
+              pose_compose(D, Ts, Tn);
+              Ts = Tn;
+            }
+          }
+          stop_level = stop ? 1 : 0;
+        }
+        __syncthreads();
+        if (stop_level) break;
+      }
+      __syncthreads();
+    }
+  }
+  const Pose Tf = Ts;
+  int conv = 1;
+  double rms = 0.0, inlf = 0.0;
+  if (ia.do_icp) {
+    if (have_stats && last_valid > 0 && last_inl > 0) {
+      inlf = static_cast<double>(last_inl) / static_cast<double>(last_valid);
+      rms = sqrt(last_r2 / static_cast<double>(last_inl));
+      conv = (inlf >= 0.5 && rms <= 0.02) ? 1 : 0;
+    } else {
+      inlf = 0.0;
+      rms = __longlong_as_double(0x7ff0000000000000ll);
+      conv = 0;
+    }
+  }
+  double score = __longlong_as_double(0x7ff0000000000000ll);
+  if (conv) {
+    // K10: raycast at the final pose fused with the Eq. 6-7 depth difference
+    float R[9], t[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(Tf.R[i]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(Tf.t[i]);
+    float sum = 0.0f;
+    int mutual = 0, synth = 0;
+    for (int p = threadIdx.x; p < g.W * g.H; p += blockDim.x) {
+      float d[3];
+      ray_dir(R, g.fx, g.fy, g.cx, g.cy, p % g.W, p / g.W, d);
+      const Hit h = raycast(prims, nprims, t, d);
+      if (h.prim < 0 || !(h.t <= kRenderMaxDepth) || !depth_valid(h.t)) continue;
+      ++synth;
+      const float dl = __uint_as_float(tex[p].x);
+      if (!depth_valid(dl)) continue;
+      ++mutual;
+      sum = __fadd_rn(sum, fabsf(__fsub_rn(dl, h.t)));
+    }
+    block_reduce_f32<1>(&sum, red, tot);
+    const int mutual_t = block_isum(mutual, ired);
+    const int synth_t = block_isum(synth, ired);
+    if (static_cast<double>(synth_t) < 0.1 * static_cast<double>(g.W) * static_cast<double>(g.H) || mutual_t == 0)
+      score = __longlong_as_double(0x7ff0000000000000ll);
+    else
+      score = tot[0] / static_cast<double>(mutual_t);
+  }
+  if (threadIdx.x == 0) {
+    out_pose[cidx] = Tf;
+    out_conv[cidx] = conv;
+    out_rms[cidx] = rms;
+    out_inl[cidx] = inlf;
+    out_score[cidx] = score;
+  }
+}
+
+// ================================ K11: per-frame result =====================================
+__global__ void k_finalize(int nA, int mode, int cand_stride, const Pose* __restrict__ cand,
+                           const int* __restrict__ ncand, const Pose* __restrict__ icp_pose,
+                           const int* __restrict__ icp_conv, const double* __restrict__ icp_score,
+                           scr_result* __restrict__ res) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nA) return;
+  scr_result r;
+  memset(&r, 0, sizeof(r));
+  r.score = __longlong_as_double(0x7ff0000000000000ll);
+  const int n = ncand[a];
+  r.n_candidates = n;
+  const size_t b = static_cast<size_t>(a) * cand_stride;
+  if (n == 0) {
+    r.status = SCR_E_NO_HYPOTHESES;
+  } else if (mode == SCR_MODE_RAW) {
+    r.has_pose = 1;
+    memcpy(&r.pose, &cand[b], sizeof(scr_pose));
+    r.score = icp_score[b];
+  } else if (mode == SCR_MODE_ICP) {
+    r.has_pose = 1;
+    if (icp_conv[b]) {
+      memcpy(&r.pose, &icp_pose[b], sizeof(scr_pose));
+      r.score = icp_score[b];
+    } else {
+      memcpy(&r.pose, &cand[b], sizeof(scr_pose));
+    }
+  } else {
+    int bi = -1;
+    double best = __longlong_as_double(0x7ff0000000000000ll);
+    for (int c = 0; c < n; ++c) {
+      const double sc = icp_conv[b + c] ? icp_score[b + c] : __longlong_as_double(0x7ff0000000000000ll);
+      if (sc < best) {
+        best = sc;
+        bi = c;
+      }
+    }
+    if (bi < 0) {
+      r.status = SCR_E_ALL_CANDIDATES_FAILED;
+    } else {
+      r.has_pose = 1;
+      memcpy(&r.pose, &icp_pose[b + bi], sizeof(scr_pose));
+      r.score = best;
+    }
+  }
+  res[a] = r;
+}
+
+// ================================ host orchestration ========================================
+namespace {
+
+FrameRefs frame_refs(scr_scene s) {
+  FrameRefs fr;
+  fr.fidx = s->ws.fidx;
+  fr.gcount = s->ws.gcount;
+  fr.gpx = s->ws.gpx;
+  fr.gcam = s->ws.gcam;
+  fr.gslot = s->ws.gslot;
+  fr.gnm = s->ws.gnm;
+  fr.tex = s->ws.tex;
+  fr.gmax = s->ws.gmax;
+  fr.T = s->T;
+  return fr;
+}
+
+int halvings(int n_cull, int n_out) {
+  int k = 0, n = n_cull;
+  while (n > n_out) {
+    n = (n + 1) / 2;
+    ++k;
+  }
+  return k;
+}
+
+template <typename T>
+scr_status grow(T** p, size_t count) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  SCR_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, count) * sizeof(T)));
+  return SCR_OK;
+}
+
+#define SCR_TRY(x)               \
+  do {                           \
+    scr_status _s = (x);         \
+    if (_s != SCR_OK) return _s; \
+  } while (0)
+
+// One relocaliser stage for the nA active frames already listed in
+// ws.fidx / ws.seeds. Results land in d_res[0..nA).
+scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, scr_result* d_res) {
+  Workspace& w = s->ws;
+  if (p.n_max <= 0 || p.n_max > 4096 || p.n_cull <= 0 || p.n_cull > 64 || p.eta <= 0 || p.n_out <= 0 ||
+      p.max_gen_iters <= 0) {
+    set_error("ransac params out of range (n_max <= 4096, n_cull <= 64)");
+    return SCR_E_ARG;
+  }
+  const int K = halvings(p.n_cull, p.n_out);
+  const int scap = p.eta * (K + 1);
+  SCR_TRY(ensure_ransac_ws(s, p.n_max, p.n_cull, scap));
+  const int jobs_per = mode == SCR_MODE_RANKED ? std::min(p.n_out, p.n_cull) : 1;
+  SCR_TRY(ensure_icp_ws(s, std::min(nA * jobs_per, 1024)));
+  const FrameRefs fr = frame_refs(s);
+  const PredView pv = s->pred_view();
+  GenParams gp{p.max_gen_iters, p.n_max, p.min_sq_dist, p.colour_thresh, p.rigidity_tol};
+  k_hypgen<<<dim3((p.n_max + 127) / 128, nA), 128, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds, w.hyp, w.hok,
+                                                                     w.hiters);
+  k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, 0, w.samples_cap, w.samples);
+  k_energy<<<dim3((p.n_max + 127) / 128, nA), 128, 0, s->stream>>>(fr, pv, w.hyp, w.hok, p.n_max, nullptr, -1,
+                                                                     w.samples, w.samples_cap, p.eta, w.henergy);
+  int P = 1;
+  while (P < p.n_max) P <<= 1;
+  k_select<<<nA, 1024, P * sizeof(unsigned long long), s->stream>>>(w.hyp, w.henergy, w.hok, nullptr, p.n_max,
+                                                                    nullptr, p.n_max, p.n_cull, p.n_out, 0, w.cand,
+                                                                    w.cenergy, w.cslot, w.ncand, w.ncull_cap);
+  s->launches += 4;
+  LmArgs la{0, w.samples_cap, w.ncull_cap, p.n_out, p.use_cov};
+  for (int k = 1; k <= K; ++k) {
+    k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, k, w.samples_cap,
+                                                         w.samples);
+    const int ns = p.eta * (k + 1);
+    if (p.pose_update) {
+      la.ns = ns;
+      k_lm<<<dim3((p.n_cull + 3) / 4, nA), 128, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, w.assoc);
+      s->launches += 1;
+    }
+    // rescore (only frames still above n_out take part; others keep their energies)
+    k_energy<<<dim3((p.n_cull + 127) / 128, nA), 128, 0, s->stream>>>(fr, pv, w.cand, nullptr, w.ncull_cap, w.ncand,
+                                                                        p.n_out, w.samples, w.samples_cap, ns,
+                                                                        w.henergy);
+    // henergy is used as scratch [nA * ncull_cap] for the rescored energies
+    int Pc = 1;
+    while (Pc < p.n_cull) Pc <<= 1;
+    k_select<<<nA, 1024, Pc * sizeof(unsigned long long), s->stream>>>(w.cand, w.henergy, nullptr, w.cslot,
+                                                                       w.ncull_cap, w.ncand, 0, p.n_cull, p.n_out, 1,
+                                                                       w.cand, w.cenergy, w.cslot, w.ncand,
+                                                                       w.ncull_cap);
+    s->launches += 3;
+  }
+  SCR_CUDA(cudaGetLastError());
+  // ICP / scoring jobs
+  const int njobs = nA * jobs_per;
+  for (int j0 = 0; j0 < njobs; j0 += w.icp_cap) {
+    const int nj = std::min(w.icp_cap, njobs - j0);
+    IcpArgs ia{w.ncull_cap, jobs_per, mode != SCR_MODE_RAW ? 1 : 0, j0,
+               static_cast<size_t>(s->k.width) * s->k.height};
+    k_icp_score<<<nj, 256, 0, s->stream>>>(ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand, w.icp_map,
+                                           w.icp_pose, w.icp_conv, w.icp_rms, w.icp_inl, w.icp_score);
+    s->launches += 1;
+  }
+  k_finalize<<<(nA + 127) / 128, 128, 0, s->stream>>>(nA, mode, w.ncull_cap, w.cand, w.ncand, w.icp_pose, w.icp_conv,
+                                                      w.icp_score, d_res);
+  s->launches += 1;
+  SCR_CUDA(cudaGetLastError());
+  return SCR_OK;
+}
+
+}  // namespace
+
+scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int scap) {
+  Workspace& w = s->ws;
+  const size_t B = static_cast<size_t>(w.cap);
+  if (nmax > w.nmax_cap) {
+    SCR_TRY(grow(&w.hyp, B * nmax));
+    SCR_TRY(grow(&w.henergy, B * std::max(nmax, 64)));
+    SCR_TRY(grow(&w.hok, B * nmax));
+    SCR_TRY(grow(&w.hiters, B * nmax));
+    w.nmax_cap = nmax;
+  }
+  if (ncull > w.ncull_cap || scap > w.samples_cap) {
+    const int nc = std::max(ncull, w.ncull_cap), sc = std::max(scap, w.samples_cap);
+    SCR_TRY(grow(&w.cand, B * nc));
+    SCR_TRY(grow(&w.cenergy, B * nc));
+    SCR_TRY(grow(&w.cslot, B * nc));
+    SCR_TRY(grow(&w.ncand, B));
+    SCR_TRY(grow(&w.samples, B * sc));
+    SCR_TRY(grow(&w.assoc, B * nc * sc));
+    SCR_TRY(grow(&w.icp_pose, B * nc));
+    SCR_TRY(grow(&w.icp_score, B * nc));
+    SCR_TRY(grow(&w.icp_conv, B * nc));
+    SCR_TRY(grow(&w.icp_rms, B * nc));
+    SCR_TRY(grow(&w.icp_inl, B * nc));
+    w.ncull_cap = nc;
+    w.samples_cap = sc;
+    if (w.henergy && static_cast<size_t>(w.nmax_cap) < static_cast<size_t>(nc)) {
+      SCR_TRY(grow(&w.henergy, B * std::max(w.nmax_cap, nc)));
+    }
+  }
+  return SCR_OK;
+}
+
+scr_status ensure_icp_ws(scr_scene s, int jobs) {
+  Workspace& w = s->ws;
+  jobs = std::max(jobs, 1);
+  if (jobs > w.icp_cap) {
+    SCR_TRY(grow(&w.icp_map, static_cast<size_t>(jobs) * s->k.width * s->k.height));
+    w.icp_cap = jobs;
+  }
+  return SCR_OK;
+}
+
+uint64_t stage_seed(uint64_t seed, int stage) { return seed + static_cast<uint64_t>(stage) * 0x9e3779b97f4a7c15ull; }
+
+// run_cascade for frames packed in workspace slots 0..n-1.
+scr_status run_cascade(scr_scene s, int n, const scr_ransac_params* stages, const int32_t* modes, const double* thr,
+                       int nstages, const uint64_t* seeds, scr_result* out) {
+  Workspace& w = s->ws;
+  std::vector<int> active(n);
+  for (int i = 0; i < n; ++i) active[i] = i;
+  std::vector<int> act_idx;
+  std::vector<uint64_t> act_seed;
+  std::vector<scr_result> res(n);
+  scr_result* d_res = nullptr;
+  SCR_CUDA(cudaMalloc(&d_res, std::max(1, n) * sizeof(scr_result)));
+  cudaEvent_t ev0, ev1;
+  cudaEventCreate(&ev0);
+  cudaEventCreate(&ev1);
+  for (int st = 0; st < nstages && !active.empty(); ++st) {
+    const int nA = static_cast<int>(active.size());
+    act_seed.resize(nA);
+    for (int i = 0; i < nA; ++i) act_seed[i] = stage_seed(seeds[active[i]], st);
+    SCR_CUDA(cudaMemcpyAsync(w.fidx, active.data(), nA * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    SCR_CUDA(cudaMemcpyAsync(w.seeds, act_seed.data(), nA * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream));
+    cudaEventRecord(ev0, s->stream);
+    scr_status rs = run_stage(s, nA, stages[st], modes[st], d_res);
+    if (rs != SCR_OK) {
+      cudaFree(d_res);
+      return rs;
+    }
+    cudaEventRecord(ev1, s->stream);
+    std::vector<scr_result> sr(nA);
+    SCR_CUDA(cudaMemcpyAsync(sr.data(), d_res, nA * sizeof(scr_result), cudaMemcpyDeviceToHost, s->stream));
+    SCR_CUDA(cudaStreamSynchronize(s->stream));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    std::vector<int> next;
+    for (int i = 0; i < nA; ++i) {
+      const int f = active[i];
+      float keep[4];
+      std::memcpy(keep, res[f].stage_ms, sizeof(keep));
+      res[f] = sr[i];
+      std::memcpy(res[f].stage_ms, keep, sizeof(keep));
+      if (st < 4) res[f].stage_ms[st] = ms / nA;
+      res[f].stage_used = st;
+      if (st < nstages - 1 && !(sr[i].score <= thr[st])) next.push_back(f);
+    }
+    active.swap(next);
+  }
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaFree(d_res);
+  std::memcpy(out, res.data(), n * sizeof(scr_result));
+  return SCR_OK;
+}
+
+}  // namespace scr
+
+using namespace scr;
+
+namespace {
+scr_status check_stage_args(int n, const scr_ransac_params* stages, const int32_t* modes, int nstages,
+                            const uint64_t* seeds, scr_result* out) {
+  if (n < 0 || !stages || !modes || nstages <= 0 || (!seeds && n > 0) || (!out && n > 0)) {
+    set_error("null or empty argument");
+    return SCR_E_ARG;
+  }
+  for (int i = 0; i < nstages; ++i)
+    if (modes[i] < 0 || modes[i] > 2) {
+      set_error("mode must be raw (0), icp (1) or ranked (2)");
+      return SCR_E_ARG;
+    }
+  return SCR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+scr_status scr_cascade_batch(scr_scene s, const scr_frame* frames, int n, const scr_ransac_params* stages,
+                             const int32_t* modes, const double* thr, int nstages, const uint64_t* seeds,
+                             scr_result* out) {
+  if (!s) return SCR_E_ARG;
+  SCR_TRY(check_stage_args(n, stages, modes, nstages, seeds, out));
+  if (nstages > 1 && !thr) return SCR_E_ARG;
+  if (!s->d_prims) {  // every mode scores its output against the model (A11)
+    set_error("relocalise: no scene model set (scr_scene_set_analytic_model)");
+    return SCR_E_ARG;
+  }
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  for (int b0 = 0; b0 < n; b0 += s->ws.cap) {
+    const int nb = std::min(s->ws.cap, n - b0);
+    for (int i = 0; i < nb; ++i) {
+      const scr_frame& fr = frames[b0 + i];
+      if (!fr.depth || !fr.rgb) return SCR_E_ARG;
+      SCR_CUDA(cudaMemcpyAsync(s->ws.depth + i * WH, fr.depth, WH * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+      SCR_CUDA(cudaMemcpyAsync(s->ws.rgb + i * WH * 3, fr.rgb, WH * 3, cudaMemcpyHostToDevice, s->stream));
+    }
+    SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, nb));
+    SCR_TRY(run_cascade(s, nb, stages, modes, thr, nstages, seeds + b0, out + b0));
+  }
+  return SCR_OK;
+}
+
+scr_status scr_relocalise_batch(scr_scene s, const scr_frame* frames, int n, const scr_ransac_params* p, int mode,
+                                const uint64_t* seeds, scr_result* out) {
+  const int32_t m = mode;
+  return scr_cascade_batch(s, frames, n, p, &m, nullptr, 1, seeds, out);
+}
+
+scr_status scr_cascade_frameset(scr_scene s, scr_frameset fs, const int32_t* idx, int n,
+                                const scr_ransac_params* stages, const int32_t* modes, const double* thr,
+                                int nstages, const uint64_t* seeds, scr_result* out) {
+  if (!s || !fs || (!idx && n > 0)) return SCR_E_ARG;
+  SCR_TRY(check_stage_args(n, stages, modes, nstages, seeds, out));
+  if (nstages > 1 && !thr) return SCR_E_ARG;
+  if (!s->d_prims) {
+    set_error("relocalise: no scene model set (scr_scene_set_analytic_model)");
+    return SCR_E_ARG;
+  }
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  for (int i = 0; i < n; ++i)
+    if (idx[i] < 0 || idx[i] >= fs->cap) return SCR_E_ARG;
+  for (int b0 = 0; b0 < n; b0 += s->ws.cap) {
+    const int nb = std::min(s->ws.cap, n - b0);
+    SCR_CUDA(cudaMemcpyAsync(s->ws.status, idx + b0, nb * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    SCR_TRY(pack_frames(s, fs->depth, fs->rgb, s->ws.status, nb));
+    SCR_TRY(run_cascade(s, nb, stages, modes, thr, nstages, seeds + b0, out + b0));
+  }
+  return SCR_OK;
+}
+
+scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_params* p, uint64_t seed,
+                            int32_t* gen_slots, scr_pose* gen_poses, int* n_gen, int32_t* surv_slots,
+                            scr_pose* surv_poses, float* surv_energy, int* n_surv) {
+  if (!s || !f || !p || !n_gen || !n_surv) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  SCR_CUDA(cudaMemcpyAsync(s->ws.depth, f->depth, WH * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->ws.rgb, f->rgb, WH * 3, cudaMemcpyHostToDevice, s->stream));
+  SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
+  const int zero = 0;
+  SCR_CUDA(cudaMemcpyAsync(s->ws.fidx, &zero, sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->ws.seeds, &seed, sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream));
+  scr_result* d_res = nullptr;
+  SCR_CUDA(cudaMalloc(&d_res, sizeof(scr_result)));
+  // raw mode still needs a model for the score; skip ICP work by using raw
+  const bool have_model = s->d_prims != nullptr;
+  if (!have_model) {
+    set_error("scr_debug_ransac: no scene model set");
+    cudaFree(d_res);
+    return SCR_E_ARG;
+  }
+  scr_status st = run_stage(s, 1, *p, SCR_MODE_RAW, d_res);
+  cudaFree(d_res);
+  if (st != SCR_OK) return st;
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  const int nmax = p->n_max;
+  std::vector<int> ok(nmax);
+  std::vector<Pose> hp(nmax);
+  SCR_CUDA(cudaMemcpy(ok.data(), s->ws.hok, nmax * sizeof(int), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(hp.data(), s->ws.hyp, nmax * sizeof(Pose), cudaMemcpyDeviceToHost));
+  int g = 0;
+  for (int i = 0; i < nmax; ++i)
+    if (ok[i]) {
+      if (gen_slots) gen_slots[g] = i;
+      if (gen_poses) std::memcpy(&gen_poses[g], &hp[i], sizeof(scr_pose));
+      ++g;
+    }
+  *n_gen = g;
+  int nc = 0;
+  SCR_CUDA(cudaMemcpy(&nc, s->ws.ncand, sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<Pose> cp(std::max(1, nc));
+  std::vector<int> cs(std::max(1, nc));
+  std::vector<float> ce(std::max(1, nc));
+  if (nc) {
+    SCR_CUDA(cudaMemcpy(cp.data(), s->ws.cand, nc * sizeof(Pose), cudaMemcpyDeviceToHost));
+    SCR_CUDA(cudaMemcpy(cs.data(), s->ws.cslot, nc * sizeof(int), cudaMemcpyDeviceToHost));
+    SCR_CUDA(cudaMemcpy(ce.data(), s->ws.cenergy, nc * sizeof(float), cudaMemcpyDeviceToHost));
+  }
+  for (int i = 0; i < nc; ++i) {
+    if (surv_slots) surv_slots[i] = cs[i];
+    if (surv_poses) std::memcpy(&surv_poses[i], &cp[i], sizeof(scr_pose));
+    if (surv_energy) surv_energy[i] = ce[i];
+  }
+  *n_surv = nc;
+  return g == 0 ? SCR_E_NO_HYPOTHESES : SCR_OK;
+}
+
+scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, scr_pose* out, int* converged,
+                         double* rms, double* inlier_frac, double* score) {
+  if (!s || !f || !init || !s->d_prims) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  SCR_TRY(ensure_ransac_ws(s, 1, 1, 1));
+  SCR_TRY(ensure_icp_ws(s, 1));
+  SCR_CUDA(cudaMemcpyAsync(s->ws.depth, f->depth, WH * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->ws.rgb, f->rgb, WH * 3, cudaMemcpyHostToDevice, s->stream));
+  SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
+  const int zero = 0, one = 1;
+  SCR_CUDA(cudaMemcpyAsync(s->ws.fidx, &zero, sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->ws.ncand, &one, sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->ws.cand, init, sizeof(Pose), cudaMemcpyHostToDevice, s->stream));
+  IcpArgs ia{s->ws.ncull_cap, 1, 1, 0, WH};
+  k_icp_score<<<1, 256, 0, s->stream>>>(ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand, s->ws.ncand,
+                                        s->ws.icp_map, s->ws.icp_pose, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl,
+                                        s->ws.icp_score);
+  SCR_CUDA(cudaGetLastError());
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  SCR_CUDA(cudaMemcpy(out, s->ws.icp_pose, sizeof(Pose), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(converged, s->ws.icp_conv, sizeof(int), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(rms, s->ws.icp_rms, sizeof(double), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(inlier_frac, s->ws.icp_inl, sizeof(double), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(score, s->ws.icp_score, sizeof(double), cudaMemcpyDeviceToHost));
+  return SCR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1207 @@
+// Scene lifetime, frame ingest (K0), forest traversal (K1), online adaptation
+// (K2 reservoir insertion, K3 Really Quick Shift) and the synthetic-scene renderer.
+//
+// Reference behaviour restated here (file:line into /root/reference):
+//   frame validity            proj/include/screloc/core.hpp:109-114
+//   compute_feature           proj/src/features.cpp:33-58
+//   sample_grid_pixels        proj/src/features.cpp:67-75
+//   Tree::find_leaf (lazy)    proj/include/screloc/forest.hpp:40-42, routing forest.hpp:21
+//   leaf_slot (tree-major)    proj/include/screloc/forest.hpp:74-79
+//   integrate_frame           SPEC.md:348-356 (source missing in the reference)
+//   reservoir_insert
+//   cluster_reservoir (RQS)
+//   update_leaves_round_robin SPEC.md:366-374
+//   clear_adaptation
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace scr {
+
+namespace {
+thread_local std::string g_err;
+}
+void set_error(const std::string& m) { g_err = m; }
+scr_status cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what;
+  return e == cudaErrorMemoryAllocation ? SCR_E_OOM : SCR_E_CUDA;
+}
+
+// =============================== K0: frame ingest ====================================
+// Packs f32 depth + RGB8 into an 8-byte texel {depth or 0, r | g<<8 | b<<16 | valid<<24}.
+// Invalid pixels carry zero depth and zero colour, which is exactly what a probe
+// landing on them contributes (features.cpp:43-56), so K1 needs one load per probe.
+__global__ void k_pack(const float* __restrict__ depth_base, const uint8_t* __restrict__ rgb_base,
+                       const int* __restrict__ idx, int WH, uint2* __restrict__ tex) {
+  const int f = blockIdx.y;
+  const size_t src = idx ? static_cast<size_t>(idx[f]) : static_cast<size_t>(f);
+  const float* dp = depth_base + src * WH;
+  const uint8_t* cp = rgb_base + src * WH * 3;
+  uint2* out = tex + static_cast<size_t>(f) * WH;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < WH; p += gridDim.x * blockDim.x) {
+    const float d = dp[p];
+    uint2 t = make_uint2(0u, 0u);
+    if (depth_valid(d)) {
+      t.x = __float_as_uint(d);
+      t.y = static_cast<uint32_t>(cp[3 * p]) | (static_cast<uint32_t>(cp[3 * p + 1]) << 8) |
+            (static_cast<uint32_t>(cp[3 * p + 2]) << 16) | (1u << 24);
+    }
+    out[p] = t;
+  }
+}
+
+// Order-preserving compaction of the valid 4-px grid (features.cpp:67-75), one CTA per frame.
+__global__ void __launch_bounds__(1024) k_grid(const uint2* __restrict__ tex, int W, int H, int gmax,
+                                               int* __restrict__ gcount, int* __restrict__ gpx) {
+  __shared__ int warp_tot[32];
+  __shared__ int base_s;
+  const int f = blockIdx.x;
+  const uint2* t = tex + static_cast<size_t>(f) * W * H;
+  const int gw = (W + 3) / 4, gh = (H + 3) / 4, total = gw * gh;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base_s = 0;
+  __syncthreads();
+  for (int chunk = 0; chunk < total; chunk += 1024) {
+    const int i = chunk + threadIdx.x;
+    int x = 0, y = 0;
+    bool v = false;
+    if (i < total) {
+      x = (i % gw) * 4;
+      y = (i / gw) * 4;
+      v = (t[static_cast<size_t>(y) * W + x].y >> 24) != 0u;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, v);
+    const int pre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) warp_tot[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+      int s = warp_tot[lane];
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, s, off);
+        if (lane >= off) s += o;
+      }
+      warp_tot[lane] = s;  // inclusive
+    }
+    __syncthreads();
+    const int wbase = wid ? warp_tot[wid - 1] : 0;
+    const int base = base_s;
+    if (v) gpx[static_cast<size_t>(f) * gmax + base + wbase + pre] = x | (y << 16);
+    __syncthreads();
+    if (threadIdx.x == 0) base_s = base + warp_tot[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) gcount[f] = base_s;
+}
+
+// =============================== K1: feature + forest traversal ========================
+// One thread per valid grid pixel. Per tree: lazy descent evaluating only the visited
+// features (forest.hpp:40-42): probe p + lround(delta / D(p)) (features.cpp:38-40), one
+// 8-byte texel gather per visited node, route right iff f >= tau (forest.hpp:21).
+// Also emits the f32 camera point (f64 backprojection, geometry.hpp:194-199) and the
+// number of predicted modes (union over trees).
+__global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, const uint2* __restrict__ tex,
+                                                const int* __restrict__ gcount, const int* __restrict__ gpx,
+                                                int gmax, int* __restrict__ gslot, int* __restrict__ gnm,
+                                                float4* __restrict__ gcam, const int* __restrict__ pcount) {
+  __shared__ short4 sspec[kFeatures];
+  for (int i = threadIdx.x; i < kFeatures; i += blockDim.x) sspec[i] = fv.specs[i];
+  __syncthreads();
+  const int f = blockIdx.y;
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= gcount[f]) return;
+  const size_t gidx = static_cast<size_t>(f) * gmax + gi;
+  const int px = gpx[gidx];
+  const int x = px & 0xffff, y = px >> 16;
+  const int W = g.W, H = g.H;
+  const uint2* T = tex + static_cast<size_t>(f) * W * H;
+  const uint2 c = T[y * W + x];
+  const float d = __uint_as_float(c.x);
+  int nm = 0;
+  for (int t = 0; t < fv.T; ++t) {
+    const int nb = fv.node_base[t];
+    int node = nb;
+    int leaf;
+    for (;;) {
+      const int4 nd = __ldg(&fv.nodes[node]);
+      if (nd.x < 0) {
+        leaf = nd.y;
+        break;
+      }
+      const short4 sp = sspec[nd.z];
+      const int qx = x + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.x), d)));
+      const int qy = y + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.y), d)));
+      uint2 pt = make_uint2(0u, 0u);
+      if (qx >= 0 && qx < W && qy >= 0 && qy < H) pt = T[qy * W + qx];
+      float v;
+      if (sp.z == 0) {
+        v = __fsub_rn(d, __uint_as_float(pt.x));
+      } else {
+        const int sh = 8 * sp.w;
+        v = __fsub_rn(static_cast<float>((c.y >> sh) & 255u), static_cast<float>((pt.y >> sh) & 255u));
+      }
+      node = nb + ((v >= __int_as_float(nd.w)) ? nd.y : nd.x);
+    }
+    const int slot = fv.leaf_base[t] + leaf;
+    gslot[gidx * fv.T + t] = slot;
+    if (pcount) nm += pcount[slot];
+  }
+  gnm[gidx] = nm;
+  const double dd = static_cast<double>(d);
+  const double X = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
+  const double Y = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
+  gcam[gidx] = make_float4(static_cast<float>(X), static_cast<float>(Y), static_cast<float>(dd), 0.0f);
+}
+
+// Debug: full 256-D feature vectors at given pixels (features.cpp:60-65).
+__global__ void k_features(ForestView fv, FrameGeom g, const uint2* __restrict__ tex, const int* __restrict__ px,
+                           int n, float* __restrict__ out) {
+  const int i = blockIdx.x;
+  const int k = threadIdx.x;
+  if (i >= n || k >= kFeatures) return;
+  const int x = px[i] & 0xffff, y = px[i] >> 16;
+  const int W = g.W, H = g.H;
+  const uint2 c = tex[y * W + x];
+  const float d = __uint_as_float(c.x);
+  const short4 sp = fv.specs[k];
+  if (!depth_valid(d)) {
+    out[static_cast<size_t>(i) * kFeatures + k] = __int_as_float(0x7fc00000);
+    return;
+  }
+  const int qx = x + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.x), d)));
+  const int qy = y + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.y), d)));
+  uint2 pt = make_uint2(0u, 0u);
+  if (qx >= 0 && qx < W && qy >= 0 && qy < H) pt = tex[qy * W + qx];
+  float v;
+  if (sp.z == 0) v = __fsub_rn(d, __uint_as_float(pt.x));
+  else v = __fsub_rn(static_cast<float>((c.y >> (8 * sp.w)) & 255u), static_cast<float>((pt.y >> (8 * sp.w)) & 255u));
+  out[static_cast<size_t>(i) * kFeatures + k] = v;
+}
+
+// =============================== K2: reservoir insertion ================================
+// Sequential Algorithm R made parallel and bit-exact: insertions of
+// one frame are grouped per leaf (count / scan / place), each insertion's rank inside its
+// leaf is its row-major pixel order, n = seen + rank, and the counter-based draw
+// j = uniform_int(n + 1) from Rng::stream(adapt_seed, slot << 32 | n) picks the target.
+// Among insertions of one frame hitting the same target slot the highest rank wins,
+// exactly as the sequential loop would overwrite it.
+__global__ void k_ins_count(const int* __restrict__ gslot, int items, unsigned* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < items) atomicAdd(&cnt[gslot[i]], 1u);
+}
+
+__global__ void __launch_bounds__(1024) k_scan(const unsigned* __restrict__ in, unsigned* __restrict__ out, int n,
+                                               unsigned* __restrict__ total) {
+  __shared__ unsigned s[1024];
+  const int per = (n + 1023) / 1024;
+  const int beg = threadIdx.x * per, end = min(n, beg + per);
+  unsigned acc = 0;
+  for (int i = beg; i < end; ++i) acc += in[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const unsigned v = threadIdx.x >= off ? s[threadIdx.x - off] : 0u;
+    __syncthreads();
+    s[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned run = threadIdx.x ? s[threadIdx.x - 1] : 0u;
+  for (int i = beg; i < end; ++i) {
+    out[i] = run;
+    run += in[i];
+  }
+  if (threadIdx.x == 1023) {
+    out[n] = s[1023];
+    if (total) *total = s[1023];
+  }
+}
+
+__global__ void k_ins_place(const int* __restrict__ gslot, int items, const unsigned* __restrict__ off,
+                            unsigned* __restrict__ cur, int* __restrict__ item_at) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= items) return;
+  const int slot = gslot[i];
+  item_at[off[slot] + atomicAdd(&cur[slot], 1u)] = i;
+}
+
+__global__ void k_ins_rank(const int* __restrict__ gslot, int T, const unsigned* __restrict__ total,
+                           const unsigned* __restrict__ off, const unsigned* __restrict__ cnt,
+                           const int* __restrict__ item_at, const uint32_t* __restrict__ seen, int kappa,
+                           uint64_t seed, int* __restrict__ tgt, int* __restrict__ rank) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= static_cast<int>(*total)) return;
+  const int item = item_at[p];
+  const int g = item / T;
+  const int slot = gslot[item];
+  const unsigned s0 = off[slot], sn = cnt[slot];
+  int r = 0;
+  for (unsigned q = s0; q < s0 + sn; ++q) r += (item_at[q] / T) < g;
+  const uint32_t n = seen[slot] + static_cast<uint32_t>(r);
+  int target;
+  if (n < static_cast<uint32_t>(kappa)) {
+    target = static_cast<int>(n);
+  } else {
+    Rng rng = rng_stream(seed, (static_cast<uint64_t>(slot) << 32) | n);
+    const uint64_t j = rng_uniform_int(rng, static_cast<uint64_t>(n) + 1);
+    target = j < static_cast<uint64_t>(kappa) ? static_cast<int>(j) : -1;
+  }
+  tgt[p] = target;
+  rank[p] = r;
+}
+
+__global__ void k_ins_commit(const int* __restrict__ gslot, int T, const unsigned* __restrict__ total,
+                             const unsigned* __restrict__ off, const unsigned* __restrict__ cnt,
+                             const int* __restrict__ item_at, const int* __restrict__ tgt,
+                             const int* __restrict__ rank, const int* __restrict__ gpx, const uint2* __restrict__ tex,
+                             FrameGeom g, Pose pose, int kappa, scr_entry* __restrict__ entries,
+                             uint32_t* __restrict__ seen) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= static_cast<int>(*total)) return;
+  const int item = item_at[p];
+  const int slot = gslot[item];
+  const unsigned s0 = off[slot], sn = cnt[slot];
+  const int my_t = tgt[p], my_r = rank[p];
+  if (my_r == 0) seen[slot] += sn;  // one writer per leaf; seen was read by k_ins_rank
+  if (my_t < 0) return;
+  for (unsigned q = s0; q < s0 + sn; ++q)
+    if (tgt[q] == my_t && rank[q] > my_r) return;  // a later insertion overwrites this one
+  const int gidx = item / T;
+  const int px = gpx[gidx];
+  const int x = px & 0xffff, y = px >> 16;
+  const uint2 c = tex[y * g.W + x];
+  const double dd = static_cast<double>(__uint_as_float(c.x));
+  const double pc[3] = {((static_cast<double>(x) - g.dcx) * dd) / g.dfx, ((static_cast<double>(y) - g.dcy) * dd) / g.dfy,
+                        dd};
+  double pw[3];
+  pose_apply(pose, pc, pw);
+  scr_entry e;
+  e.x = static_cast<float>(pw[0]);
+  e.y = static_cast<float>(pw[1]);
+  e.z = static_cast<float>(pw[2]);
+  e.r = static_cast<uint8_t>(c.y & 255u);
+  e.g = static_cast<uint8_t>((c.y >> 8) & 255u);
+  e.b = static_cast<uint8_t>((c.y >> 16) & 255u);
+  e.pad = 0;
+  entries[static_cast<size_t>(slot) * kappa + my_t] = e;
+}
+
+// =============================== K3: Really Quick Shift ==================================
+// One CTA per scheduled leaf; the reservoir (<= kappa entries) lives in shared memory.
+// density_i = sum_j exp(-|xi - xj|^2 / 2 sigma^2) (f64 accumulation in j order), link to
+// the nearest strictly-higher-density point within tau (ties: lower index), components by
+// pointer chasing, clusters of size >= min sorted by (size desc, root asc), top M_max,
+// mu / colour / Sigma + 1e-6 I in f64, Sigma^-1 and Sigma^-1/2 via 3x3 Jacobi.
+struct RqsParams {
+  float c;       // -1 / (2 sigma^2), rounded once on the host
+  float tau2;    // tau^2
+  int min_size, max_clusters, kappa;
+};
+
+__global__ void __launch_bounds__(256) k_rqs(const scr_entry* __restrict__ entries, const uint32_t* __restrict__ seen,
+                                             int64_t L, int64_t cursor, int nleaves, RqsParams rp,
+                                             int* __restrict__ pcount, ModeGeom* __restrict__ pgeom,
+                                             float4* __restrict__ pcol, float* __restrict__ pcov,
+                                             const scr_entry* __restrict__ single, int single_n,
+                                             int* __restrict__ labels_out) {
+  extern __shared__ unsigned char smem_raw[];
+  const int kappa = rp.kappa;
+  float* sx = reinterpret_cast<float*>(smem_raw);
+  float* sy = sx + kappa;
+  float* sz = sy + kappa;
+  uint32_t* scol = reinterpret_cast<uint32_t*>(sz + kappa);
+  double* rho = reinterpret_cast<double*>(scol + kappa);
+  int* parent = reinterpret_cast<int*>(rho + kappa);
+  int* root = parent + kappa;
+  int* size = root + kappa;
+  int* rlist = size + kappa;
+  __shared__ int nroots;
+
+  int64_t slot = 0;
+  int n;
+  const scr_entry* e;
+  if (single) {
+    e = single;
+    n = single_n;
+  } else {
+    slot = (cursor + blockIdx.x) % L;
+    n = static_cast<int>(min(seen[slot], static_cast<uint32_t>(kappa)));
+    e = entries + slot * kappa;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const scr_entry v = e[i];
+    sx[i] = v.x;
+    sy[i] = v.y;
+    sz[i] = v.z;
+    scol[i] = v.r | (v.g << 8) | (v.b << 16);
+    size[i] = 0;
+  }
+  if (threadIdx.x == 0) nroots = 0;
+  __syncthreads();
+  // density
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float xi = sx[i], yi = sy[i], zi = sz[i];
+    double acc = 0.0;
+    for (int j = 0; j < n; ++j) {
+      const float dx = __fsub_rn(xi, sx[j]), dy = __fsub_rn(yi, sy[j]), dz = __fsub_rn(zi, sz[j]);
+      const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+      acc = acc + static_cast<double>(det_expf(__fmul_rn(d2, rp.c)));
+    }
+    rho[i] = acc;
+  }
+  __syncthreads();
+  // link
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float xi = sx[i], yi = sy[i], zi = sz[i];
+    const double ri = rho[i];
+    float best = __int_as_float(0x7f800000);
+    int bj = -1;
+    for (int j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const double rj = rho[j];
+      if (!(rj > ri || (rj == ri && j < i))) continue;
+      const float dx = __fsub_rn(xi, sx[j]), dy = __fsub_rn(yi, sy[j]), dz = __fsub_rn(zi, sz[j]);
+      const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+      if (d2 <= rp.tau2 && d2 < best) {
+        best = d2;
+        bj = j;
+      }
+    }
+    parent[i] = bj;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int r = i;
+    while (parent[r] >= 0) r = parent[r];
+    root[i] = r;
+    atomicAdd(&size[r], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (parent[i] < 0 && size[i] >= rp.min_size) {
+      rlist[atomicAdd(&nroots, 1)] = i;
+    }
+  }
+  __syncthreads();
+  const int R = nroots;
+  // rank roots by (size desc, index asc); parent[] (no longer needed) becomes the
+  // root -> cluster map. rlist is only read here, so the ranking is race-free.
+  for (int i = threadIdx.x; i < n; i += blockDim.x) parent[i] = -1;
+  __syncthreads();
+  for (int q = threadIdx.x; q < R; q += blockDim.x) {
+    const int i = rlist[q];
+    const int si = size[i];
+    int rk = 0;
+    for (int u = 0; u < R; ++u) {
+      const int j = rlist[u];
+      rk += (size[j] > si) || (size[j] == si && j < i);
+    }
+    if (rk < rp.max_clusters) parent[i] = rk;
+  }
+  __syncthreads();
+  const int ncl = min(R, rp.max_clusters);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int lab = parent[root[i]];
+    if (labels_out) labels_out[i] = lab;
+    root[i] = lab;  // root[] now holds labels
+  }
+  __syncthreads();
+  if (threadIdx.x < ncl) {
+    const int k = threadIdx.x;
+    double sxm = 0, sym = 0, szm = 0, sr = 0, sg = 0, sb = 0;
+    int cnt = 0;
+    for (int i = 0; i < n; ++i) {
+      if (root[i] != k) continue;
+      sxm = sxm + static_cast<double>(sx[i]);
+      sym = sym + static_cast<double>(sy[i]);
+      szm = szm + static_cast<double>(sz[i]);
+      const uint32_t cc = scol[i];
+      sr = sr + static_cast<double>(cc & 255u);
+      sg = sg + static_cast<double>((cc >> 8) & 255u);
+      sb = sb + static_cast<double>((cc >> 16) & 255u);
+      ++cnt;
+    }
+    const double dn = static_cast<double>(cnt);
+    const double mx = sxm / dn, my = sym / dn, mz = szm / dn;
+    double c00 = 0, c01 = 0, c02 = 0, c11 = 0, c12 = 0, c22 = 0;
+    for (int i = 0; i < n; ++i) {
+      if (root[i] != k) continue;
+      const double dx = static_cast<double>(sx[i]) - mx, dy = static_cast<double>(sy[i]) - my,
+                   dz = static_cast<double>(sz[i]) - mz;
+      c00 = c00 + dx * dx; c01 = c01 + dx * dy; c02 = c02 + dx * dz;
+      c11 = c11 + dy * dy; c12 = c12 + dy * dz; c22 = c22 + dz * dz;
+    }
+    c00 = c00 / dn + 1e-6; c01 = c01 / dn; c02 = c02 / dn;
+    c11 = c11 / dn + 1e-6; c12 = c12 / dn; c22 = c22 / dn + 1e-6;
+    const double S[9] = {c00, c01, c02, c01, c11, c12, c02, c12, c22};
+    double lam[3], V[9];
+    eig3(S, lam, V);
+    double il[3], isl[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double l = lam[q] > 1e-12 ? lam[q] : 1e-12;
+      il[q] = 1.0 / l;
+      isl[q] = 1.0 / sqrt(l);
+    }
+#define SCR_FN(w, a, b) \
+  ((V[3 * (a) + 0] * w[0] * V[3 * (b) + 0] + V[3 * (a) + 1] * w[1] * V[3 * (b) + 1]) + V[3 * (a) + 2] * w[2] * V[3 * (b) + 2])
+    ModeGeom m;
+    m.q0 = make_float4(static_cast<float>(mx), static_cast<float>(my), static_cast<float>(mz),
+                       static_cast<float>(SCR_FN(il, 0, 0)));
+    m.q1 = make_float4(static_cast<float>(SCR_FN(il, 1, 1)), static_cast<float>(SCR_FN(il, 2, 2)),
+                       static_cast<float>(2.0 * SCR_FN(il, 0, 1)), static_cast<float>(2.0 * SCR_FN(il, 0, 2)));
+    m.q2 = make_float4(static_cast<float>(2.0 * SCR_FN(il, 1, 2)), static_cast<float>(SCR_FN(isl, 0, 0)),
+                       static_cast<float>(SCR_FN(isl, 0, 1)), static_cast<float>(SCR_FN(isl, 0, 2)));
+    m.q3 = make_float4(static_cast<float>(SCR_FN(isl, 1, 1)), static_cast<float>(SCR_FN(isl, 1, 2)),
+                       static_cast<float>(SCR_FN(isl, 2, 2)), 0.0f);
+#undef SCR_FN
+    const size_t mi = static_cast<size_t>(slot) * kMaxModes + k;
+    pgeom[mi] = m;
+    pcol[mi] = make_float4(static_cast<float>(sr / dn), static_cast<float>(sg / dn), static_cast<float>(sb / dn),
+                           __int_as_float(cnt));
+    float* cv = pcov + mi * 6;
+    cv[0] = static_cast<float>(c00); cv[1] = static_cast<float>(c01); cv[2] = static_cast<float>(c02);
+    cv[3] = static_cast<float>(c11); cv[4] = static_cast<float>(c12); cv[5] = static_cast<float>(c22);
+  }
+  if (threadIdx.x == 0) pcount[slot] = ncl;
+}
+
+// =============================== synthetic renderer (fixture) ==============================
+SCR_DEV uint32_t hash3(int x, int y, uint32_t seed) {
+  uint32_t h = static_cast<uint32_t>(x) * 73856093u ^ static_cast<uint32_t>(y) * 19349663u ^ seed;
+  h ^= h >> 16;
+  h *= 0x7feb352du;
+  h ^= h >> 15;
+  h *= 0x846ca68bu;
+  h ^= h >> 16;
+  return h;
+}
+
+__global__ void k_render(const Prim* __restrict__ prims, int nprims, FrameGeom g, const Pose* __restrict__ poses,
+                         float* __restrict__ depth, uint8_t* __restrict__ rgb) {
+  const int f = blockIdx.y;
+  const int WH = g.W * g.H;
+  float R[9], o[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(poses[f].R[i]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o[i] = static_cast<float>(poses[f].t[i]);
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < WH; p += gridDim.x * blockDim.x) {
+    const int x = p % g.W, y = p / g.W;
+    float d[3];
+    ray_dir(R, g.fx, g.fy, g.cx, g.cy, x, y, d);
+    const Hit h = raycast(prims, nprims, o, d);
+    const size_t idx = static_cast<size_t>(f) * WH + p;
+    if (h.prim < 0 || !(h.t <= kRenderMaxDepth)) {
+      depth[idx] = 0.0f;
+      rgb[3 * idx] = rgb[3 * idx + 1] = rgb[3 * idx + 2] = 0;
+      continue;
+    }
+    depth[idx] = h.t;
+    float q[3], n[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) q[i] = __fmaf_rn(h.t, d[i], o[i]);
+    hit_normal(prims, h.prim, h.face, q, n);
+    const float ax = fabsf(n[0]), ay = fabsf(n[1]), az = fabsf(n[2]);
+    const int dom = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);
+    const int u = dom == 0 ? 1 : 0, v = dom == 2 ? 1 : 2;
+    const Prim& pr = prims[h.prim];
+    const float inv = __fdiv_rn(1.0f, pr.cell);
+    const int iu = static_cast<int>(floorf(__fmul_rn(q[u], inv)));
+    const int iv = static_cast<int>(floorf(__fmul_rn(q[v], inv)));
+    const uint32_t hh = hash3(iu, iv, pr.tex_seed);
+    const float fct = __fadd_rn(0.35f, __fmul_rn(0.65f, __fdiv_rn(static_cast<float>(hh & 255u), 255.0f)));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float val = __fadd_rn(__fmul_rn(pr.colour[c], fct), 0.5f);
+      rgb[3 * idx + c] = static_cast<uint8_t>(min(255, max(0, static_cast<int>(val))));
+    }
+  }
+}
+
+}  // namespace scr
+
+using namespace scr;
+
+// =============================== host side ============================================
+ForestView scr_scene_s::forest_view() const {
+  ForestView v;
+  v.nodes = d_nodes;
+  v.specs = d_specs;
+  v.T = T;
+  for (int t = 0; t < kMaxTrees; ++t) {
+    v.node_base[t] = t < T ? node_base[t] : 0;
+    v.leaf_base[t] = t < T ? leaf_base[t] : 0;
+  }
+  return v;
+}
+
+namespace {
+template <typename T>
+bool rd(const uint8_t* d, size_t n, size_t& off, T* v) {
+  if (off + sizeof(T) > n) return false;
+  std::memcpy(v, d + off, sizeof(T));
+  off += sizeof(T);
+  return true;
+}
+scr_status malformed(const std::string& m) {
+  set_error("deserialize_forest: " + m);
+  return SCR_E_MALFORMED_DATA;
+}
+template <typename T>
+scr_status dalloc(T** p, size_t count) {
+  SCR_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, count) * sizeof(T)));
+  return SCR_OK;
+}
+#define SCR_TRY(x)                       \
+  do {                                   \
+    scr_status _s = (x);                 \
+    if (_s != SCR_OK) return _s;         \
+  } while (0)
+}  // namespace
+
+extern "C" {
+
+const char* scr_last_error(void) { return g_err.c_str(); }
+const char* scr_version(void) { return "screloc-b200 0.1 (sm_100a)"; }
+
+scr_status scr_device_open(int ordinal, scr_device* out) {
+  if (!out) return SCR_E_ARG;
+  int n = 0;
+  SCR_CUDA(cudaGetDeviceCount(&n));
+  if (ordinal < 0 || ordinal >= n) {
+    set_error("scr_device_open: no such device");
+    return SCR_E_ARG;
+  }
+  SCR_CUDA(cudaSetDevice(ordinal));
+  scr_device d = new scr_device_s();
+  d->ordinal = ordinal;
+  cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, ordinal);
+  *out = d;
+  return SCR_OK;
+}
+
+void scr_device_close(scr_device d) { delete d; }
+
+scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const scr_forest_params* fp,
+                            const scr_intrinsics* k, uint64_t adapt_seed, int max_batch, scr_scene* out) {
+  if (!dev || !blob || !fp || !k || !out || max_batch <= 0) {
+    set_error("scr_scene_create: null argument");
+    return SCR_E_ARG;
+  }
+  if (!(k->fx > 0 && k->fy > 0 && k->cx >= 0 && k->cx < k->width && k->cy >= 0 && k->cy < k->height)) {
+    set_error("scr_scene_create: invalid intrinsics (geometry.hpp:52-54)");
+    return SCR_E_ARG;
+  }
+  if (fp->capacity <= 0 || fp->capacity > 4096 || fp->max_clusters <= 0 || fp->max_clusters > kMaxModes) {
+    set_error("scr_scene_create: capacity must be in (0, 4096] and max_clusters in (0, 50]");
+    return SCR_E_ARG;
+  }
+  // ---- parse the forest (SPEC.md:300 layout; validation mirrors deserialize_forest) ----
+  size_t off = 0;
+  char magic[4];
+  for (int i = 0; i < 4; ++i)
+    if (!rd(blob, n, off, &magic[i])) return malformed("truncated at offset " + std::to_string(off));
+  if (magic[0] != 'S' || magic[1] != 'C' || magic[2] != 'R' || magic[3] != 'F') return malformed("bad magic");
+  uint32_t version, nt, ns;
+  if (!rd(blob, n, off, &version)) return malformed("truncated at offset " + std::to_string(off));
+  if (version != 1) return malformed("unsupported version " + std::to_string(version));
+  if (!rd(blob, n, off, &nt) || !rd(blob, n, off, &ns)) return malformed("truncated at offset " + std::to_string(off));
+  if (ns != kFeatures) return malformed("spec count " + std::to_string(ns));
+  if (nt == 0 || nt > static_cast<uint32_t>(kMaxTrees)) return malformed("tree count " + std::to_string(nt));
+  std::vector<short4> specs(kFeatures);
+  for (uint32_t i = 0; i < ns; ++i) {
+    uint8_t kind, ch;
+    int16_t dx, dy;
+    if (!rd(blob, n, off, &kind) || !rd(blob, n, off, &ch) || !rd(blob, n, off, &dx) || !rd(blob, n, off, &dy))
+      return malformed("truncated at offset " + std::to_string(off));
+    if (kind > 1 || ch > 2) return malformed("bad spec at offset " + std::to_string(off));
+    specs[i] = make_short4(dx, dy, kind, ch);
+  }
+  std::vector<int4> nodes;
+  std::vector<int> node_base, leaf_base;
+  int64_t L = 0;
+  for (uint32_t t = 0; t < nt; ++t) {
+    uint32_t nn;
+    int32_t leaves;
+    if (!rd(blob, n, off, &nn) || !rd(blob, n, off, &leaves)) return malformed("truncated at offset " + std::to_string(off));
+    if (nn == 0 || nn > (1u << 26) || leaves <= 0) return malformed("bad node count");
+    node_base.push_back(static_cast<int>(nodes.size()));
+    leaf_base.push_back(static_cast<int>(L));
+    const size_t first = nodes.size();
+    for (uint32_t i = 0; i < nn; ++i) {
+      int32_t feat, left, right, leaf;
+      float thr;
+      if (!rd(blob, n, off, &feat) || !rd(blob, n, off, &thr) || !rd(blob, n, off, &left) ||
+          !rd(blob, n, off, &right) || !rd(blob, n, off, &leaf))
+        return malformed("truncated at offset " + std::to_string(off));
+      int4 v;
+      if (left < 0) {
+        if (leaf < 0 || leaf >= leaves) return malformed("bad leaf id");
+        v = make_int4(-1, leaf, 0, 0);
+      } else {
+        if (left <= static_cast<int32_t>(i) || right <= static_cast<int32_t>(i) || left >= static_cast<int32_t>(nn) ||
+            right >= static_cast<int32_t>(nn) || feat < 0 || feat >= kFeatures)
+          return malformed("bad branch node " + std::to_string(i));
+        int tb;
+        std::memcpy(&tb, &thr, 4);
+        v = make_int4(left, right, feat, tb);
+      }
+      nodes.push_back(v);
+    }
+    (void)first;
+    L += leaves;
+  }
+  if (off != n) return malformed("trailing bytes at offset " + std::to_string(off));
+
+  SCR_CUDA(cudaSetDevice(dev->ordinal));
+  scr_scene s = new scr_scene_s();
+  s->dev = dev;
+  s->k = *k;
+  s->fp = *fp;
+  s->adapt_seed = adapt_seed;
+  s->T = static_cast<int>(nt);
+  s->L = L;
+  s->node_base = node_base;
+  s->leaf_base = leaf_base;
+  s->geom.W = k->width;
+  s->geom.H = k->height;
+  s->geom.fx = static_cast<float>(k->fx);
+  s->geom.fy = static_cast<float>(k->fy);
+  s->geom.cx = static_cast<float>(k->cx);
+  s->geom.cy = static_cast<float>(k->cy);
+  s->geom.dfx = k->fx;
+  s->geom.dfy = k->fy;
+  s->geom.dcx = k->cx;
+  s->geom.dcy = k->cy;
+  auto fail = [&](scr_status st) {
+    scr_scene_destroy(s);
+    return st;
+  };
+  cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
+  scr_status st;
+  if ((st = dalloc(&s->d_nodes, nodes.size())) != SCR_OK) return fail(st);
+  if ((st = dalloc(&s->d_specs, kFeatures)) != SCR_OK) return fail(st);
+  const size_t kappa = static_cast<size_t>(fp->capacity);
+  if ((st = dalloc(&s->d_entries, static_cast<size_t>(L) * kappa)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&s->d_seen, L)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&s->d_count, L)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&s->d_geom, static_cast<size_t>(L) * kMaxModes)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&s->d_col, static_cast<size_t>(L) * kMaxModes)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&s->d_cov, static_cast<size_t>(L) * kMaxModes * 6)) != SCR_OK) return fail(st);
+  e = cudaMemcpy(s->d_nodes, nodes.data(), nodes.size() * sizeof(int4), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "upload nodes"));
+  e = cudaMemcpy(s->d_specs, specs.data(), kFeatures * sizeof(short4), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "upload specs"));
+  // workspace
+  Workspace& w = s->ws;
+  w.cap = max_batch;
+  w.gmax = ((k->width + 3) / 4) * ((k->height + 3) / 4);
+  const size_t WH = static_cast<size_t>(k->width) * k->height;
+  const size_t B = static_cast<size_t>(max_batch);
+  if ((st = dalloc(&w.depth, B * WH)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.rgb, B * WH * 3)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.tex, B * WH)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.gcount, B)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.gpx, B * w.gmax)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.gcam, B * w.gmax)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.gslot, B * w.gmax * s->T)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.fidx, B)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.seeds, B)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.status, B)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.ins_cnt, L)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.ins_off, L + 1)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.ins_cur, L)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.ins_item, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.ins_tgt, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.ins_rank, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.ins_total, 1)) != SCR_OK) return fail(st);
+  if ((st = scr_reset(s)) != SCR_OK) return fail(st);
+  e = cudaFuncSetAttribute(k_rqs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "cudaFuncSetAttribute(k_rqs)"));
+  e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "scene create sync"));
+  *out = s;
+  return SCR_OK;
+}
+
+void scr_scene_destroy(scr_scene s) {
+  if (!s) return;
+  cudaSetDevice(s->dev->ordinal);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  void* ptrs[] = {s->d_nodes, s->d_specs, s->d_entries, s->d_seen, s->d_count, s->d_geom, s->d_col, s->d_cov,
+                  s->d_prims, s->ws.depth, s->ws.rgb, s->ws.tex, s->ws.gcount, s->ws.gpx, s->ws.gcam, s->ws.gslot,
+                  s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
+                  s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
+                  s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
+                  s->ws.status, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
+                  s->ws.ins_rank, s->ws.ins_total};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+int64_t scr_scene_total_leaves(scr_scene s) { return s ? s->L : 0; }
+void* scr_scene_stream(scr_scene s) { return s ? static_cast<void*>(s->stream) : nullptr; }
+int64_t scr_kernel_launches(scr_scene s) { return s ? s->launches : 0; }
+int64_t scr_update_cursor(scr_scene s) { return s ? s->cursor : 0; }
+
+scr_status scr_scene_set_analytic_model(scr_scene s, const scr_prim* prims, int n) {
+  if (!s || (!prims && n > 0) || n < 0) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  std::vector<Prim> p(n);
+  for (int i = 0; i < n; ++i) {
+    p[i].type = prims[i].type;
+    for (int q = 0; q < 3; ++q) {
+      p[i].a[q] = prims[i].a[q];
+      p[i].b[q] = prims[i].b[q];
+      p[i].colour[q] = prims[i].colour[q];
+    }
+    p[i].cell = prims[i].cell;
+    p[i].tex_seed = prims[i].tex_seed;
+    if (p[i].type != 0 && p[i].type != 1) {
+      set_error("scr_scene_set_analytic_model: unknown primitive type");
+      return SCR_E_ARG;
+    }
+  }
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  if (s->d_prims) SCR_CUDA(cudaFree(s->d_prims));
+  s->d_prims = nullptr;
+  s->n_prims = n;
+  if (n > 0) {
+    SCR_CUDA(cudaMalloc(&s->d_prims, n * sizeof(Prim)));
+    SCR_CUDA(cudaMemcpy(s->d_prims, p.data(), n * sizeof(Prim), cudaMemcpyHostToDevice));
+  }
+  return SCR_OK;
+}
+
+scr_status scr_reset(scr_scene s) {
+  if (!s) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_CUDA(cudaMemsetAsync(s->d_entries, 0, static_cast<size_t>(s->L) * s->fp.capacity * sizeof(scr_entry), s->stream));
+  SCR_CUDA(cudaMemsetAsync(s->d_seen, 0, s->L * sizeof(uint32_t), s->stream));
+  SCR_CUDA(cudaMemsetAsync(s->d_count, 0, s->L * sizeof(int), s->stream));
+  SCR_CUDA(cudaMemsetAsync(s->d_geom, 0, static_cast<size_t>(s->L) * kMaxModes * sizeof(ModeGeom), s->stream));
+  SCR_CUDA(cudaMemsetAsync(s->d_col, 0, static_cast<size_t>(s->L) * kMaxModes * sizeof(float4), s->stream));
+  SCR_CUDA(cudaMemsetAsync(s->d_cov, 0, static_cast<size_t>(s->L) * kMaxModes * 6 * sizeof(float), s->stream));
+  s->cursor = 0;
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  return SCR_OK;
+}
+
+}  // extern "C"
+
+namespace scr {
+
+// K0 + grid + K1 for n frames whose raw buffers are at depth_base/rgb_base (device)
+// selected by d_idx (or identity), into workspace slots 0..n-1.
+scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_base, const int* d_idx, int n) {
+  Workspace& w = s->ws;
+  const int W = s->k.width, H = s->k.height, WH = W * H;
+  k_pack<<<dim3((WH + 1023) / 1024 < 64 ? (WH + 1023) / 1024 : 64, n), 256, 0, s->stream>>>(depth_base, rgb_base,
+                                                                                            d_idx, WH, w.tex);
+  k_grid<<<n, 1024, 0, s->stream>>>(w.tex, W, H, w.gmax, w.gcount, w.gpx);
+  k_leaves<<<dim3((w.gmax + 127) / 128, n), 128, 0, s->stream>>>(s->forest_view(), s->geom, w.tex, w.gcount, w.gpx,
+                                                               w.gmax, w.gslot, w.gnm, w.gcam, s->d_count);
+  s->launches += 3;
+  SCR_CUDA(cudaGetLastError());
+  return SCR_OK;
+}
+
+}  // namespace scr
+
+namespace {
+scr_status upload_frames(scr_scene s, const scr_frame* frames, int n) {
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  for (int i = 0; i < n; ++i) {
+    if (!frames[i].depth || !frames[i].rgb) {
+      set_error("frame with null depth or colour");
+      return SCR_E_ARG;
+    }
+    SCR_CUDA(cudaMemcpyAsync(s->ws.depth + i * WH, frames[i].depth, WH * sizeof(float), cudaMemcpyHostToDevice,
+                             s->stream));
+    SCR_CUDA(cudaMemcpyAsync(s->ws.rgb + i * WH * 3, frames[i].rgb, WH * 3, cudaMemcpyHostToDevice, s->stream));
+  }
+  return SCR_OK;
+}
+
+// integrate_frame for the frame packed in workspace slot 0.
+scr_status integrate_slot0(scr_scene s, const scr_pose* pose) {
+  Workspace& w = s->ws;
+  const int T = s->T;
+  const int items_max = w.gmax * T;
+  int G = 0;
+  SCR_CUDA(cudaMemcpyAsync(&G, w.gcount, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  if (G == 0) return SCR_OK;
+  const int items = G * T;
+  (void)items_max;
+  SCR_CUDA(cudaMemsetAsync(w.ins_cnt, 0, s->L * sizeof(unsigned), s->stream));
+  SCR_CUDA(cudaMemsetAsync(w.ins_cur, 0, s->L * sizeof(unsigned), s->stream));
+  Pose P;
+  std::memcpy(P.R, pose->R, sizeof(P.R));
+  std::memcpy(P.t, pose->t, sizeof(P.t));
+  const int tb = 256, nb = (items + tb - 1) / tb;
+  k_ins_count<<<nb, tb, 0, s->stream>>>(w.gslot, items, w.ins_cnt);
+  k_scan<<<1, 1024, 0, s->stream>>>(w.ins_cnt, w.ins_off, static_cast<int>(s->L), w.ins_total);
+  k_ins_place<<<nb, tb, 0, s->stream>>>(w.gslot, items, w.ins_off, w.ins_cur, w.ins_item);
+  k_ins_rank<<<nb, tb, 0, s->stream>>>(w.gslot, T, w.ins_total, w.ins_off, w.ins_cnt, w.ins_item, s->d_seen,
+                                      s->fp.capacity, s->adapt_seed, w.ins_tgt, w.ins_rank);
+  k_ins_commit<<<nb, tb, 0, s->stream>>>(w.gslot, T, w.ins_total, w.ins_off, w.ins_cnt, w.ins_item, w.ins_tgt,
+                                        w.ins_rank, w.gpx, w.tex, s->geom, P, s->fp.capacity, s->d_entries,
+                                        s->d_seen);
+  s->launches += 5;
+  SCR_CUDA(cudaGetLastError());
+  return SCR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+scr_status scr_train(scr_scene s, const scr_frame* frame, const scr_pose* pose) { return scr_train_batch(s, frame, pose, 1); }
+
+scr_status scr_train_batch(scr_scene s, const scr_frame* frames, const scr_pose* poses, int n) {
+  if (!s || (!frames && n > 0) || (!poses && n > 0) || n < 0) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  for (int i = 0; i < n; ++i) {
+    if (!frames[i].pose_reliable) {
+      set_error("integrate_frame: pose flagged unreliable");
+      return SCR_E_UNRELIABLE_POSE;
+    }
+    SCR_TRY(upload_frames(s, &frames[i], 1));
+    SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
+    SCR_TRY(integrate_slot0(s, &poses[i]));
+  }
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  return SCR_OK;
+}
+
+scr_status scr_train_frameset(scr_scene s, scr_frameset fs, const int32_t* idx, const scr_pose* poses, int n) {
+  if (!s || !fs || (!idx && n > 0) || (!poses && n > 0)) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  for (int i = 0; i < n; ++i) {
+    if (idx[i] < 0 || idx[i] >= fs->cap) return SCR_E_ARG;
+    SCR_TRY(pack_frames(s, fs->depth + idx[i] * WH, fs->rgb + idx[i] * WH * 3, nullptr, 1));
+    SCR_TRY(integrate_slot0(s, &poses[i]));
+  }
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  return SCR_OK;
+}
+
+scr_status scr_update(scr_scene s, int64_t leaves_per_call) {
+  if (!s || leaves_per_call < 0) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const int64_t n = std::min<int64_t>(leaves_per_call, s->L);
+  if (n == 0) return SCR_OK;
+  RqsParams rp;
+  rp.c = static_cast<float>(-1.0 / (2.0 * static_cast<double>(s->fp.sigma) * static_cast<double>(s->fp.sigma)));
+  rp.tau2 = static_cast<float>(static_cast<double>(s->fp.tau) * static_cast<double>(s->fp.tau));
+  rp.min_size = s->fp.min_cluster_size;
+  rp.max_clusters = s->fp.max_clusters;
+  rp.kappa = s->fp.capacity;
+  const size_t smem = static_cast<size_t>(rp.kappa) * (4 * 4 + 8 + 4 * 4);
+  for (int64_t done = 0; done < n; done += 65535) {
+    const int chunk = static_cast<int>(std::min<int64_t>(65535, n - done));
+    k_rqs<<<chunk, 256, smem, s->stream>>>(s->d_entries, s->d_seen, s->L, (s->cursor + done) % s->L, chunk, rp,
+                                           s->d_count, s->d_geom, s->d_col, s->d_cov, nullptr, 0, nullptr);
+    s->launches += 1;
+  }
+  SCR_CUDA(cudaGetLastError());
+  s->cursor = (s->cursor + n) % s->L;
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  return SCR_OK;
+}
+
+scr_status scr_debug_cluster(scr_scene s, const scr_entry* e, int n, scr_mode* out, int32_t* labels, int* n_modes) {
+  if (!s || n < 0 || n > s->fp.capacity || !out || !n_modes) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  // run the production kernel on a scratch "leaf" 0 of a private prediction table
+  scr_entry* d_e = nullptr;
+  int* d_lab = nullptr;
+  int* d_cnt = nullptr;
+  ModeGeom* d_g = nullptr;
+  float4* d_c = nullptr;
+  float* d_v = nullptr;
+  SCR_CUDA(cudaMalloc(&d_e, std::max(1, n) * sizeof(scr_entry)));
+  SCR_CUDA(cudaMalloc(&d_lab, std::max(1, n) * sizeof(int)));
+  SCR_CUDA(cudaMalloc(&d_cnt, sizeof(int)));
+  SCR_CUDA(cudaMalloc(&d_g, kMaxModes * sizeof(ModeGeom)));
+  SCR_CUDA(cudaMalloc(&d_c, kMaxModes * sizeof(float4)));
+  SCR_CUDA(cudaMalloc(&d_v, kMaxModes * 6 * sizeof(float)));
+  if (n) SCR_CUDA(cudaMemcpy(d_e, e, n * sizeof(scr_entry), cudaMemcpyHostToDevice));
+  RqsParams rp;
+  rp.c = static_cast<float>(-1.0 / (2.0 * static_cast<double>(s->fp.sigma) * static_cast<double>(s->fp.sigma)));
+  rp.tau2 = static_cast<float>(static_cast<double>(s->fp.tau) * static_cast<double>(s->fp.tau));
+  rp.min_size = s->fp.min_cluster_size;
+  rp.max_clusters = s->fp.max_clusters;
+  rp.kappa = s->fp.capacity;
+  const size_t smem = static_cast<size_t>(rp.kappa) * (4 * 4 + 8 + 4 * 4);
+  k_rqs<<<1, 256, smem, s->stream>>>(nullptr, nullptr, 1, 0, 1, rp, d_cnt, d_g, d_c, d_v, d_e, n, d_lab);
+  SCR_CUDA(cudaGetLastError());
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  int cnt = 0;
+  SCR_CUDA(cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<ModeGeom> g(kMaxModes);
+  std::vector<float4> c(kMaxModes);
+  std::vector<float> v(kMaxModes * 6);
+  SCR_CUDA(cudaMemcpy(g.data(), d_g, kMaxModes * sizeof(ModeGeom), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(c.data(), d_c, kMaxModes * sizeof(float4), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(v.data(), d_v, kMaxModes * 6 * sizeof(float), cudaMemcpyDeviceToHost));
+  if (labels && n) SCR_CUDA(cudaMemcpy(labels, d_lab, n * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < cnt; ++i) {
+    scr_mode& m = out[i];
+    m.mu[0] = g[i].q0.x; m.mu[1] = g[i].q0.y; m.mu[2] = g[i].q0.z;
+    m.colour[0] = c[i].x; m.colour[1] = c[i].y; m.colour[2] = c[i].z;
+    for (int q = 0; q < 6; ++q) m.cov[q] = v[6 * i + q];
+    m.icov[0] = g[i].q0.w; m.icov[1] = g[i].q1.x; m.icov[2] = g[i].q1.y;
+    m.icov[3] = g[i].q1.z; m.icov[4] = g[i].q1.w; m.icov[5] = g[i].q2.x;
+    m.isqrt[0] = g[i].q2.y; m.isqrt[1] = g[i].q2.z; m.isqrt[2] = g[i].q2.w;
+    m.isqrt[3] = g[i].q3.x; m.isqrt[4] = g[i].q3.y; m.isqrt[5] = g[i].q3.z;
+    std::memcpy(&m.size, &c[i].w, 4);
+  }
+  *n_modes = cnt;
+  cudaFree(d_e); cudaFree(d_lab); cudaFree(d_cnt); cudaFree(d_g); cudaFree(d_c); cudaFree(d_v);
+  return SCR_OK;
+}
+
+scr_status scr_dump_seen(scr_scene s, uint32_t* out) {
+  if (!s || !out) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  SCR_CUDA(cudaMemcpy(out, s->d_seen, s->L * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return SCR_OK;
+}
+
+scr_status scr_dump_entries(scr_scene s, int64_t slot0, int64_t nslots, scr_entry* out) {
+  if (!s || !out || slot0 < 0 || nslots < 0 || slot0 + nslots > s->L) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  SCR_CUDA(cudaMemcpy(out, s->d_entries + slot0 * s->fp.capacity,
+                      static_cast<size_t>(nslots) * s->fp.capacity * sizeof(scr_entry), cudaMemcpyDeviceToHost));
+  return SCR_OK;
+}
+
+scr_status scr_dump_predictions(scr_scene s, int32_t* counts, scr_mode* modes) {
+  if (!s || !counts) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  SCR_CUDA(cudaMemcpy(counts, s->d_count, s->L * sizeof(int), cudaMemcpyDeviceToHost));
+  if (!modes) return SCR_OK;
+  const size_t M = static_cast<size_t>(s->L) * kMaxModes;
+  std::vector<ModeGeom> g(M);
+  std::vector<float4> c(M);
+  std::vector<float> v(M * 6);
+  SCR_CUDA(cudaMemcpy(g.data(), s->d_geom, M * sizeof(ModeGeom), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(c.data(), s->d_col, M * sizeof(float4), cudaMemcpyDeviceToHost));
+  SCR_CUDA(cudaMemcpy(v.data(), s->d_cov, M * 6 * sizeof(float), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < M; ++i) {
+    scr_mode& m = modes[i];
+    m.mu[0] = g[i].q0.x; m.mu[1] = g[i].q0.y; m.mu[2] = g[i].q0.z;
+    m.colour[0] = c[i].x; m.colour[1] = c[i].y; m.colour[2] = c[i].z;
+    for (int q = 0; q < 6; ++q) m.cov[q] = v[6 * i + q];
+    m.icov[0] = g[i].q0.w; m.icov[1] = g[i].q1.x; m.icov[2] = g[i].q1.y;
+    m.icov[3] = g[i].q1.z; m.icov[4] = g[i].q1.w; m.icov[5] = g[i].q2.x;
+    m.isqrt[0] = g[i].q2.y; m.isqrt[1] = g[i].q2.z; m.isqrt[2] = g[i].q2.w;
+    m.isqrt[3] = g[i].q3.x; m.isqrt[4] = g[i].q3.y; m.isqrt[5] = g[i].q3.z;
+    std::memcpy(&m.size, &c[i].w, 4);
+  }
+  return SCR_OK;
+}
+
+scr_status scr_load_predictions(scr_scene s, const int32_t* counts, const scr_mode* modes) {
+  if (!s || !counts || !modes) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t M = static_cast<size_t>(s->L) * kMaxModes;
+  std::vector<ModeGeom> g(M);
+  std::vector<float4> c(M);
+  std::vector<float> v(M * 6);
+  for (size_t i = 0; i < M; ++i) {
+    const scr_mode& m = modes[i];
+    g[i].q0 = make_float4(m.mu[0], m.mu[1], m.mu[2], m.icov[0]);
+    g[i].q1 = make_float4(m.icov[1], m.icov[2], m.icov[3], m.icov[4]);
+    g[i].q2 = make_float4(m.icov[5], m.isqrt[0], m.isqrt[1], m.isqrt[2]);
+    g[i].q3 = make_float4(m.isqrt[3], m.isqrt[4], m.isqrt[5], 0.0f);
+    float sz;
+    std::memcpy(&sz, &m.size, 4);
+    c[i] = make_float4(m.colour[0], m.colour[1], m.colour[2], sz);
+    for (int q = 0; q < 6; ++q) v[6 * i + q] = m.cov[q];
+  }
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  SCR_CUDA(cudaMemcpy(s->d_count, counts, s->L * sizeof(int), cudaMemcpyHostToDevice));
+  SCR_CUDA(cudaMemcpy(s->d_geom, g.data(), M * sizeof(ModeGeom), cudaMemcpyHostToDevice));
+  SCR_CUDA(cudaMemcpy(s->d_col, c.data(), M * sizeof(float4), cudaMemcpyHostToDevice));
+  SCR_CUDA(cudaMemcpy(s->d_cov, v.data(), M * 6 * sizeof(float), cudaMemcpyHostToDevice));
+  return SCR_OK;
+}
+
+size_t scr_predictions_bytes(scr_scene s) {
+  if (!s) return 0;
+  const size_t M = static_cast<size_t>(s->L) * kMaxModes;
+  return s->L * sizeof(int) + M * (sizeof(ModeGeom) + sizeof(float4) + 6 * sizeof(float));
+}
+
+scr_status scr_predictions_export(scr_scene s, void* dst) {
+  if (!s || !dst) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t M = static_cast<size_t>(s->L) * kMaxModes;
+  char* p = static_cast<char*>(dst);
+  SCR_CUDA(cudaMemcpyAsync(p, s->d_count, s->L * sizeof(int), cudaMemcpyDeviceToDevice, s->stream));
+  p += s->L * sizeof(int);
+  SCR_CUDA(cudaMemcpyAsync(p, s->d_geom, M * sizeof(ModeGeom), cudaMemcpyDeviceToDevice, s->stream));
+  p += M * sizeof(ModeGeom);
+  SCR_CUDA(cudaMemcpyAsync(p, s->d_col, M * sizeof(float4), cudaMemcpyDeviceToDevice, s->stream));
+  p += M * sizeof(float4);
+  SCR_CUDA(cudaMemcpyAsync(p, s->d_cov, M * 6 * sizeof(float), cudaMemcpyDeviceToDevice, s->stream));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  return SCR_OK;
+}
+
+scr_status scr_predictions_import(scr_scene s, const void* src) {
+  if (!s || !src) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t M = static_cast<size_t>(s->L) * kMaxModes;
+  const char* p = static_cast<const char*>(src);
+  SCR_CUDA(cudaMemcpyAsync(s->d_count, p, s->L * sizeof(int), cudaMemcpyDeviceToDevice, s->stream));
+  p += s->L * sizeof(int);
+  SCR_CUDA(cudaMemcpyAsync(s->d_geom, p, M * sizeof(ModeGeom), cudaMemcpyDeviceToDevice, s->stream));
+  p += M * sizeof(ModeGeom);
+  SCR_CUDA(cudaMemcpyAsync(s->d_col, p, M * sizeof(float4), cudaMemcpyDeviceToDevice, s->stream));
+  p += M * sizeof(float4);
+  SCR_CUDA(cudaMemcpyAsync(s->d_cov, p, M * 6 * sizeof(float), cudaMemcpyDeviceToDevice, s->stream));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  return SCR_OK;
+}
+
+scr_status scr_debug_leaves(scr_scene s, const scr_frame* f, int32_t* grid_px, int32_t* leaves, int* n_grid) {
+  if (!s || !f || !n_grid) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(upload_frames(s, f, 1));
+  SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
+  int G = 0;
+  SCR_CUDA(cudaMemcpyAsync(&G, s->ws.gcount, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  *n_grid = G;
+  if (grid_px) SCR_CUDA(cudaMemcpy(grid_px, s->ws.gpx, G * sizeof(int), cudaMemcpyDeviceToHost));
+  if (leaves) {
+    std::vector<int> sl(static_cast<size_t>(G) * s->T);
+    if (G) SCR_CUDA(cudaMemcpy(sl.data(), s->ws.gslot, sl.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int g = 0; g < G; ++g)
+      for (int t = 0; t < s->T; ++t) leaves[g * s->T + t] = sl[g * s->T + t] - s->leaf_base[t];
+  }
+  return SCR_OK;
+}
+
+scr_status scr_debug_features(scr_scene s, const scr_frame* f, const int32_t* px, int n, float* out) {
+  if (!s || !f || !px || !out || n < 0) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(upload_frames(s, f, 1));
+  SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
+  int* d_px = nullptr;
+  float* d_out = nullptr;
+  SCR_CUDA(cudaMalloc(&d_px, std::max(1, n) * sizeof(int)));
+  SCR_CUDA(cudaMalloc(&d_out, std::max(1, n) * kFeatures * sizeof(float)));
+  SCR_CUDA(cudaMemcpy(d_px, px, n * sizeof(int), cudaMemcpyHostToDevice));
+  if (n) k_features<<<n, kFeatures, 0, s->stream>>>(s->forest_view(), s->geom, s->ws.tex, d_px, n, d_out);
+  SCR_CUDA(cudaGetLastError());
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  SCR_CUDA(cudaMemcpy(out, d_out, static_cast<size_t>(n) * kFeatures * sizeof(float), cudaMemcpyDeviceToHost));
+  cudaFree(d_px);
+  cudaFree(d_out);
+  for (int i = 0; i < n; ++i) {
+    const int x = px[i] & 0xffff, y = px[i] >> 16;
+    if (x >= s->k.width || y >= s->k.height) {
+      set_error("compute_feature: pixel out of bounds");
+      return SCR_E_INVALID_CENTRE_PIXEL;
+    }
+    const float d = f->depth[static_cast<size_t>(y) * s->k.width + x];
+    if (!(d > 0.0f && d <= kMaxValidDepth)) {
+      set_error("compute_feature: invalid depth at centre pixel");
+      return SCR_E_INVALID_CENTRE_PIXEL;
+    }
+  }
+  return SCR_OK;
+}
+
+// ---- frame sets ----
+scr_status scr_frameset_create(scr_scene s, int cap, scr_frameset* out) {
+  if (!s || cap <= 0 || !out) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  scr_frameset fs = new scr_frameset_s();
+  fs->scene = s;
+  fs->cap = cap;
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  cudaError_t e = cudaMalloc(&fs->depth, cap * WH * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&fs->rgb, cap * WH * 3);
+  if (e != cudaSuccess) {
+    scr_frameset_destroy(fs);
+    return cuda_fail(e, "scr_frameset_create");
+  }
+  *out = fs;
+  return SCR_OK;
+}
+
+void scr_frameset_destroy(scr_frameset fs) {
+  if (!fs) return;
+  cudaSetDevice(fs->scene->dev->ordinal);
+  cudaStreamSynchronize(fs->scene->stream);
+  if (fs->depth) cudaFree(fs->depth);
+  if (fs->rgb) cudaFree(fs->rgb);
+  delete fs;
+}
+
+scr_status scr_frameset_upload(scr_frameset fs, int first, const scr_frame* frames, int n) {
+  if (!fs || first < 0 || n < 0 || first + n > fs->cap) return SCR_E_ARG;
+  scr_scene s = fs->scene;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  for (int i = 0; i < n; ++i) {
+    SCR_CUDA(cudaMemcpyAsync(fs->depth + (first + i) * WH, frames[i].depth, WH * sizeof(float), cudaMemcpyHostToDevice,
+                             s->stream));
+    SCR_CUDA(cudaMemcpyAsync(fs->rgb + (first + i) * WH * 3, frames[i].rgb, WH * 3, cudaMemcpyHostToDevice, s->stream));
+  }
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  return SCR_OK;
+}
+
+scr_status scr_frameset_render(scr_frameset fs, int first, const scr_pose* poses, int n) {
+  if (!fs || first < 0 || n < 0 || first + n > fs->cap || !poses) return SCR_E_ARG;
+  scr_scene s = fs->scene;
+  if (!s->d_prims) {
+    set_error("scr_frameset_render: no analytic model set");
+    return SCR_E_ARG;
+  }
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  Pose* d_p = nullptr;
+  SCR_CUDA(cudaMalloc(&d_p, std::max(1, n) * sizeof(Pose)));
+  SCR_CUDA(cudaMemcpy(d_p, poses, n * sizeof(Pose), cudaMemcpyHostToDevice));
+  for (int c0 = 0; c0 < n; c0 += 65535) {
+    const int c = std::min(65535, n - c0);
+    k_render<<<dim3(64, c), 256, 0, s->stream>>>(s->d_prims, s->n_prims, s->geom, d_p + c0,
+                                                 fs->depth + (first + c0) * WH, fs->rgb + (first + c0) * WH * 3);
+  }
+  SCR_CUDA(cudaGetLastError());
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  cudaFree(d_p);
+  return SCR_OK;
+}
+
+scr_status scr_frameset_download(scr_frameset fs, int first, int n, float* depth, uint8_t* rgb) {
+  if (!fs || first < 0 || n < 0 || first + n > fs->cap) return SCR_E_ARG;
+  scr_scene s = fs->scene;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  if (depth) SCR_CUDA(cudaMemcpy(depth, fs->depth + first * WH, n * WH * sizeof(float), cudaMemcpyDeviceToHost));
+  if (rgb) SCR_CUDA(cudaMemcpy(rgb, fs->rgb + first * WH * 3, n * WH * 3, cudaMemcpyDeviceToHost));
+  return SCR_OK;
+}
+
+}  // extern "C"
