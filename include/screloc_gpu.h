@@ -171,6 +171,12 @@ scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, 
                          double* rms, double* inlier_frac, double* score);
 /* number of kernel launches issued by this scene so far (bench accounting) */
 int64_t scr_kernel_launches(scr_scene s);
+/* in-library profiler: CUDA events bracket every launch on the scene stream; reset on enable */
+scr_status scr_profile_enable(scr_scene s, int enable);
+/* per-kernel totals since the last enable: names, device ms, launches (arrays of `cap`);
+ * work[7] = {mode evals, sample evals, LM terms, ICP terms, rays, node visits, generation
+ * attempts}; returns the number of kernel kinds */
+int scr_profile_read(scr_scene s, const char** names, double* ms, int64_t* launches, uint64_t* work, int cap);
 
 #ifdef __cplusplus
 }

@@ -477,3 +477,38 @@ int or_grid_count(void* fp, void* sp, const float* depth, const uint8_t* rgb, co
   });
 }
 }
+
+extern "C" {
+// n consecutive integrate_frame calls; per frame the forest descent runs in parallel over
+// grid pixels, the reservoir insertions stay in the sequential (pixel, tree) order.
+int or_integrate_batch(void* sp, void* fp, const float* depth, const uint8_t* rgb, const or_intrinsics* k,
+                       const or_pose* poses, int n, int threads) {
+  return guarded([&] {
+    AdaptState& s = *static_cast<AdaptState*>(sp);
+    const Forest& f = *static_cast<Forest*>(fp);
+    const size_t px = static_cast<size_t>(k->width) * k->height;
+    const int T = static_cast<int>(f.trees.size());
+    for (int i = 0; i < n; ++i) {
+      const Frame fr = mk_frame(depth + px * i, rgb + 3 * px * i, *k, 1);
+      const Pose pose = to_pose(poses[i].R, poses[i].t);
+      const std::vector<int> grid = sample_grid_pixels(fr, 4);
+      std::vector<int32_t> leaves(grid.size() * T);
+      parallel_for(static_cast<int>(grid.size()), threads, [&](int g) {
+        for (int t = 0; t < T; ++t)
+          leaves[static_cast<size_t>(g) * T + t] = find_leaf(f.trees[t], fr, grid[g] & 0xffff, grid[g] >> 16, f.specs);
+      });
+      for (size_t g = 0; g < grid.size(); ++g) {
+        const int x = grid[g] & 0xffff, y = grid[g] >> 16;
+        const size_t idx = static_cast<size_t>(y) * fr.width + x;
+        double pc[3], pw[3];
+        backproject(x, y, static_cast<double>(fr.depth[idx]), fr.k, pc);
+        transform_point(pose, pc, pw);
+        const Entry e{static_cast<float>(pw[0]), static_cast<float>(pw[1]), static_cast<float>(pw[2]),
+                      fr.rgb[3 * idx], fr.rgb[3 * idx + 1], fr.rgb[3 * idx + 2], 0};
+        for (int t = 0; t < T; ++t) reservoir_insert(s, f.leaf_base[t] + leaves[g * T + t], e);
+      }
+    }
+    return 0;
+  });
+}
+}

@@ -169,6 +169,8 @@ class Oracle:
             "or_energy": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(Pose), P(i32), C.c_int, P(flt)]),
             "or_lm": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(Pose), P(i32), C.c_int, C.c_int,
                                 P(dbl)]),
+            "or_integrate_batch": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(Pose), C.c_int,
+                                             C.c_int]),
             "or_grid_count": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(i32), C.c_int]),
         }
         for name, (res, args) in sig.items():

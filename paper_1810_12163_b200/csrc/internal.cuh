@@ -18,6 +18,29 @@ scr_status cuda_fail(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ::scr::cuda_fail(_e, #expr);   \
   } while (0)
 
+// ---- in-library profiler: CUDA events around every launch on the scene stream --------
+enum KernelId {
+  K_PACK, K_GRID, K_LEAVES, K_HYPGEN, K_SAMPLES, K_ENERGY, K_SELECT, K_LM, K_ICP, K_FINALIZE, K_INSERT, K_RQS,
+  K_RENDER, K_COUNT
+};
+// device work counters (u64), indexed by W_*; meaning documented in DESIGN.md "Roofline"
+enum WorkId {
+  W_MODE_EVALS, W_SAMPLE_EVALS, W_LM_TERMS, W_ICP_TERMS, W_RAYS, W_NODE_VISITS, W_GEN_ATTEMPTS, W_LM_ASSOC, W_COUNT
+};
+
+struct Profiler {
+  bool on = false;
+  struct Rec {
+    int kid;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[K_COUNT] = {};
+  long long launches[K_COUNT] = {};
+  unsigned long long* d_work = nullptr;
+};
+
 struct ForestView {
   const int4* nodes;     // {left, right|leaf_id, feature, threshold bits}; left < 0 marks a leaf
   const short4* specs;   // {dx, dy, kind, channel}
@@ -113,6 +136,7 @@ struct scr_scene_s {
   int n_prims = 0;
   scr::Workspace ws;
   int64_t launches = 0;
+  scr::Profiler prof;
   scr::ForestView forest_view() const;
   scr::PredView pred_view() const { return {d_count, d_geom, d_col}; }
 };
@@ -125,6 +149,28 @@ struct scr_frameset_s {
 };
 
 namespace scr {
+cudaEvent_t prof_event(scr_scene s);
+void prof_flush(scr_scene s);
+inline unsigned long long* work_ptr(scr_scene s) { return s->prof.on ? s->prof.d_work : nullptr; }
+
+// Launch wrapper: counts every launch and, when profiling, brackets it with events.
+#define SCR_LAUNCH(s, kid, ...)                                   \
+  do {                                                            \
+    cudaEvent_t _ea = nullptr, _eb = nullptr;                     \
+    if ((s)->prof.on) {                                           \
+      _ea = ::scr::prof_event(s);                                 \
+      _eb = ::scr::prof_event(s);                                 \
+      cudaEventRecord(_ea, (s)->stream);                          \
+    }                                                             \
+    __VA_ARGS__;                                                  \
+    if ((s)->prof.on) {                                           \
+      cudaEventRecord(_eb, (s)->stream);                          \
+      (s)->prof.pending.push_back({(kid), _ea, _eb});             \
+    }                                                             \
+    (s)->launches++;                                              \
+    (s)->prof.launches[(kid)]++;                                  \
+  } while (0)
+
 // scene.cu
 scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_base, const int* d_idx, int n);
 scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int samples);

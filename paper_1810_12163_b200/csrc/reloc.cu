@@ -56,7 +56,8 @@ SCR_DEV int mode_index(const FrameRefs& fr, const int* pcount, size_t gbase, int
 // max_iters. Draw order and checks follow DESIGN.md A1/A7.
 __global__ void __launch_bounds__(128) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
                                                 const uint64_t* __restrict__ seeds, Pose* __restrict__ hyp,
-                                                int* __restrict__ hok, int* __restrict__ hiters) {
+                                                int* __restrict__ hok, int* __restrict__ hiters,
+                                                unsigned long long* __restrict__ work) {
   const int a = blockIdx.y;
   const int slot = blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= gp.nmax) return;
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(128) k_hypgen(GenParams gp, FrameGeom g, Frame
   if (ok) hyp[out] = T;
   hok[out] = ok;
   hiters[out] = ok ? it + 1 : gp.max_iters;
+  if (work) atomicAdd(&work[W_GEN_ATTEMPTS], static_cast<unsigned long long>(ok ? it + 1 : (G > 0 ? gp.max_iters : 0)));
 }
 
 // Sample batch k of frame a: eta draws of uniform_int(G) from Rng::stream(seed, nmax + k).
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(128) k_energy(FrameRefs fr, PredView pv, const
                                                 const int* __restrict__ ok, int stride,
                                                 const int* __restrict__ nper, int min_n,
                                                 const int* __restrict__ samples, int scap, int ns,
-                                                float* __restrict__ out) {
+                                                float* __restrict__ out, unsigned long long* __restrict__ work) {
   const int a = blockIdx.y;
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = nper ? nper[a] : stride;
@@ -178,10 +180,13 @@ __global__ void __launch_bounds__(128) k_energy(FrameRefs fr, PredView pv, const
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
   const int* smp = samples + static_cast<size_t>(a) * scap;
   float E = 0.0f;
+  unsigned long long evals = 0, sevals = 0;
   for (int s = 0; s < ns; ++s) {
     const int gi = smp[s];
     const size_t gb = fbase + gi;
     if (fr.gnm[gb] == 0) continue;
+    evals += fr.gnm[gb];
+    ++sevals;
     const float4 c = fr.gcam[gb];
     float y[3];
     xform_f32(R, t, c.x, c.y, c.z, y);
@@ -200,6 +205,10 @@ __global__ void __launch_bounds__(128) k_energy(FrameRefs fr, PredView pv, const
     E = __fadd_rn(E, __fsqrt_rn(fmaxf(qmin, 0.0f)));
   }
   out[idx] = E;
+  if (work) {
+    atomicAdd(&work[W_MODE_EVALS], evals);
+    atomicAdd(&work[W_SAMPLE_EVALS], sevals);
+  }
 }
 
 // ================================ K7: cull / halving ========================================
@@ -330,7 +339,7 @@ SCR_DEV void lm_accum(const Pose& H, const double x[3], const ModeGeom& mg, bool
 
 __global__ void __launch_bounds__(128) k_lm(FrameRefs fr, PredView pv, LmArgs la, const int* __restrict__ samples,
                                             Pose* __restrict__ cand, const int* __restrict__ ncand,
-                                            int* __restrict__ assoc) {
+                                            int* __restrict__ assoc, unsigned long long* __restrict__ work) {
   const int a = blockIdx.y;
   const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -353,6 +362,7 @@ __global__ void __launch_bounds__(128) k_lm(FrameRefs fr, PredView pv, LmArgs la
       for (int i = lane; i < la.ns; i += 32) {
         const size_t gb = fbase + smp[i];
         int best_m = -1;
+        if (work && fr.gnm[gb] > 0) atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(fr.gnm[gb]));
         if (fr.gnm[gb] > 0) {
           const float4 c = fr.gcam[gb];
           float y[3];
@@ -387,13 +397,16 @@ __global__ void __launch_bounds__(128) k_lm(FrameRefs fr, PredView pv, LmArgs la
     double acc[28];
 #pragma unroll
     for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+    int terms = 0;
     for (int i = lane; i < la.ns; i += 32) {
       const int mi = as[i];
       if (mi < 0) continue;
       const float4 c = fr.gcam[fbase + smp[i]];
       const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
       lm_accum(H, x, pv.geom[mi], la.use_cov != 0, acc, true);
+      ++terms;
     }
+    if (work) atomicAdd(&work[W_LM_TERMS], static_cast<unsigned long long>(terms));
 #pragma unroll
     for (int k = 0; k < 28; ++k) acc[k] = warp_sum_xor(acc[k]);
     const double E = acc[27];
@@ -486,7 +499,7 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
                                                    const int* __restrict__ ncand, uint2* __restrict__ maps,
                                                    Pose* __restrict__ out_pose, int* __restrict__ out_conv,
                                                    double* __restrict__ out_rms, double* __restrict__ out_inl,
-                                                   double* __restrict__ out_score) {
+                                                   double* __restrict__ out_score, unsigned long long* __restrict__ work) {
   __shared__ double red[kLanes / 32][32];
   __shared__ double tot[32];
   __shared__ int ired[kLanes / 32];
@@ -525,6 +538,7 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
         ti[i] = static_cast<float>(Tinv.t[i]);
       }
       // K8: model map of this level at the reference pose
+      if (work && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(Wl * Hl));
       for (int p = threadIdx.x; p < Wl * Hl; p += blockDim.x) {
         float d[3];
         ray_dir(Rr, fxl, fyl, cxl, cyl, p % Wl, p / Wl, d);
@@ -600,6 +614,7 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
         block_reduce_f32<28>(acc, red, tot);
         const int inl_t = block_isum(inl, ired);
         const int valid_t = block_isum(valid, ired);
+        if (work && threadIdx.x == 0) atomicAdd(&work[W_ICP_TERMS], static_cast<unsigned long long>(valid_t));
         if (level == 0) {
           last_inl = inl_t;
           last_valid = valid_t;
@@ -662,6 +677,7 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
     for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(Tf.t[i]);
     float sum = 0.0f;
     int mutual = 0, synth = 0;
+    if (work && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(g.W * g.H));
     for (int p = threadIdx.x; p < g.W * g.H; p += blockDim.x) {
       float d[3];
       ray_dir(R, g.fx, g.fy, g.cx, g.cy, p % g.W, p / g.W, d);
@@ -795,39 +811,45 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   const FrameRefs fr = frame_refs(s);
   const PredView pv = s->pred_view();
   GenParams gp{p.max_gen_iters, p.n_max, p.min_sq_dist, p.colour_thresh, p.rigidity_tol};
-  k_hypgen<<<dim3((p.n_max + 127) / 128, nA), 128, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds, w.hyp, w.hok,
-                                                                     w.hiters);
-  k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, 0, w.samples_cap, w.samples);
-  k_energy<<<dim3((p.n_max + 127) / 128, nA), 128, 0, s->stream>>>(fr, pv, w.hyp, w.hok, p.n_max, nullptr, -1,
-                                                                     w.samples, w.samples_cap, p.eta, w.henergy);
+  unsigned long long* wk = work_ptr(s);
+  SCR_LAUNCH(s, K_HYPGEN,
+             (k_hypgen<<<dim3((p.n_max + 127) / 128, nA), 128, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds, w.hyp,
+                                                                              w.hok, w.hiters, wk)));
+  SCR_LAUNCH(s, K_SAMPLES,
+             (k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, 0, w.samples_cap,
+                                                                   w.samples)));
+  SCR_LAUNCH(s, K_ENERGY,
+             (k_energy<<<dim3((p.n_max + 127) / 128, nA), 128, 0, s->stream>>>(
+                 fr, pv, w.hyp, w.hok, p.n_max, nullptr, -1, w.samples, w.samples_cap, p.eta, w.henergy, wk)));
   int P = 1;
   while (P < p.n_max) P <<= 1;
-  k_select<<<nA, 1024, P * sizeof(unsigned long long), s->stream>>>(w.hyp, w.henergy, w.hok, nullptr, p.n_max,
-                                                                    nullptr, p.n_max, p.n_cull, p.n_out, 0, w.cand,
-                                                                    w.cenergy, w.cslot, w.ncand, w.ncull_cap);
-  s->launches += 4;
+  SCR_LAUNCH(s, K_SELECT,
+             (k_select<<<nA, 1024, P * sizeof(unsigned long long), s->stream>>>(
+                 w.hyp, w.henergy, w.hok, nullptr, p.n_max, nullptr, p.n_max, p.n_cull, p.n_out, 0, w.cand,
+                 w.cenergy, w.cslot, w.ncand, w.ncull_cap)));
   LmArgs la{0, w.samples_cap, w.ncull_cap, p.n_out, p.use_cov};
   for (int k = 1; k <= K; ++k) {
-    k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, k, w.samples_cap,
-                                                         w.samples);
+    SCR_LAUNCH(s, K_SAMPLES,
+               (k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, k,
+                                                                     w.samples_cap, w.samples)));
     const int ns = p.eta * (k + 1);
     if (p.pose_update) {
       la.ns = ns;
-      k_lm<<<dim3((p.n_cull + 3) / 4, nA), 128, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, w.assoc);
-      s->launches += 1;
+      SCR_LAUNCH(s, K_LM,
+                 (k_lm<<<dim3((p.n_cull + 3) / 4, nA), 128, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand,
+                                                                            w.assoc, wk)));
     }
-    // rescore (only frames still above n_out take part; others keep their energies)
-    k_energy<<<dim3((p.n_cull + 127) / 128, nA), 128, 0, s->stream>>>(fr, pv, w.cand, nullptr, w.ncull_cap, w.ncand,
-                                                                        p.n_out, w.samples, w.samples_cap, ns,
-                                                                        w.henergy);
-    // henergy is used as scratch [nA * ncull_cap] for the rescored energies
+    // rescore (only frames still above n_out take part); henergy is scratch [nA * ncull_cap]
+    SCR_LAUNCH(s, K_ENERGY,
+               (k_energy<<<dim3((p.n_cull + 127) / 128, nA), 128, 0, s->stream>>>(
+                   fr, pv, w.cand, nullptr, w.ncull_cap, w.ncand, p.n_out, w.samples, w.samples_cap, ns, w.henergy,
+                   wk)));
     int Pc = 1;
     while (Pc < p.n_cull) Pc <<= 1;
-    k_select<<<nA, 1024, Pc * sizeof(unsigned long long), s->stream>>>(w.cand, w.henergy, nullptr, w.cslot,
-                                                                       w.ncull_cap, w.ncand, 0, p.n_cull, p.n_out, 1,
-                                                                       w.cand, w.cenergy, w.cslot, w.ncand,
-                                                                       w.ncull_cap);
-    s->launches += 3;
+    SCR_LAUNCH(s, K_SELECT,
+               (k_select<<<nA, 1024, Pc * sizeof(unsigned long long), s->stream>>>(
+                   w.cand, w.henergy, nullptr, w.cslot, w.ncull_cap, w.ncand, 0, p.n_cull, p.n_out, 1, w.cand,
+                   w.cenergy, w.cslot, w.ncand, w.ncull_cap)));
   }
   SCR_CUDA(cudaGetLastError());
   // ICP / scoring jobs
@@ -836,13 +858,14 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
     const int nj = std::min(w.icp_cap, njobs - j0);
     IcpArgs ia{w.ncull_cap, jobs_per, mode != SCR_MODE_RAW ? 1 : 0, j0,
                static_cast<size_t>(s->k.width) * s->k.height};
-    k_icp_score<<<nj, 256, 0, s->stream>>>(ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand, w.icp_map,
-                                           w.icp_pose, w.icp_conv, w.icp_rms, w.icp_inl, w.icp_score);
-    s->launches += 1;
+    SCR_LAUNCH(s, K_ICP,
+               (k_icp_score<<<nj, 256, 0, s->stream>>>(ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand,
+                                                       w.icp_map, w.icp_pose, w.icp_conv, w.icp_rms, w.icp_inl,
+                                                       w.icp_score, wk)));
   }
-  k_finalize<<<(nA + 127) / 128, 128, 0, s->stream>>>(nA, mode, w.ncull_cap, w.cand, w.ncand, w.icp_pose, w.icp_conv,
-                                                      w.icp_score, d_res);
-  s->launches += 1;
+  SCR_LAUNCH(s, K_FINALIZE,
+             (k_finalize<<<(nA + 127) / 128, 128, 0, s->stream>>>(nA, mode, w.ncull_cap, w.cand, w.ncand, w.icp_pose,
+                                                                  w.icp_conv, w.icp_score, d_res)));
   SCR_CUDA(cudaGetLastError());
   return SCR_OK;
 }
@@ -923,6 +946,7 @@ scr_status run_cascade(scr_scene s, int n, const scr_ransac_params* stages, cons
     std::vector<scr_result> sr(nA);
     SCR_CUDA(cudaMemcpyAsync(sr.data(), d_res, nA * sizeof(scr_result), cudaMemcpyDeviceToHost, s->stream));
     SCR_CUDA(cudaStreamSynchronize(s->stream));
+    prof_flush(s);
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, ev0, ev1);
     std::vector<int> next;
@@ -1093,9 +1117,10 @@ scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, 
   SCR_CUDA(cudaMemcpyAsync(s->ws.ncand, &one, sizeof(int), cudaMemcpyHostToDevice, s->stream));
   SCR_CUDA(cudaMemcpyAsync(s->ws.cand, init, sizeof(Pose), cudaMemcpyHostToDevice, s->stream));
   IcpArgs ia{s->ws.ncull_cap, 1, 1, 0, WH};
-  k_icp_score<<<1, 256, 0, s->stream>>>(ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand, s->ws.ncand,
-                                        s->ws.icp_map, s->ws.icp_pose, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl,
-                                        s->ws.icp_score);
+  SCR_LAUNCH(s, K_ICP,
+             (k_icp_score<<<1, 256, 0, s->stream>>>(ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand,
+                                                    s->ws.ncand, s->ws.icp_map, s->ws.icp_pose, s->ws.icp_conv,
+                                                    s->ws.icp_rms, s->ws.icp_inl, s->ws.icp_score, nullptr)));
   SCR_CUDA(cudaGetLastError());
   SCR_CUDA(cudaStreamSynchronize(s->stream));
   SCR_CUDA(cudaMemcpy(out, s->ws.icp_pose, sizeof(Pose), cudaMemcpyDeviceToHost));

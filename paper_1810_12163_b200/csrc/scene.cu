@@ -27,6 +27,32 @@ namespace {
 thread_local std::string g_err;
 }
 void set_error(const std::string& m) { g_err = m; }
+
+cudaEvent_t prof_event(scr_scene s) {
+  if (s->prof.pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = s->prof.pool.back();
+  s->prof.pool.pop_back();
+  return e;
+}
+
+// Folds the completed launch events into per-kernel totals (call after a stream sync).
+void prof_flush(scr_scene s) {
+  for (auto& r : s->prof.pending) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) s->prof.ms[r.kid] += ms;
+    s->prof.pool.push_back(r.a);
+    s->prof.pool.push_back(r.b);
+  }
+  s->prof.pending.clear();
+}
+
+const char* const kKernelNames[K_COUNT] = {"k_pack", "k_grid", "k_leaves", "k_hypgen", "k_draw_samples", "k_energy",
+                                           "k_select", "k_lm", "k_icp_score", "k_finalize", "k_insert", "k_rqs",
+                                           "k_render"};
 scr_status cuda_fail(cudaError_t e, const char* what) {
   g_err = std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what;
   return e == cudaErrorMemoryAllocation ? SCR_E_OOM : SCR_E_CUDA;
@@ -107,7 +133,8 @@ __global__ void __launch_bounds__(1024) k_grid(const uint2* __restrict__ tex, in
 __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, const uint2* __restrict__ tex,
                                                 const int* __restrict__ gcount, const int* __restrict__ gpx,
                                                 int gmax, int* __restrict__ gslot, int* __restrict__ gnm,
-                                                float4* __restrict__ gcam, const int* __restrict__ pcount) {
+                                                float4* __restrict__ gcam, const int* __restrict__ pcount,
+                                                unsigned long long* __restrict__ work) {
   __shared__ short4 sspec[kFeatures];
   for (int i = threadIdx.x; i < kFeatures; i += blockDim.x) sspec[i] = fv.specs[i];
   __syncthreads();
@@ -121,7 +148,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
   const uint2* T = tex + static_cast<size_t>(f) * W * H;
   const uint2 c = T[y * W + x];
   const float d = __uint_as_float(c.x);
-  int nm = 0;
+  int nm = 0, visits = 0;
   for (int t = 0; t < fv.T; ++t) {
     const int nb = fv.node_base[t];
     int node = nb;
@@ -132,6 +159,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
         leaf = nd.y;
         break;
       }
+      ++visits;
       const short4 sp = sspec[nd.z];
       const int qx = x + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.x), d)));
       const int qy = y + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.y), d)));
@@ -151,6 +179,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
     if (pcount) nm += pcount[slot];
   }
   gnm[gidx] = nm;
+  if (work) atomicAdd(&work[W_NODE_VISITS], static_cast<unsigned long long>(visits));
   const double dd = static_cast<double>(d);
   const double X = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
   const double Y = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
@@ -747,6 +776,35 @@ void scr_scene_destroy(scr_scene s) {
   delete s;
 }
 
+scr_status scr_profile_enable(scr_scene s, int enable) {
+  if (!s) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  prof_flush(s);
+  if (!s->prof.d_work) SCR_CUDA(cudaMalloc(&s->prof.d_work, W_COUNT * sizeof(unsigned long long)));
+  SCR_CUDA(cudaMemset(s->prof.d_work, 0, W_COUNT * sizeof(unsigned long long)));
+  for (int k = 0; k < K_COUNT; ++k) {
+    s->prof.ms[k] = 0.0;
+    s->prof.launches[k] = 0;
+  }
+  s->prof.on = enable != 0;
+  return SCR_OK;
+}
+
+int scr_profile_read(scr_scene s, const char** names, double* ms, int64_t* launches, uint64_t* work, int cap) {
+  if (!s) return 0;
+  cudaSetDevice(s->dev->ordinal);
+  cudaStreamSynchronize(s->stream);
+  prof_flush(s);
+  for (int k = 0; k < K_COUNT && k < cap; ++k) {
+    if (names) names[k] = kKernelNames[k];
+    if (ms) ms[k] = s->prof.ms[k];
+    if (launches) launches[k] = s->prof.launches[k];
+  }
+  if (work && s->prof.d_work) cudaMemcpy(work, s->prof.d_work, W_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return K_COUNT;
+}
+
 int64_t scr_scene_total_leaves(scr_scene s) { return s ? s->L : 0; }
 void* scr_scene_stream(scr_scene s) { return s ? static_cast<void*>(s->stream) : nullptr; }
 int64_t scr_kernel_launches(scr_scene s) { return s ? s->launches : 0; }
@@ -804,12 +862,13 @@ namespace scr {
 scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_base, const int* d_idx, int n) {
   Workspace& w = s->ws;
   const int W = s->k.width, H = s->k.height, WH = W * H;
-  k_pack<<<dim3((WH + 1023) / 1024 < 64 ? (WH + 1023) / 1024 : 64, n), 256, 0, s->stream>>>(depth_base, rgb_base,
-                                                                                            d_idx, WH, w.tex);
-  k_grid<<<n, 1024, 0, s->stream>>>(w.tex, W, H, w.gmax, w.gcount, w.gpx);
-  k_leaves<<<dim3((w.gmax + 127) / 128, n), 128, 0, s->stream>>>(s->forest_view(), s->geom, w.tex, w.gcount, w.gpx,
-                                                               w.gmax, w.gslot, w.gnm, w.gcam, s->d_count);
-  s->launches += 3;
+  const int pack_blocks = (WH + 1023) / 1024 < 64 ? (WH + 1023) / 1024 : 64;
+  SCR_LAUNCH(s, K_PACK, (k_pack<<<dim3(pack_blocks, n), 256, 0, s->stream>>>(depth_base, rgb_base, d_idx, WH, w.tex)));
+  SCR_LAUNCH(s, K_GRID, (k_grid<<<n, 1024, 0, s->stream>>>(w.tex, W, H, w.gmax, w.gcount, w.gpx)));
+  SCR_LAUNCH(s, K_LEAVES,
+             (k_leaves<<<dim3((w.gmax + 127) / 128, n), 128, 0, s->stream>>>(
+                 s->forest_view(), s->geom, w.tex, w.gcount, w.gpx, w.gmax, w.gslot, w.gnm, w.gcam, s->d_count,
+                 work_ptr(s))));
   SCR_CUDA(cudaGetLastError());
   return SCR_OK;
 }
@@ -848,15 +907,18 @@ scr_status integrate_slot0(scr_scene s, const scr_pose* pose) {
   std::memcpy(P.R, pose->R, sizeof(P.R));
   std::memcpy(P.t, pose->t, sizeof(P.t));
   const int tb = 256, nb = (items + tb - 1) / tb;
-  k_ins_count<<<nb, tb, 0, s->stream>>>(w.gslot, items, w.ins_cnt);
-  k_scan<<<1, 1024, 0, s->stream>>>(w.ins_cnt, w.ins_off, static_cast<int>(s->L), w.ins_total);
-  k_ins_place<<<nb, tb, 0, s->stream>>>(w.gslot, items, w.ins_off, w.ins_cur, w.ins_item);
-  k_ins_rank<<<nb, tb, 0, s->stream>>>(w.gslot, T, w.ins_total, w.ins_off, w.ins_cnt, w.ins_item, s->d_seen,
-                                      s->fp.capacity, s->adapt_seed, w.ins_tgt, w.ins_rank);
-  k_ins_commit<<<nb, tb, 0, s->stream>>>(w.gslot, T, w.ins_total, w.ins_off, w.ins_cnt, w.ins_item, w.ins_tgt,
-                                        w.ins_rank, w.gpx, w.tex, s->geom, P, s->fp.capacity, s->d_entries,
-                                        s->d_seen);
-  s->launches += 5;
+  SCR_LAUNCH(s, K_INSERT, (k_ins_count<<<nb, tb, 0, s->stream>>>(w.gslot, items, w.ins_cnt)));
+  SCR_LAUNCH(s, K_INSERT,
+             (k_scan<<<1, 1024, 0, s->stream>>>(w.ins_cnt, w.ins_off, static_cast<int>(s->L), w.ins_total)));
+  SCR_LAUNCH(s, K_INSERT,
+             (k_ins_place<<<nb, tb, 0, s->stream>>>(w.gslot, items, w.ins_off, w.ins_cur, w.ins_item)));
+  SCR_LAUNCH(s, K_INSERT,
+             (k_ins_rank<<<nb, tb, 0, s->stream>>>(w.gslot, T, w.ins_total, w.ins_off, w.ins_cnt, w.ins_item,
+                                                  s->d_seen, s->fp.capacity, s->adapt_seed, w.ins_tgt, w.ins_rank)));
+  SCR_LAUNCH(s, K_INSERT,
+             (k_ins_commit<<<nb, tb, 0, s->stream>>>(w.gslot, T, w.ins_total, w.ins_off, w.ins_cnt, w.ins_item,
+                                                    w.ins_tgt, w.ins_rank, w.gpx, w.tex, s->geom, P,
+                                                    s->fp.capacity, s->d_entries, s->d_seen)));
   SCR_CUDA(cudaGetLastError());
   return SCR_OK;
 }
@@ -909,9 +971,10 @@ scr_status scr_update(scr_scene s, int64_t leaves_per_call) {
   const size_t smem = static_cast<size_t>(rp.kappa) * (4 * 4 + 8 + 4 * 4);
   for (int64_t done = 0; done < n; done += 65535) {
     const int chunk = static_cast<int>(std::min<int64_t>(65535, n - done));
-    k_rqs<<<chunk, 256, smem, s->stream>>>(s->d_entries, s->d_seen, s->L, (s->cursor + done) % s->L, chunk, rp,
-                                           s->d_count, s->d_geom, s->d_col, s->d_cov, nullptr, 0, nullptr);
-    s->launches += 1;
+    SCR_LAUNCH(s, K_RQS,
+               (k_rqs<<<chunk, 256, smem, s->stream>>>(s->d_entries, s->d_seen, s->L, (s->cursor + done) % s->L,
+                                                       chunk, rp, s->d_count, s->d_geom, s->d_col, s->d_cov, nullptr,
+                                                       0, nullptr)));
   }
   SCR_CUDA(cudaGetLastError());
   s->cursor = (s->cursor + n) % s->L;
@@ -1184,8 +1247,10 @@ scr_status scr_frameset_render(scr_frameset fs, int first, const scr_pose* poses
   SCR_CUDA(cudaMemcpy(d_p, poses, n * sizeof(Pose), cudaMemcpyHostToDevice));
   for (int c0 = 0; c0 < n; c0 += 65535) {
     const int c = std::min(65535, n - c0);
-    k_render<<<dim3(64, c), 256, 0, s->stream>>>(s->d_prims, s->n_prims, s->geom, d_p + c0,
-                                                 fs->depth + (first + c0) * WH, fs->rgb + (first + c0) * WH * 3);
+    SCR_LAUNCH(s, K_RENDER,
+               (k_render<<<dim3(64, c), 256, 0, s->stream>>>(s->d_prims, s->n_prims, s->geom, d_p + c0,
+                                                             fs->depth + (first + c0) * WH,
+                                                             fs->rgb + (first + c0) * WH * 3)));
   }
   SCR_CUDA(cudaGetLastError());
   SCR_CUDA(cudaStreamSynchronize(s->stream));

@@ -141,6 +141,8 @@ SIGNATURES = {
                                    _P(_i32), _P(Pose), _P(_flt), _P(C.c_int)]),
     "scr_debug_icp": (C.c_int, [_vp, _P(Frame), _P(Pose), _P(Pose), _P(C.c_int), _P(_dbl), _P(_dbl), _P(_dbl)]),
     "scr_kernel_launches": (_i64, [_vp]),
+    "scr_profile_enable": (C.c_int, [_vp, C.c_int]),
+    "scr_profile_read": (C.c_int, [_vp, _P(C.c_char_p), _P(_dbl), _P(_i64), _P(_u64), C.c_int]),
     "scr_generate_random_forest": (_sz, [_u64, C.c_int, _dbl, C.c_int, C.c_int, _P(C.c_uint8), _sz]),
     "scr_generate_synthetic_scene": (C.c_int, [_u64, C.c_int, _vp, C.c_int]),
     "scr_generate_trajectory": (None, [_u64, C.c_int, C.c_int, _P(Pose)]),
