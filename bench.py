@@ -153,7 +153,7 @@ def kernel_flops(name: str, work: dict, n_prims: int) -> float | None:
     if name == "k_energy":
         return FLOPS["mode_eval"] * work["mode_evals"] + FLOPS["sample_eval"] * work["sample_evals"]
     if name == "k_icp_score":
-        return FLOPS["icp_term"] * work["icp_terms"] + FLOPS["ray_prim"] * n_prims * work["rays"]
+        return FLOPS["icp_term"] * work["icp_terms"] + FLOPS["ray_prim"] * work["ray_prim_tests"]
     if name == "k_lm":
         return FLOPS["lm_term"] * work["lm_terms"] + FLOPS["mode_eval"] * work.get("lm_assoc_evals", 0)
     return None
@@ -334,6 +334,7 @@ def run_ours(args):
         "roofline": roofline,
         "accuracy": {"success_5cm_5deg": round(succ, 4), "frames": n_res, "stage_mix": stage_hist},
         "kernel_share": share,
+        "work": prof["work"],
         "adapt": {"frames": args.adapt_frames, "seconds": round(adapt_s, 2), "broadcast_ms": bcast_ms},
     }
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -383,7 +384,7 @@ def cpu_baseline(gscene, fs, poses, seeds, prims, gpu_results, args):
     for idx, res in gpu_results:
         for i, r in zip(idx, res):
             gpu_by_frame.setdefault(i, r)
-    sample = sorted(gpu_by_frame)[: max(threads, 8)]
+    sample = sorted(gpu_by_frame)[:256]
     D, RGB = fs.download(0, max(sample) + 1)
     st = [of.ransac_params(p) for p in ("fast", "intermediate", "slow")]
     done, t0, ok, exact, n = [], time.perf_counter(), 0, 0, 0
@@ -409,7 +410,7 @@ def cpu_baseline(gscene, fs, poses, seeds, prims, gpu_results, args):
                 exact += 1
         done.extend(part)
         el = time.perf_counter() - t0
-        if el > args.cpu_seconds or len(done) >= 4 * len(sample):
+        if el > args.cpu_seconds or len(done) >= len(sample):
             break
     base = {"value": round(len(done) / el, 3), "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{len(done)} test frames ({len(set(done))} distinct) through the same cascade, "

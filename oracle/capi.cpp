@@ -448,7 +448,7 @@ int or_energy(void* fp, void* sp, const float* depth, const uint8_t* rgb, const 
     FrameCtx c;
     build_frame_ctx(c, *static_cast<Forest*>(fp), *static_cast<AdaptState*>(sp), fr);
     std::vector<int> s(samples, samples + n);
-    *out = energy(c, *static_cast<AdaptState*>(sp), to_pose(H->R, H->t), s);
+    *out = energy(c, *static_cast<AdaptState*>(sp), to_pose(H->R, H->t), s, n > 0 ? n : 1);
     return 0;
   });
 }

@@ -190,7 +190,8 @@ struct Hypothesis {
 };
 int generate_hypothesis(const FrameCtx& c, const AdaptState& s, const RansacParams& p, Rng& rng, Pose* out,
                         int* attempts);
-float energy(const FrameCtx& c, const AdaptState& s, const Pose& H, const std::vector<int>& samples);
+// Eq. 5 accumulated per eta-sample batch: E = sum_b E_b (batches in order), E_b sequential.
+float energy(const FrameCtx& c, const AdaptState& s, const Pose& H, const std::vector<int>& samples, int eta);
 void draw_samples(uint64_t seed, int batch, int n_max, int eta, int G, std::vector<int>& out);
 void lm_refine(const FrameCtx& c, const AdaptState& s, Pose& H, const std::vector<int>& samples, bool use_cov,
                double* final_surrogate = nullptr);
@@ -227,7 +228,8 @@ uint64_t stage_seed(uint64_t seed, int stage);
 
 // Canonical reduction orders shared (by definition, not by code) with the GPU.
 constexpr int kLmLanes = 32;
-constexpr int kIcpLanes = 256;
+constexpr int kIcpCtas = 8;                    // ICP / score: 8-CTA cluster
+constexpr int kIcpLanes = 256 * kIcpCtas;      // lanes = threads of the cluster
 constexpr int kIcpIters[3] = {4, 5, 10};  // level 0 (fine), 1, 2 (coarse)
 
 }  // namespace oracle

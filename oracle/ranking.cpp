@@ -54,11 +54,12 @@ void render_model_map(const Scene& s, const Pose& T, const Intrinsics& k, ModelM
     }
 }
 
-// 256 lanes: lane l owns pixels p = l (mod 256) in row-major order and accumulates in
-// f32; lanes are widened to f64, combined by an xor butterfly inside each 32-lane warp,
-// then the 8 warp sums are added sequentially.
+// kIcpLanes = 8 x 256 lanes (the threads of an 8-CTA cluster): lane l owns pixels
+// p = l (mod kIcpLanes) in row-major order and accumulates in f32; lanes are widened to
+// f64 and combined by an xor butterfly inside each 32-lane warp, the 8 warp sums of a CTA
+// are added sequentially, then the 8 CTA sums are added sequentially.
 void canonical_reduce(const float lanes[kIcpLanes][kIcpAcc], int nacc, double out[]) {
-  double warp_sum[kIcpLanes / 32][kIcpAcc];
+  static thread_local double warp_sum[kIcpLanes / 32][kIcpAcc];
   for (int w = 0; w < kIcpLanes / 32; ++w) {
     double v[32][kIcpAcc];
     for (int l = 0; l < 32; ++l)
@@ -73,9 +74,13 @@ void canonical_reduce(const float lanes[kIcpLanes][kIcpAcc], int nacc, double ou
     for (int a = 0; a < nacc; ++a) warp_sum[w][a] = v[0][a];
   }
   for (int a = 0; a < nacc; ++a) {
-    double s = warp_sum[0][a];
-    for (int w = 1; w < kIcpLanes / 32; ++w) s = s + warp_sum[w][a];
-    out[a] = s;
+    double total = 0.0;
+    for (int c = 0; c < kIcpCtas; ++c) {
+      double s = warp_sum[8 * c][a];
+      for (int w = 1; w < 8; ++w) s = s + warp_sum[8 * c + w][a];
+      total = c == 0 ? s : total + s;
+    }
+    out[a] = total;
   }
 }
 }  // namespace
@@ -106,8 +111,8 @@ IcpResult icp_refine(const Scene& s, const Pose& init, const Frame& fr) {
       float R[9], tf[3];
       for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(T.R[i]);
       for (int i = 0; i < 3; ++i) tf[i] = static_cast<float>(T.t[i]);
-      float lanes[kIcpLanes][kIcpAcc];
-      int lane_inl[kIcpLanes], lane_valid[kIcpLanes];
+      static thread_local float lanes[kIcpLanes][kIcpAcc];
+      static thread_local int lane_inl[kIcpLanes], lane_valid[kIcpLanes];
       for (int l = 0; l < kIcpLanes; ++l) {
         for (int a = 0; a < kIcpAcc; ++a) lanes[l][a] = 0.0f;
         lane_inl[l] = lane_valid[l] = 0;
@@ -200,7 +205,7 @@ IcpResult icp_refine(const Scene& s, const Pose& init, const Frame& fr) {
 // depth_diff_score (Eqs. 6-7): mean |D_live - D_synth| over pixels valid
 // in both; inf if valid(D_synth)/|Omega| < 0.1 or the mutual set is empty.
 double depth_diff_images(const float* live, const float* synth, int W, int H) {
-  float lanes[kIcpLanes][kIcpAcc];
+  static thread_local float lanes[kIcpLanes][kIcpAcc];
   int mutual = 0, nsynth = 0;
   for (int l = 0; l < kIcpLanes; ++l) lanes[l][0] = 0.0f;
   for (int p = 0; p < W * H; ++p) {

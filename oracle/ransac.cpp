@@ -151,12 +151,18 @@ static inline float quad_icov(const float* ic, float d0, float d1, float d2) {
 static inline float quad_eucl(float d0, float d1, float d2) { return std::fma(d0, d0, std::fma(d1, d1, d2 * d2)); }
 
 // Eq. 5: E = sum_i min_modes ||Sigma^-1/2 (H x_i - mu)||, evaluated as
-// sqrt(min d^T Sigma^-1 d); samples without modes contribute 0; sequential f32 sum.
-float energy(const FrameCtx& c, const AdaptState& s, const Pose& H, const std::vector<int>& samples) {
+// sqrt(min d^T Sigma^-1 d); samples without modes contribute 0; f32 sums: sequential within
+// each eta-sample batch, then batch totals added in batch order (DESIGN.md numerics contract).
+float energy(const FrameCtx& c, const AdaptState& s, const Pose& H, const std::vector<int>& samples, int eta) {
   float R[9], t[3];
   pose_to_f32(H, R, t);
-  float E = 0.0f;
-  for (int g : samples) {
+  float E = 0.0f, Eb = 0.0f;
+  for (size_t i = 0; i < samples.size(); ++i) {
+    if (i > 0 && i % static_cast<size_t>(eta) == 0) {  // batch boundary
+      E = E + Eb;
+      Eb = 0.0f;
+    }
+    const int g = samples[i];
     const int nm = c.nmodes[g];
     if (nm == 0) continue;
     float y[3];
@@ -167,9 +173,9 @@ float energy(const FrameCtx& c, const AdaptState& s, const Pose& H, const std::v
       const float q = quad_icov(md->icov, y[0] - md->mu[0], y[1] - md->mu[1], y[2] - md->mu[2]);
       qmin = std::fmin(qmin, q);
     }
-    E = E + std::sqrt(std::fmax(qmin, 0.0f));
+    Eb = Eb + std::sqrt(std::fmax(qmin, 0.0f));
   }
-  return E;
+  return E + Eb;
 }
 
 namespace {
@@ -332,7 +338,7 @@ std::vector<Hypothesis> preemptive_ransac(const FrameCtx& c, const AdaptState& s
   if (hyps.empty()) throw Error(E_NO_HYPOTHESES, "preemptive_ransac: every generation slot failed");
   std::vector<int> I;
   draw_samples(seed, 0, p.n_max, p.eta, G, I);
-  for (auto& h : hyps) h.energy = energy(c, s, h.pose, I);
+  for (auto& h : hyps) h.energy = energy(c, s, h.pose, I, p.eta);
   std::sort(hyps.begin(), hyps.end(), hyp_less);
   if (static_cast<int>(hyps.size()) > p.n_cull) hyps.resize(p.n_cull);
   int k = 1;
@@ -340,7 +346,7 @@ std::vector<Hypothesis> preemptive_ransac(const FrameCtx& c, const AdaptState& s
     draw_samples(seed, k, p.n_max, p.eta, G, I);
     for (auto& h : hyps) {
       if (p.pose_update) lm_refine(c, s, h.pose, I, p.use_cov != 0);
-      h.energy = energy(c, s, h.pose, I);
+      h.energy = energy(c, s, h.pose, I, p.eta);
     }
     std::sort(hyps.begin(), hyps.end(), hyp_less);
     hyps.resize((hyps.size() + 1) / 2);

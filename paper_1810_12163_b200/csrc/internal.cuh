@@ -25,7 +25,7 @@ enum KernelId {
 };
 // device work counters (u64), indexed by W_*; meaning documented in DESIGN.md "Roofline"
 enum WorkId {
-  W_MODE_EVALS, W_SAMPLE_EVALS, W_LM_TERMS, W_ICP_TERMS, W_RAYS, W_NODE_VISITS, W_GEN_ATTEMPTS, W_LM_ASSOC, W_COUNT
+  W_MODE_EVALS, W_SAMPLE_EVALS, W_LM_TERMS, W_ICP_TERMS, W_RAYS, W_NODE_VISITS, W_GEN_ATTEMPTS, W_LM_ASSOC, W_RAY_PRIMS, W_COUNT
 };
 
 struct Profiler {
@@ -73,6 +73,7 @@ struct Workspace {
   float4* gcam = nullptr;     // [cap * gmax] camera point (f32 of the f64 backprojection)
   int* gslot = nullptr;       // [cap * gmax * T]
   int* gnm = nullptr;         // [cap * gmax] number of modes (union over trees)
+  int4* grec = nullptr;       // [cap * gmax] {x|y<<16, depth bits, rgb | nm<<24, 6-bit counts of trees 0..4}
   // RANSAC (grown on demand)
   int nmax_cap = 0, ncull_cap = 0, samples_cap = 0;
   Pose* hyp = nullptr;        // [cap * nmax]
@@ -83,6 +84,7 @@ struct Workspace {
   float* cenergy = nullptr;   // [cap * ncull]
   int* cslot = nullptr;       // [cap * ncull]
   int* ncand = nullptr;       // [cap]
+  float* epart = nullptr;     // per-batch partial energies [cap * ncull * kEnergyBatches]
   int* samples = nullptr;     // [cap * samples_cap]
   int* assoc = nullptr;       // [cap * ncull * samples_cap]
   // ranking / ICP
@@ -95,7 +97,8 @@ struct Workspace {
   double* icp_inl = nullptr;
   int* fidx = nullptr;        // active frame list [cap]
   uint64_t* seeds = nullptr;  // [cap]
-  int* status = nullptr;      // [cap]
+  int* status = nullptr;      // [cap] frame-set indices for pack_frames
+  int* hctr = nullptr;        // [cap] per-frame generation slot counters
   // reservoir insertion scratch (one frame)
   unsigned* ins_cnt = nullptr;  // [L]
   unsigned* ins_off = nullptr;  // [L + 1]
@@ -176,6 +179,7 @@ scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_
 scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int samples);
 scr_status ensure_icp_ws(scr_scene s, int jobs);
 // reloc.cu
+scr_status reloc_init();
 scr_status run_cascade(scr_scene s, int n, const scr_ransac_params* stages, const int32_t* modes,
                        const double* thr, int nstages, const uint64_t* seeds, scr_result* out);
 scr_status run_ransac_debug(scr_scene s, const scr_ransac_params* p, uint64_t seed, int32_t* gen_slots,

@@ -19,6 +19,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 
 namespace scr {
@@ -37,6 +39,7 @@ struct FrameRefs {  // per-batch views of the packed frames
   const float4* gcam;
   const int* gslot;
   const int* gnm;
+  const int4* grec;
   const uint2* tex;
   int gmax, T;
 };
@@ -52,90 +55,141 @@ SCR_DEV int mode_index(const FrameRefs& fr, const int* pcount, size_t gbase, int
 }
 
 // ================================ K4: hypothesis generation ================================
-// One thread per (frame, slot); slot s draws from Rng::stream(seed, s) and retries up to
-// max_iters. Draw order and checks follow DESIGN.md A1/A7.
-__global__ void __launch_bounds__(128) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
-                                                const uint64_t* __restrict__ seeds, Pose* __restrict__ hyp,
-                                                int* __restrict__ hok, int* __restrict__ hiters,
-                                                unsigned long long* __restrict__ work) {
+// Generation slots are independent (slot s draws from Rng::stream(seed, s) and retries up
+// to max_iters; draw order and checks per DESIGN.md A1/A7), so lanes pull
+// slots from a per-frame atomic counter and never idle behind a slower lane. An attempt
+// reads the 16-byte per-pixel records written by K1 (pixel, depth, colour, per-tree mode
+// counts), so the colour check needs one slot + one colour load; the world points of the
+// other two modes are only fetched when it passes. Uniform draws use exact Barrett
+// reductions with precomputed reciprocals/thresholds (same values as the 64-bit modulo).
+constexpr int kMaxModeUnion = kMaxTrees * kMaxModes;
+constexpr int kGenThreadsPerFrame = 2048;
+
+SCR_DEV uint64_t draw(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
+  for (;;) {
+    const uint64_t v = rng_next(r);
+    if (v >= thr) return mod_barrett(v, n, m);
+  }
+}
+
+SCR_DEV int pick_mode(const FrameRefs& fr, const int* pcount, size_t gb, uint32_t counts, bool fast, int pick) {
+  if (fast) {
+    for (int t = 0; t < fr.T; ++t) {
+      const int c = static_cast<int>((counts >> (6 * t)) & 63u);
+      if (pick < c) return fr.gslot[gb * fr.T + t] * kMaxModes + pick;
+      pick -= c;
+    }
+    return -1;
+  }
+  return mode_index(fr, pcount, gb, pick);
+}
+
+// Kabsch (f64 SVD) runs only for triplets that passed every check; out of line so it does
+// not set the register budget of the retry loop.
+__device__ __noinline__ bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return kabsch3(cm, w, *T); }
+
+__global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
+                                                const uint64_t* __restrict__ seeds, int* __restrict__ slot_ctr,
+                                                Pose* __restrict__ hyp, int* __restrict__ hok,
+                                                int* __restrict__ hiters, unsigned long long* __restrict__ work) {
+  __shared__ uint64_t s_m[kMaxModeUnion + 1];    // Barrett reciprocal for mode counts 1..400
+  __shared__ uint64_t s_thr[kMaxModeUnion + 1];  // rejection threshold (2^64 mod n)
+  for (int i = threadIdx.x; i <= kMaxModeUnion; i += blockDim.x) {
+    const uint64_t n = i ? static_cast<uint64_t>(i) : 1;
+    const uint64_t m = barrett_m(n);
+    s_m[i] = m;
+    s_thr[i] = mod_barrett(0 - n, n, m);
+  }
+  __syncthreads();
   const int a = blockIdx.y;
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= gp.nmax) return;
   const int f = fr.fidx[a];
   const uint64_t G = static_cast<uint64_t>(fr.gcount[f]);
-  const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
-  Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(slot));
-  int ok = 0, it = 0;
-  Pose T;
-  if (G > 0) {
-    const size_t fbase = static_cast<size_t>(f) * fr.gmax;
-    const uint2* tex = fr.tex + static_cast<size_t>(f) * g.W * g.H;
-    for (it = 0; it < gp.max_iters; ++it) {
-      int gi[3], mi[3];
-      bool good = true;
+  const uint64_t mG = G ? barrett_m(G) : 1, tG = G ? mod_barrett(0 - G, G, mG) : 0;
+  const uint64_t m3 = 0x5555555555555555ull, t3 = 1;  // floor((2^64-1)/3), 2^64 mod 3
+  const bool fast = fr.T <= 5;
+  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  unsigned long long attempts_total = 0;
+  for (int slot = atomicAdd(&slot_ctr[a], 1); slot < gp.nmax; slot = atomicAdd(&slot_ctr[a], 1)) {
+    const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
+    Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(slot));
+    int ok = 0, it = 0;
+    Pose T;
+    if (G > 0) {
+      for (it = 0; it < gp.max_iters; ++it) {
+        int4 rec[3];
+        int pick[3], gix[3];
+        bool good = true;
 #pragma unroll 1
-      for (int k = 0; k < 3; ++k) {
-        gi[k] = static_cast<int>(rng_uniform_int(rng, G));
-        const int nm = fr.gnm[fbase + gi[k]];
-        if (nm == 0) {
-          good = false;
-          break;
+        for (int k = 0; k < 3; ++k) {
+          const int gi = static_cast<int>(draw(rng, G, mG, tG));
+          gix[k] = gi;
+          rec[k] = fr.grec[fbase + gi];
+          const int nm = fast ? (static_cast<uint32_t>(rec[k].z) >> 24) : fr.gnm[fbase + gi];
+          if (nm == 0) {
+            good = false;
+            break;
+          }
+          pick[k] = static_cast<int>(draw(rng, static_cast<uint64_t>(nm), s_m[nm], s_thr[nm]));
         }
-        mi[k] = mode_index(fr, pv.count, fbase + gi[k], static_cast<int>(rng_uniform_int(rng, static_cast<uint64_t>(nm))));
-      }
-      if (!good) continue;
-      const int cc = static_cast<int>(rng_uniform_int(rng, 3));
-      {
-        const int px = fr.gpx[fbase + gi[cc]];
-        const uint32_t col = tex[(px >> 16) * g.W + (px & 0xffff)].y;
-        const float4 mc = pv.col[mi[cc]];
-        float linf = 0.0f;
-        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
-        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 8) & 255u), mc.y)));
-        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 16) & 255u), mc.z)));
-        if (linf > gp.colour_thresh) continue;
-      }
-      double w[9], cm[9];
+        if (!good) continue;
+        const int cc = static_cast<int>(draw(rng, 3, m3, t3));
+        int mi[3];
+        mi[cc] = pick_mode(fr, pv.count, fbase + gix[cc], static_cast<uint32_t>(rec[cc].w), fast, pick[cc]);
+        {
+          const uint32_t col = static_cast<uint32_t>(rec[cc].z);
+          const float4 mc = pv.col[mi[cc]];
+          float linf = 0.0f;
+          linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
+          linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 8) & 255u), mc.y)));
+          linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 16) & 255u), mc.z)));
+          if (linf > gp.colour_thresh) continue;
+        }
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float4 q0 = pv.geom[mi[k]].q0;
-        w[3 * k + 0] = static_cast<double>(q0.x);
-        w[3 * k + 1] = static_cast<double>(q0.y);
-        w[3 * k + 2] = static_cast<double>(q0.z);
-        const int px = fr.gpx[fbase + gi[k]];
-        const int x = px & 0xffff, y = px >> 16;
-        const double dd = static_cast<double>(__uint_as_float(tex[y * g.W + x].x));
-        cm[3 * k + 0] = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
-        cm[3 * k + 1] = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
-        cm[3 * k + 2] = dd;
-      }
-      double dw2[3], dc2[3];
-      bool close = false;
+        for (int k = 0; k < 3; ++k)
+          if (k != cc) mi[k] = pick_mode(fr, pv.count, fbase + gix[k], static_cast<uint32_t>(rec[k].w), fast, pick[k]);
+        double w[9], cm[9];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
-        const double ax = w[3 * pa] - w[3 * pb], ay = w[3 * pa + 1] - w[3 * pb + 1], az = w[3 * pa + 2] - w[3 * pb + 2];
-        dw2[q] = (ax * ax + ay * ay) + az * az;
-        const double bx = cm[3 * pa] - cm[3 * pb], by = cm[3 * pa + 1] - cm[3 * pb + 1],
-                     bz = cm[3 * pa + 2] - cm[3 * pb + 2];
-        dc2[q] = (bx * bx + by * by) + bz * bz;
-        if (dw2[q] < gp.min_sq_dist) close = true;
-      }
-      if (close) continue;
-      bool nonrigid = false;
+        for (int k = 0; k < 3; ++k) {
+          const float4 q0 = pv.geom[mi[k]].q0;
+          w[3 * k + 0] = static_cast<double>(q0.x);
+          w[3 * k + 1] = static_cast<double>(q0.y);
+          w[3 * k + 2] = static_cast<double>(q0.z);
+          const int x = rec[k].x & 0xffff, y = rec[k].x >> 16;
+          const double dd = static_cast<double>(__int_as_float(rec[k].y));
+          cm[3 * k + 0] = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
+          cm[3 * k + 1] = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
+          cm[3 * k + 2] = dd;
+        }
+        double dw2[3], dc2[3];
+        bool close = false;
 #pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > gp.rigidity_tol) nonrigid = true;
-      if (nonrigid) continue;
-      if (!kabsch3(cm, w, T)) continue;
-      ok = 1;
-      break;
+        for (int q = 0; q < 3; ++q) {
+          const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
+          const double ax = w[3 * pa] - w[3 * pb], ay = w[3 * pa + 1] - w[3 * pb + 1],
+                       az = w[3 * pa + 2] - w[3 * pb + 2];
+          dw2[q] = (ax * ax + ay * ay) + az * az;
+          const double bx = cm[3 * pa] - cm[3 * pb], by = cm[3 * pa + 1] - cm[3 * pb + 1],
+                       bz = cm[3 * pa + 2] - cm[3 * pb + 2];
+          dc2[q] = (bx * bx + by * by) + bz * bz;
+          if (dw2[q] < gp.min_sq_dist) close = true;
+        }
+        if (close) continue;
+        bool nonrigid = false;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > gp.rigidity_tol) nonrigid = true;
+        if (nonrigid) continue;
+        if (!kabsch3_cold(cm, w, &T)) continue;
+        ok = 1;
+        break;
+      }
     }
+    if (ok) hyp[out] = T;
+    hok[out] = ok;
+    hiters[out] = ok ? it + 1 : gp.max_iters;
+    attempts_total += static_cast<unsigned long long>(ok ? it + 1 : (G > 0 ? gp.max_iters : 0));
   }
-  if (ok) hyp[out] = T;
-  hok[out] = ok;
-  hiters[out] = ok ? it + 1 : gp.max_iters;
-  if (work) atomicAdd(&work[W_GEN_ATTEMPTS], static_cast<unsigned long long>(ok ? it + 1 : (G > 0 ? gp.max_iters : 0)));
+  if (work) atomicAdd(&work[W_GEN_ATTEMPTS], attempts_total);
 }
 
 // Sample batch k of frame a: eta draws of uniform_int(G) from Rng::stream(seed, nmax + k).
@@ -150,65 +204,240 @@ __global__ void k_draw_samples(FrameRefs fr, const uint64_t* __restrict__ seeds,
     return;
   }
   Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(nmax) + static_cast<uint64_t>(batch));
-  for (int i = 0; i < eta; ++i) out[i] = static_cast<int>(rng_uniform_int(rng, G));
+  const uint64_t mG = barrett_m(G);
+  for (int i = 0; i < eta; ++i) out[i] = static_cast<int>(rng_uniform_int_m(rng, G, mG));
 }
 
 // ================================ K5: Eq. 5 energy =========================================
-// One thread per (frame, hypothesis); a warp holds 32 hypotheses of one frame walking the
-// same samples, so every mode load is warp-uniform (one broadcast transaction).
-__global__ void __launch_bounds__(128) k_energy(FrameRefs fr, PredView pv, const Pose* __restrict__ poses,
-                                                const int* __restrict__ ok, int stride,
-                                                const int* __restrict__ nper, int min_n,
-                                                const int* __restrict__ samples, int scap, int ns,
-                                                float* __restrict__ out, unsigned long long* __restrict__ work) {
-  const int a = blockIdx.y;
-  const int h = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n = nper ? nper[a] : stride;
-  if (h >= n || n <= min_n) return;
-  const size_t idx = static_cast<size_t>(a) * stride + h;
-  if (ok && !ok[idx]) {
-    out[idx] = __int_as_float(0x7f800000);
-    return;
-  }
+// Energy is accumulated per eta-sample batch (E = sum_b E_b in batch order, E_b sequential
+// over the batch's samples; DESIGN.md numerics contract). One CTA per (frame, batch,
+// hypothesis tile): the batch's camera points and the predicted modes of its samples are
+// staged in shared memory (chunked by a mode budget), then each thread owns one
+// hypothesis and sweeps the staged samples in order; all threads read the same staged
+// mode at the same time (shared-memory broadcast), so the inner loop is pure FP32.
+constexpr int kEnergyModeCap = 1024;    // staged modes per chunk: 1024 x 48 B = 48 KB
+constexpr int kEnergySampleCap = 512;   // eta <= 512 (Table 4)
+constexpr int kEnergyBatches = 8;       // sample batches per frame (1 + halvings)
+
+struct EnergyArgs {
+  const Pose* poses;
+  const int* ok;
+  int stride;
+  const int* nper;
+  int min_n;
+  const int* samples;
+  int scap, eta, batch0;
+  float* out;
+  int kb;  // 0: out[a*stride + h] = E_b; else out[(a*stride + h)*kb + b] = E_b
+};
+
+__global__ void __launch_bounds__(256) k_energy(EnergyArgs ea, FrameRefs fr, PredView pv,
+                                                unsigned long long* __restrict__ work) {
+  extern __shared__ float4 es_mode[];  // kEnergyModeCap * 3
+  __shared__ float4 es_cam[kEnergySampleCap];
+  __shared__ int es_off[kEnergySampleCap + 1];
+  const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
+  const int n = ea.nper ? ea.nper[a] : ea.stride;
+  if (n <= ea.min_n) return;
+  const int h0 = blockIdx.x * blockDim.x;
+  if (h0 >= n) return;
+  const int h = h0 + threadIdx.x;
+  const size_t idx = static_cast<size_t>(a) * ea.stride + h;
+  const bool active = h < n && (!ea.ok || ea.ok[idx]);
   float R[9], t[3];
-  const Pose& P = poses[idx];
+  if (active) {
+    const Pose& P = ea.poses[idx];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(P.R[i]);
+    for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(P.R[i]);
 #pragma unroll
-  for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(P.t[i]);
+    for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(P.t[i]);
+  }
   const int f = fr.fidx[a];
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
-  const int* smp = samples + static_cast<size_t>(a) * scap;
+  const int* smp = ea.samples + static_cast<size_t>(a) * ea.scap + static_cast<size_t>(b) * ea.eta;
+  const int eta = ea.eta;
+  for (int s = threadIdx.x; s < eta; s += blockDim.x) es_off[s] = fr.gnm[fbase + smp[s]];
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive prefix of the per-sample mode counts
+    const int lane = threadIdx.x;
+    const int per = (eta + 31) / 32;
+    const int s0 = min(eta, lane * per), s1 = min(eta, s0 + per);
+    int local = 0;
+    for (int s = s0; s < s1; ++s) local += es_off[s];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - local;
+    for (int s = s0; s < s1; ++s) {
+      const int c = es_off[s];
+      es_off[s] = run;
+      run += c;
+    }
+    if (lane == 31) es_off[eta] = incl;
+  }
+  __syncthreads();
   float E = 0.0f;
   unsigned long long evals = 0, sevals = 0;
-  for (int s = 0; s < ns; ++s) {
-    const int gi = smp[s];
-    const size_t gb = fbase + gi;
-    if (fr.gnm[gb] == 0) continue;
-    evals += fr.gnm[gb];
-    ++sevals;
-    const float4 c = fr.gcam[gb];
-    float y[3];
-    xform_f32(R, t, c.x, c.y, c.z, y);
-    float qmin = __int_as_float(0x7f800000);
-    for (int tt = 0; tt < fr.T; ++tt) {
-      const int slot = fr.gslot[gb * fr.T + tt];
-      const int cnt = pv.count[slot];
-      const ModeGeom* mg = pv.geom + static_cast<size_t>(slot) * kMaxModes;
-      for (int m = 0; m < cnt; ++m) {
-        const float4 q0 = mg[m].q0, q1 = mg[m].q1, q2 = mg[m].q2;
-        const float q = quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(y[0], q0.x), __fsub_rn(y[1], q0.y),
-                                  __fsub_rn(y[2], q0.z));
-        qmin = fminf(qmin, q);
+  int s0 = 0;
+  while (s0 < eta) {
+    int lo = s0 + 1, hi = eta;  // largest s1 whose modes fit the staging budget
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (es_off[mid] - es_off[s0] <= kEnergyModeCap) lo = mid;
+      else hi = mid - 1;
+    }
+    const int s1 = lo;
+    for (int s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
+      const size_t gb = fbase + smp[s];
+      es_cam[s - s0] = fr.gcam[gb];
+      int base = es_off[s] - es_off[s0];
+      for (int tt = 0; tt < fr.T; ++tt) {
+        const int slot = fr.gslot[gb * fr.T + tt];
+        const int cnt = pv.count[slot];
+        const ModeGeom* mg = pv.geom + static_cast<size_t>(slot) * kMaxModes;
+        for (int m = 0; m < cnt; ++m, ++base) {
+          es_mode[3 * base + 0] = mg[m].q0;
+          es_mode[3 * base + 1] = mg[m].q1;
+          es_mode[3 * base + 2] = mg[m].q2;
+        }
       }
     }
-    E = __fadd_rn(E, __fsqrt_rn(fmaxf(qmin, 0.0f)));
+    __syncthreads();
+    if (active) {
+      const int cbase = es_off[s0];
+      for (int s = s0; s < s1; ++s) {
+        const int m0 = es_off[s] - cbase, m1 = es_off[s + 1] - cbase;
+        if (m1 == m0) continue;
+        const float4 c = es_cam[s - s0];
+        float y[3];
+        xform_f32(R, t, c.x, c.y, c.z, y);
+        float qmin = __int_as_float(0x7f800000);
+        for (int m = m0; m < m1; ++m) {
+          const float4 q0 = es_mode[3 * m + 0], q1 = es_mode[3 * m + 1], q2 = es_mode[3 * m + 2];
+          const float q = quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(y[0], q0.x), __fsub_rn(y[1], q0.y),
+                                    __fsub_rn(y[2], q0.z));
+          qmin = fminf(qmin, q);
+        }
+        E = __fadd_rn(E, __fsqrt_rn(fmaxf(qmin, 0.0f)));
+        evals += static_cast<unsigned long long>(m1 - m0);
+        ++sevals;
+      }
+    }
+    __syncthreads();
+    s0 = s1;
   }
-  out[idx] = E;
-  if (work) {
+  if (h < n) {
+    const float v = active ? E : __int_as_float(0x7f800000);
+    if (ea.kb == 0) ea.out[idx] = v;
+    else ea.out[idx * ea.kb + b] = v;
+  }
+  if (work && active) {
     atomicAdd(&work[W_MODE_EVALS], evals);
     atomicAdd(&work[W_SAMPLE_EVALS], sevals);
   }
+}
+
+// Re-scoring the <= 64 surviving hypotheses on one sample batch: warp per sample, lane l
+// owns hypotheses l and l + 32, so each predicted mode is loaded once per warp (uniform
+// load) and used for 2 x 32 hypotheses. Per-sample energies e[h][s] go to shared memory;
+// thread h then adds its row in sample order (the batch energy E_b, same bits as a
+// sequential sweep: samples without modes contribute +0).
+constexpr int kSmallHyps = 64;
+
+__global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs fr, PredView pv,
+                                                      unsigned long long* __restrict__ work) {
+  extern __shared__ float es_e[];  // [kSmallHyps][eta + 1]
+  __shared__ float s_pose[kSmallHyps][12];
+  const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
+  const int n = ea.nper ? ea.nper[a] : ea.stride;
+  if (n <= ea.min_n) return;
+  for (int h = threadIdx.x; h < n; h += blockDim.x) {
+    const Pose& P = ea.poses[static_cast<size_t>(a) * ea.stride + h];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) s_pose[h][i] = static_cast<float>(P.R[i]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s_pose[h][9 + i] = static_cast<float>(P.t[i]);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int h0 = lane, h1 = lane + 32;
+  const bool v0 = h0 < n, v1 = h1 < n;
+  float R0[9], t0[3], R1[9], t1[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    R0[i] = v0 ? s_pose[h0][i] : 0.0f;
+    R1[i] = v1 ? s_pose[h1][i] : 0.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    t0[i] = v0 ? s_pose[h0][9 + i] : 0.0f;
+    t1[i] = v1 ? s_pose[h1][9 + i] : 0.0f;
+  }
+  const int f = fr.fidx[a];
+  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  const int* smp = ea.samples + static_cast<size_t>(a) * ea.scap + static_cast<size_t>(b) * ea.eta;
+  const int eta = ea.eta, ld = eta + 1;
+  unsigned long long evals = 0, sevals = 0;
+  for (int s = wid; s < eta; s += nw) {
+    const size_t gb = fbase + smp[s];
+    const int nm = fr.gnm[gb];
+    float e0 = 0.0f, e1 = 0.0f;
+    if (nm > 0) {
+      const float4 c = fr.gcam[gb];
+      float y0[3], y1[3];
+      xform_f32(R0, t0, c.x, c.y, c.z, y0);
+      xform_f32(R1, t1, c.x, c.y, c.z, y1);
+      float m0 = __int_as_float(0x7f800000), m1 = m0;
+      for (int tt = 0; tt < fr.T; ++tt) {
+        const int slot = fr.gslot[gb * fr.T + tt];
+        const int cnt = pv.count[slot];
+        const ModeGeom* mg = pv.geom + static_cast<size_t>(slot) * kMaxModes;
+        for (int m = 0; m < cnt; ++m) {
+          const float4 q0 = mg[m].q0, q1 = mg[m].q1, q2 = mg[m].q2;
+          m0 = fminf(m0, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(y0[0], q0.x),
+                                   __fsub_rn(y0[1], q0.y), __fsub_rn(y0[2], q0.z)));
+          m1 = fminf(m1, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(y1[0], q0.x),
+                                   __fsub_rn(y1[1], q0.y), __fsub_rn(y1[2], q0.z)));
+        }
+      }
+      e0 = __fsqrt_rn(fmaxf(m0, 0.0f));
+      e1 = __fsqrt_rn(fmaxf(m1, 0.0f));
+      if (lane == 0) {
+        evals += static_cast<unsigned long long>(nm) * static_cast<unsigned long long>(n);
+        sevals += static_cast<unsigned long long>(n);
+      }
+    }
+    if (v0) es_e[h0 * ld + s] = e0;
+    if (v1) es_e[h1 * ld + s] = e1;
+  }
+  __syncthreads();
+  if (threadIdx.x < n) {
+    const int h = threadIdx.x;
+    float E = 0.0f;
+    for (int s = 0; s < eta; ++s) E = __fadd_rn(E, es_e[h * ld + s]);
+    const size_t idx = static_cast<size_t>(a) * ea.stride + h;
+    if (ea.kb == 0) ea.out[idx] = E;
+    else ea.out[idx * ea.kb + b] = E;
+  }
+  if (work && lane == 0 && sevals) {
+    atomicAdd(&work[W_MODE_EVALS], evals);
+    atomicAdd(&work[W_SAMPLE_EVALS], sevals);
+  }
+}
+
+// E(I_k) = base + E_b0 + ... + E_b1 in batch order (base = E(I_{k-1}) when poses did not move).
+__global__ void k_energy_sum(const int* __restrict__ ncand, int n_out, int stride, int kb, int b0, int b1,
+                             const float* __restrict__ base, const float* __restrict__ part, float* __restrict__ out) {
+  const int a = blockIdx.x, h = threadIdx.x;
+  const int n = ncand[a];
+  if (n <= n_out || h >= n) return;
+  const size_t idx = static_cast<size_t>(a) * stride + h;
+  float E = base ? base[idx] : 0.0f;
+  for (int b = b0; b <= b1; ++b) E = __fadd_rn(E, part[idx * kb + b]);
+  out[idx] = E;
 }
 
 // ================================ K7: cull / halving ========================================
@@ -455,9 +684,17 @@ __global__ void __launch_bounds__(128) k_lm(FrameRefs fr, PredView pv, LmArgs la
 }
 
 // ================================ K8-K10: ICP + raycast + depth-difference score ============
-// One 256-thread CTA per (frame, candidate) job. Thread l owns pixels p = l (mod 256) of
-// each pass (the canonical reduction order of DESIGN.md); per-thread partials are f32,
-// combined in f64 by a warp xor butterfly and then sequentially over the 8 warps.
+// One 8-CTA thread-block cluster (8 x 256 threads) per (frame, candidate) job. Thread
+// lane l = rank * 256 + tid owns pixels p = l (mod 2048) of every pass (the canonical
+// order of DESIGN.md). Per-thread partials are f32; each CTA widens them to f64 and
+// reduces them (warp xor butterfly, then its 8 warps in order); CTA 0 then adds the 8
+// CTA partials in rank order through distributed shared memory, solves the 6x6 system
+// and publishes the new pose, which the other CTAs read back over DSMEM.
+namespace cg = cooperative_groups;
+constexpr int kIcpCtas = 8;
+constexpr int kIcpThreads = 256;
+constexpr int kIcpLanes = kIcpCtas * kIcpThreads;
+
 struct IcpArgs {
   int cand_stride, n_cand_jobs;  // jobs per frame (1 for icp/raw, n_out for ranked)
   int do_icp;
@@ -466,52 +703,104 @@ struct IcpArgs {
 };
 
 template <int NV>
-__device__ __forceinline__ void block_reduce_f32(const float* v, double (*red)[32], double* out) {
-  constexpr int nv = NV;
+__device__ __forceinline__ void cta_reduce_f32(const float* v, double (*red)[32], double* out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < nv; ++k) {
+  for (int k = 0; k < NV; ++k) {
     const double s = warp_sum_xor(static_cast<double>(v[k]));
     if (lane == 0) red[wid][k] = s;
   }
   __syncthreads();
-  if (threadIdx.x < nv) {
+  if (threadIdx.x < NV) {
     double s = red[0][threadIdx.x];
-    for (int w = 1; w < (kLanes / 32); ++w) s = s + red[w][threadIdx.x];
+    for (int w = 1; w < kIcpThreads / 32; ++w) s = s + red[w][threadIdx.x];
     out[threadIdx.x] = s;
   }
   __syncthreads();
 }
 
-__device__ __forceinline__ int block_isum(int v, int* ired) {
+// Warp 0 builds the ascending list of primitives that can be seen from (R, o) with the
+// given intrinsics; the ray casts of the pass then only test those (identical hits).
+__device__ __forceinline__ void build_plist(const Prim* prims, int nprims, const float R[9], const float o[3],
+                                            float fx, float fy, float cx, float cy, int W, int H,
+                                            unsigned char* list, int* count) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int i0 = 0; i0 < nprims; i0 += 32) {
+      const int i = i0 + lane;
+      const bool in = i < nprims && prim_in_view(prims[i], R, o, fx, fy, cx, cy, W, H);
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      if (in) list[base + __popc(bal & ((1u << lane) - 1u))] = static_cast<unsigned char>(i);
+      base += __popc(bal);
+    }
+    if (lane == 0) *count = base;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int cta_isum(int v, int* ired) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   v = warp_isum(v);
   if (lane == 0) ired[wid] = v;
   __syncthreads();
   int s = 0;
-  for (int w = 0; w < kLanes / 32; ++w) s += ired[w];
+  for (int w = 0; w < kIcpThreads / 32; ++w) s += ired[w];
   __syncthreads();
   return s;
 }
 
-__global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, FrameRefs fr, const Prim* __restrict__ prims,
-                                                   int nprims, const Pose* __restrict__ cand,
-                                                   const int* __restrict__ ncand, uint2* __restrict__ maps,
-                                                   Pose* __restrict__ out_pose, int* __restrict__ out_conv,
-                                                   double* __restrict__ out_rms, double* __restrict__ out_inl,
-                                                   double* __restrict__ out_score, unsigned long long* __restrict__ work) {
-  __shared__ double red[kLanes / 32][32];
-  __shared__ double tot[32];
-  __shared__ int ired[kLanes / 32];
-  __shared__ Pose Ts;
+// Gauss-Newton step of ICP on the reduced normal equations (one thread): damped 6x6
+// Cholesky solve, T <- exp(delta) T. Kept out of line (and un-unrolled) so its f64
+// temporaries do not set the register budget of the pixel loops.
+__device__ __noinline__ bool icp_step(const double* tot, Pose* T) {
+  double M[36], rhs[6], delta[6];
+  int k = 0;
+#pragma unroll 1
+  for (int p = 0; p < 6; ++p)
+#pragma unroll 1
+    for (int q = p; q < 6; ++q, ++k) {
+      M[6 * p + q] = tot[k];
+      M[6 * q + p] = tot[k];
+    }
+  const double mu = 1e-6 * ((((((tot[0] + tot[6]) + tot[11]) + tot[15]) + tot[18]) + tot[20]) / 6.0);
+#pragma unroll 1
+  for (int p = 0; p < 6; ++p) {
+    rhs[p] = -tot[21 + p];
+    M[6 * p + p] = M[6 * p + p] + mu;
+  }
+  if (!chol6(M, rhs, delta)) return false;
+  Pose D, Tn;
+  exp_se3(delta, D);
+  pose_compose(D, *T, Tn);
+  *T = Tn;
+  return true;
+}
+
+__global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 3)
+    k_icp_score(IcpArgs ia, FrameGeom g, FrameRefs fr, const Prim* __restrict__ prims, int nprims,
+                const Pose* __restrict__ cand, const int* __restrict__ ncand, uint2* __restrict__ maps,
+                Pose* __restrict__ out_pose, int* __restrict__ out_conv, double* __restrict__ out_rms,
+                double* __restrict__ out_inl, double* __restrict__ out_score, unsigned long long* __restrict__ work) {
+  __shared__ double red[kIcpThreads / 32][32];
+  __shared__ double part[32];   // this CTA's f64 partials (read by CTA 0 over DSMEM)
+  __shared__ int ipart[4];
+  __shared__ int ired[kIcpThreads / 32];
+  __shared__ Pose Ts;           // current estimate (authoritative copy in CTA 0)
   __shared__ int stop_level;
-  const int job = ia.job0 + blockIdx.x;
+  __shared__ unsigned char s_plist[256];
+  __shared__ int s_pn;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int lane_id = rank * kIcpThreads + threadIdx.x;
+  const int jl = blockIdx.x / kIcpCtas;  // job within this launch
+  const int job = ia.job0 + jl;
   const int a = job / ia.n_cand_jobs, c = job % ia.n_cand_jobs;
-  if (c >= ncand[a]) return;
+  if (c >= ncand[a]) return;  // uniform over the cluster
   const int f = fr.fidx[a];
   const size_t cidx = static_cast<size_t>(a) * ia.cand_stride + c;
   const uint2* tex = fr.tex + static_cast<size_t>(f) * g.W * g.H;
-  uint2* map = maps + static_cast<size_t>(blockIdx.x) * ia.map_stride;
+  uint2* map = maps + static_cast<size_t>(jl) * ia.map_stride;
   if (threadIdx.x == 0) Ts = cand[cidx];
   __syncthreads();
   int last_inl = 0, last_valid = 0;
@@ -537,18 +826,21 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
         tr[i] = static_cast<float>(Tref.t[i]);
         ti[i] = static_cast<float>(Tinv.t[i]);
       }
-      // K8: model map of this level at the reference pose
-      if (work && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(Wl * Hl));
-      for (int p = threadIdx.x; p < Wl * Hl; p += blockDim.x) {
+      // K8: model map of this level at the reference pose (split over the cluster)
+      if (work && rank == 0 && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(Wl * Hl));
+      build_plist(prims, nprims, Rr, tr, fxl, fyl, cxl, cyl, Wl, Hl, s_plist, &s_pn);
+      const int npl = s_pn;
+      if (work && rank == 0 && threadIdx.x == 0)
+        atomicAdd(&work[W_RAY_PRIMS], static_cast<unsigned long long>(Wl * Hl) * npl);
+      for (int p = lane_id; p < Wl * Hl; p += kIcpLanes) {
         float d[3];
         ray_dir(Rr, fxl, fyl, cxl, cyl, p % Wl, p / Wl, d);
-        const Hit h = raycast(prims, nprims, tr, d);
+        const Hit h = raycast_list(prims, s_plist, npl, tr, d);
         uint2 v = make_uint2(0u, 0xffffffffu);
         if (h.prim >= 0 && h.t <= kRenderMaxDepth) v = make_uint2(__float_as_uint(h.t), h.prim | (h.face << 16));
         map[p] = v;
       }
-      if (threadIdx.x == 0) stop_level = 0;
-      __syncthreads();
+      cluster.sync();  // map complete and visible to the whole cluster
       const int iters = level == 2 ? 10 : (level == 1 ? 5 : 4);
       for (int it = 0; it < iters; ++it) {
         const Pose T = Ts;
@@ -562,7 +854,7 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
         for (int k = 0; k < 28; ++k) acc[k] = 0.0f;
         int inl = 0, valid = 0;
         // K9: projective point-to-plane association + normal equations
-        for (int p = threadIdx.x; p < Wl * Hl; p += blockDim.x) {
+        for (int p = lane_id; p < Wl * Hl; p += kIcpLanes) {
           const int x = p % Wl, y = p / Wl;
           const float dl = __uint_as_float(tex[(y * fs) * g.W + x * fs].x);
           if (!depth_valid(dl)) continue;
@@ -611,61 +903,81 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
           acc[27] = __fmaf_rn(r, r, acc[27]);
           ++inl;
         }
-        block_reduce_f32<28>(acc, red, tot);
-        const int inl_t = block_isum(inl, ired);
-        const int valid_t = block_isum(valid, ired);
-        if (work && threadIdx.x == 0) atomicAdd(&work[W_ICP_TERMS], static_cast<unsigned long long>(valid_t));
-        if (level == 0) {
-          last_inl = inl_t;
-          last_valid = valid_t;
-          last_r2 = tot[27];
+        cta_reduce_f32<28>(acc, red, part);
+        const int inl_c = cta_isum(inl, ired);
+        const int valid_c = cta_isum(valid, ired);
+        if (threadIdx.x == 0) {
+          ipart[0] = inl_c;
+          ipart[1] = valid_c;
+        }
+        cluster.sync();  // [A] all CTA partials written
+        if (rank == 0) {
+          if (threadIdx.x < 28) {
+            double tot = part[threadIdx.x];
+            for (int r = 1; r < kIcpCtas; ++r) tot = tot + cluster.map_shared_rank(part, r)[threadIdx.x];
+            red[0][threadIdx.x] = tot;
+          }
+          if (threadIdx.x == 32) {
+            int inl_t = 0, valid_t = 0;
+            for (int r = 0; r < kIcpCtas; ++r) {
+              inl_t += cluster.map_shared_rank(ipart, r)[0];
+              valid_t += cluster.map_shared_rank(ipart, r)[1];
+            }
+            ired[0] = inl_t;
+            ired[1] = valid_t;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            const double* tot = red[0];
+            const int inl_t = ired[0];
+            if (work) atomicAdd(&work[W_ICP_TERMS], static_cast<unsigned long long>(ired[1]));
+            if (level == 0) {
+              ipart[2] = inl_t;
+              ipart[3] = ired[1];
+              part[28] = tot[27];
+            }
+            stop_level = (inl_t < 6 || !icp_step(tot, &Ts)) ? 1 : 0;
+          }
+        }
+        cluster.sync();  // [B] pose / stop flag published by CTA 0
+        if (rank != 0) {
+          if (threadIdx.x == 0) {
+            Ts = *cluster.map_shared_rank(&Ts, 0);
+            stop_level = *cluster.map_shared_rank(&stop_level, 0);
+          }
+          __syncthreads();
+        }
+        if (level == 0 && rank == 0) {
+          last_inl = ipart[2];
+          last_valid = ipart[3];
+          last_r2 = part[28];
           have_stats = true;
         }
-        if (threadIdx.x == 0) {
-          bool stop = inl_t < 6;
-          if (!stop) {
-            double M[36], rhs[6], delta[6];
-            int k = 0;
-            for (int p = 0; p < 6; ++p)
-              for (int q = p; q < 6; ++q, ++k) {
-                M[6 * p + q] = tot[k];
-                M[6 * q + p] = tot[k];
-              }
-            const double mu = 1e-6 * ((((((tot[0] + tot[6]) + tot[11]) + tot[15]) + tot[18]) + tot[20]) / 6.0);
-            for (int p = 0; p < 6; ++p) {
-              rhs[p] = -tot[21 + p];
-              M[6 * p + p] = M[6 * p + p] + mu;
-            }
-            if (!chol6(M, rhs, delta)) {
-              stop = true;
-            } else {
-              Pose D, Tn;
-              exp_se3(delta, D);
-              pose_compose(D, Ts, Tn);
-              Ts = Tn;
-            }
-          }
-          stop_level = stop ? 1 : 0;
-        }
-        __syncthreads();
         if (stop_level) break;
       }
-      __syncthreads();
+      cluster.sync();  // everyone is done with this level's map before it is overwritten
     }
   }
   const Pose Tf = Ts;
   int conv = 1;
   double rms = 0.0, inlf = 0.0;
-  if (ia.do_icp) {
-    if (have_stats && last_valid > 0 && last_inl > 0) {
-      inlf = static_cast<double>(last_inl) / static_cast<double>(last_valid);
-      rms = sqrt(last_r2 / static_cast<double>(last_inl));
-      conv = (inlf >= 0.5 && rms <= 0.02) ? 1 : 0;
-    } else {
-      inlf = 0.0;
-      rms = __longlong_as_double(0x7ff0000000000000ll);
-      conv = 0;
+  if (ia.do_icp) {  // only CTA 0 holds the statistics; broadcast the decision
+    if (rank == 0) {
+      if (have_stats && last_valid > 0 && last_inl > 0) {
+        inlf = static_cast<double>(last_inl) / static_cast<double>(last_valid);
+        rms = sqrt(last_r2 / static_cast<double>(last_inl));
+        conv = (inlf >= 0.5 && rms <= 0.02) ? 1 : 0;
+      } else {
+        inlf = 0.0;
+        rms = __longlong_as_double(0x7ff0000000000000ll);
+        conv = 0;
+      }
+      if (threadIdx.x == 0) stop_level = conv;
     }
+    cluster.sync();
+    if (rank != 0 && threadIdx.x == 0) stop_level = *cluster.map_shared_rank(&stop_level, 0);
+    __syncthreads();
+    conv = stop_level;
   }
   double score = __longlong_as_double(0x7ff0000000000000ll);
   if (conv) {
@@ -677,11 +989,15 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
     for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(Tf.t[i]);
     float sum = 0.0f;
     int mutual = 0, synth = 0;
-    if (work && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(g.W * g.H));
-    for (int p = threadIdx.x; p < g.W * g.H; p += blockDim.x) {
+    if (work && rank == 0 && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(g.W * g.H));
+    build_plist(prims, nprims, R, t, g.fx, g.fy, g.cx, g.cy, g.W, g.H, s_plist, &s_pn);
+    const int npl = s_pn;
+    if (work && rank == 0 && threadIdx.x == 0)
+      atomicAdd(&work[W_RAY_PRIMS], static_cast<unsigned long long>(g.W * g.H) * npl);
+    for (int p = lane_id; p < g.W * g.H; p += kIcpLanes) {
       float d[3];
       ray_dir(R, g.fx, g.fy, g.cx, g.cy, p % g.W, p / g.W, d);
-      const Hit h = raycast(prims, nprims, t, d);
+      const Hit h = raycast_list(prims, s_plist, npl, t, d);
       if (h.prim < 0 || !(h.t <= kRenderMaxDepth) || !depth_valid(h.t)) continue;
       ++synth;
       const float dl = __uint_as_float(tex[p].x);
@@ -689,15 +1005,29 @@ __global__ void __launch_bounds__(256) k_icp_score(IcpArgs ia, FrameGeom g, Fram
       ++mutual;
       sum = __fadd_rn(sum, fabsf(__fsub_rn(dl, h.t)));
     }
-    block_reduce_f32<1>(&sum, red, tot);
-    const int mutual_t = block_isum(mutual, ired);
-    const int synth_t = block_isum(synth, ired);
-    if (static_cast<double>(synth_t) < 0.1 * static_cast<double>(g.W) * static_cast<double>(g.H) || mutual_t == 0)
-      score = __longlong_as_double(0x7ff0000000000000ll);
-    else
-      score = tot[0] / static_cast<double>(mutual_t);
+    cta_reduce_f32<1>(&sum, red, part);
+    const int mutual_c = cta_isum(mutual, ired);
+    const int synth_c = cta_isum(synth, ired);
+    if (threadIdx.x == 0) {
+      ipart[0] = mutual_c;
+      ipart[1] = synth_c;
+    }
+    cluster.sync();
+    if (rank == 0 && threadIdx.x == 0) {
+      double tot = part[0];
+      int mutual_t = ipart[0], synth_t = ipart[1];
+      for (int r = 1; r < kIcpCtas; ++r) {
+        tot = tot + cluster.map_shared_rank(part, r)[0];
+        mutual_t += cluster.map_shared_rank(ipart, r)[0];
+        synth_t += cluster.map_shared_rank(ipart, r)[1];
+      }
+      if (!(static_cast<double>(synth_t) < 0.1 * static_cast<double>(g.W) * static_cast<double>(g.H) ||
+            mutual_t == 0))
+        score = tot / static_cast<double>(mutual_t);
+    }
+    cluster.sync();  // keep every CTA's shared memory alive until CTA 0 has read it
   }
-  if (threadIdx.x == 0) {
+  if (rank == 0 && threadIdx.x == 0) {
     out_pose[cidx] = Tf;
     out_conv[cidx] = conv;
     out_rms[cidx] = rms;
@@ -765,6 +1095,7 @@ FrameRefs frame_refs(scr_scene s) {
   fr.gcam = s->ws.gcam;
   fr.gslot = s->ws.gslot;
   fr.gnm = s->ws.gnm;
+  fr.grec = s->ws.grec;
   fr.tex = s->ws.tex;
   fr.gmax = s->ws.gmax;
   fr.T = s->T;
@@ -805,6 +1136,10 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   }
   const int K = halvings(p.n_cull, p.n_out);
   const int scap = p.eta * (K + 1);
+  if (K + 1 > kEnergyBatches || p.eta > kEnergySampleCap) {
+    set_error("ransac params: eta <= 512 and at most 7 sample batches (n_cull / n_out <= 64)");
+    return SCR_E_ARG;
+  }
   SCR_TRY(ensure_ransac_ws(s, p.n_max, p.n_cull, scap));
   const int jobs_per = mode == SCR_MODE_RANKED ? std::min(p.n_out, p.n_cull) : 1;
   SCR_TRY(ensure_icp_ws(s, std::min(nA * jobs_per, 1024)));
@@ -812,15 +1147,20 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   const PredView pv = s->pred_view();
   GenParams gp{p.max_gen_iters, p.n_max, p.min_sq_dist, p.colour_thresh, p.rigidity_tol};
   unsigned long long* wk = work_ptr(s);
+  SCR_CUDA(cudaMemsetAsync(w.hctr, 0, nA * sizeof(int), s->stream));  // per-frame slot counters
+  const int gen_threads = std::min(p.n_max, kGenThreadsPerFrame);
   SCR_LAUNCH(s, K_HYPGEN,
-             (k_hypgen<<<dim3((p.n_max + 127) / 128, nA), 128, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds, w.hyp,
-                                                                              w.hok, w.hiters, wk)));
+             (k_hypgen<<<dim3((gen_threads + 127) / 128, nA), 128, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds,
+                                                                                  w.hctr, w.hyp, w.hok, w.hiters,
+                                                                                  wk)));
   SCR_LAUNCH(s, K_SAMPLES,
              (k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, 0, w.samples_cap,
                                                                    w.samples)));
-  SCR_LAUNCH(s, K_ENERGY,
-             (k_energy<<<dim3((p.n_max + 127) / 128, nA), 128, 0, s->stream>>>(
-                 fr, pv, w.hyp, w.hok, p.n_max, nullptr, -1, w.samples, w.samples_cap, p.eta, w.henergy, wk)));
+  const size_t esmem = static_cast<size_t>(kEnergyModeCap) * 3 * sizeof(float4);
+  {
+    EnergyArgs ea{w.hyp, w.hok, p.n_max, nullptr, -1, w.samples, w.samples_cap, p.eta, 0, w.henergy, 0};
+    SCR_LAUNCH(s, K_ENERGY, (k_energy<<<dim3((p.n_max + 255) / 256, 1, nA), 256, esmem, s->stream>>>(ea, fr, pv, wk)));
+  }
   int P = 1;
   while (P < p.n_max) P <<= 1;
   SCR_LAUNCH(s, K_SELECT,
@@ -839,11 +1179,19 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
                  (k_lm<<<dim3((p.n_cull + 3) / 4, nA), 128, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand,
                                                                             w.assoc, wk)));
     }
-    // rescore (only frames still above n_out take part); henergy is scratch [nA * ncull_cap]
-    SCR_LAUNCH(s, K_ENERGY,
-               (k_energy<<<dim3((p.n_cull + 127) / 128, nA), 128, 0, s->stream>>>(
-                   fr, pv, w.cand, nullptr, w.ncull_cap, w.ncand, p.n_out, w.samples, w.samples_cap, ns, w.henergy,
-                   wk)));
+    // rescore (only frames still above n_out take part): per-batch partial energies, then
+    // E(I_k) = E(I_{k-1}) + E_k without LM (poses unchanged), or the full batch sum with LM
+    {
+      const int b0 = p.pose_update ? 0 : k;
+      EnergyArgs ea{w.cand, nullptr, w.ncull_cap, w.ncand, p.n_out, w.samples, w.samples_cap, p.eta, b0, w.epart,
+                    kEnergyBatches};
+      const size_t smem_small = static_cast<size_t>(kSmallHyps) * (p.eta + 1) * sizeof(float);
+      SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<dim3(1, k - b0 + 1, nA), 256, smem_small, s->stream>>>(ea, fr, pv,
+                                                                                                        wk)));
+      SCR_LAUNCH(s, K_ENERGY, (k_energy_sum<<<nA, 64, 0, s->stream>>>(w.ncand, p.n_out, w.ncull_cap, kEnergyBatches,
+                                                                      b0, k, p.pose_update ? nullptr : w.cenergy,
+                                                                      w.epart, w.henergy)));
+    }
     int Pc = 1;
     while (Pc < p.n_cull) Pc <<= 1;
     SCR_LAUNCH(s, K_SELECT,
@@ -859,7 +1207,7 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
     IcpArgs ia{w.ncull_cap, jobs_per, mode != SCR_MODE_RAW ? 1 : 0, j0,
                static_cast<size_t>(s->k.width) * s->k.height};
     SCR_LAUNCH(s, K_ICP,
-               (k_icp_score<<<nj, 256, 0, s->stream>>>(ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand,
+               (k_icp_score<<<nj * kIcpCtas, kIcpThreads, 0, s->stream>>>(ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand,
                                                        w.icp_map, w.icp_pose, w.icp_conv, w.icp_rms, w.icp_inl,
                                                        w.icp_score, wk)));
   }
@@ -871,6 +1219,14 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
 }
 
 }  // namespace
+
+scr_status reloc_init() {
+  SCR_CUDA(cudaFuncSetAttribute(k_energy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kEnergyModeCap * 3 * sizeof(float4))));
+  SCR_CUDA(cudaFuncSetAttribute(k_energy_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmallHyps * (kEnergySampleCap + 1) * sizeof(float))));
+  return SCR_OK;
+}
 
 scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int scap) {
   Workspace& w = s->ws;
@@ -895,6 +1251,7 @@ scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int scap) {
     SCR_TRY(grow(&w.icp_conv, B * nc));
     SCR_TRY(grow(&w.icp_rms, B * nc));
     SCR_TRY(grow(&w.icp_inl, B * nc));
+    SCR_TRY(grow(&w.epart, B * nc * kEnergyBatches));
     w.ncull_cap = nc;
     w.samples_cap = sc;
     if (w.henergy && static_cast<size_t>(w.nmax_cap) < static_cast<size_t>(nc)) {
@@ -1118,7 +1475,7 @@ scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, 
   SCR_CUDA(cudaMemcpyAsync(s->ws.cand, init, sizeof(Pose), cudaMemcpyHostToDevice, s->stream));
   IcpArgs ia{s->ws.ncull_cap, 1, 1, 0, WH};
   SCR_LAUNCH(s, K_ICP,
-             (k_icp_score<<<1, 256, 0, s->stream>>>(ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand,
+             (k_icp_score<<<kIcpCtas, kIcpThreads, 0, s->stream>>>(ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand,
                                                     s->ws.ncand, s->ws.icp_map, s->ws.icp_pose, s->ws.icp_conv,
                                                     s->ws.icp_rms, s->ws.icp_inl, s->ws.icp_score, nullptr)));
   SCR_CUDA(cudaGetLastError());

@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(1024) k_grid(const uint2* __restrict__ tex, in
 __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, const uint2* __restrict__ tex,
                                                 const int* __restrict__ gcount, const int* __restrict__ gpx,
                                                 int gmax, int* __restrict__ gslot, int* __restrict__ gnm,
-                                                float4* __restrict__ gcam, const int* __restrict__ pcount,
-                                                unsigned long long* __restrict__ work) {
+                                                float4* __restrict__ gcam, int4* __restrict__ grec,
+                                                const int* __restrict__ pcount, unsigned long long* __restrict__ work) {
   __shared__ short4 sspec[kFeatures];
   for (int i = threadIdx.x; i < kFeatures; i += blockDim.x) sspec[i] = fv.specs[i];
   __syncthreads();
@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
   const uint2 c = T[y * W + x];
   const float d = __uint_as_float(c.x);
   int nm = 0, visits = 0;
+  uint32_t counts = 0;
   for (int t = 0; t < fv.T; ++t) {
     const int nb = fv.node_base[t];
     int node = nb;
@@ -176,9 +177,15 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
     }
     const int slot = fv.leaf_base[t] + leaf;
     gslot[gidx * fv.T + t] = slot;
-    if (pcount) nm += pcount[slot];
+    const int cnt = pcount ? pcount[slot] : 0;
+    nm += cnt;
+    if (t < 5) counts |= static_cast<uint32_t>(cnt) << (6 * t);
   }
   gnm[gidx] = nm;
+  // packed per-pixel record for hypothesis generation: pixel, depth, colour + |M(u)|,
+  // per-tree mode counts (6 bits each, trees 0..4)
+  grec[gidx] = make_int4(px, static_cast<int>(c.x), static_cast<int>((c.y & 0xffffffu) | (min(nm, 255) << 24)),
+                         static_cast<int>(counts));
   if (work) atomicAdd(&work[W_NODE_VISITS], static_cast<unsigned long long>(visits));
   const double dd = static_cast<double>(d);
   const double X = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
@@ -740,9 +747,11 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   if ((st = dalloc(&w.gcam, B * w.gmax)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.gslot, B * w.gmax * s->T)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.grec, B * w.gmax)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.fidx, B)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.status, B)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.hctr, B)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.ins_cnt, L)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.ins_off, L + 1)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.ins_cur, L)) != SCR_OK) return fail(st);
@@ -753,6 +762,7 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   if ((st = scr_reset(s)) != SCR_OK) return fail(st);
   e = cudaFuncSetAttribute(k_rqs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return fail(cuda_fail(e, "cudaFuncSetAttribute(k_rqs)"));
+  if ((st = reloc_init()) != SCR_OK) return fail(st);
   e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "scene create sync"));
   *out = s;
@@ -768,7 +778,7 @@ void scr_scene_destroy(scr_scene s) {
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
-                  s->ws.status, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
+                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
                   s->ws.ins_rank, s->ws.ins_total};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -811,7 +821,10 @@ int64_t scr_kernel_launches(scr_scene s) { return s ? s->launches : 0; }
 int64_t scr_update_cursor(scr_scene s) { return s ? s->cursor : 0; }
 
 scr_status scr_scene_set_analytic_model(scr_scene s, const scr_prim* prims, int n) {
-  if (!s || (!prims && n > 0) || n < 0) return SCR_E_ARG;
+  if (!s || (!prims && n > 0) || n < 0 || n > 256) {
+    set_error("scr_scene_set_analytic_model: 0..256 primitives");
+    return SCR_E_ARG;
+  }
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   std::vector<Prim> p(n);
   for (int i = 0; i < n; ++i) {
@@ -867,8 +880,8 @@ scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_
   SCR_LAUNCH(s, K_GRID, (k_grid<<<n, 1024, 0, s->stream>>>(w.tex, W, H, w.gmax, w.gcount, w.gpx)));
   SCR_LAUNCH(s, K_LEAVES,
              (k_leaves<<<dim3((w.gmax + 127) / 128, n), 128, 0, s->stream>>>(
-                 s->forest_view(), s->geom, w.tex, w.gcount, w.gpx, w.gmax, w.gslot, w.gnm, w.gcam, s->d_count,
-                 work_ptr(s))));
+                 s->forest_view(), s->geom, w.tex, w.gcount, w.gpx, w.gmax, w.gslot, w.gnm, w.gcam, w.grec,
+                 s->d_count, work_ptr(s))));
   SCR_CUDA(cudaGetLastError());
   return SCR_OK;
 }

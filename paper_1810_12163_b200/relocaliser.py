@@ -175,14 +175,14 @@ class Scene:
         N.check(self.lib.scr_profile_enable(self.handle, 1 if enable else 0), "scr_profile_enable")
 
     WORK_NAMES = ("mode_evals", "sample_evals", "lm_terms", "icp_terms", "rays", "node_visits", "gen_attempts",
-                  "lm_assoc_evals")
+                  "lm_assoc_evals", "ray_prim_tests")
 
     def profile_read(self) -> dict:
         cap = 32
         names = (C.c_char_p * cap)()
         ms = (C.c_double * cap)()
         n = (C.c_int64 * cap)()
-        work = (C.c_uint64 * 8)()
+        work = (C.c_uint64 * 16)()
         k = self.lib.scr_profile_read(self.handle, names, ms, n, work, cap)
         kernels = {names[i].decode(): {"ms": ms[i], "launches": n[i]} for i in range(k)}
         return {"kernels": kernels, "work": {w: int(work[i]) for i, w in enumerate(self.WORK_NAMES)}}
