@@ -74,6 +74,7 @@ struct Workspace {
   int* gslot = nullptr;       // [cap * gmax * T]
   int* gnm = nullptr;         // [cap * gmax] number of modes (union over trees)
   int4* grec = nullptr;       // [cap * gmax] {x|y<<16, depth bits, rgb | nm<<24, 6-bit counts of trees 0..4}
+  uint4* gleaf = nullptr;     // [cap * gmax] 16-bit leaf ids of trees 0..7
   // RANSAC (grown on demand)
   int nmax_cap = 0, ncull_cap = 0, samples_cap = 0;
   Pose* hyp = nullptr;        // [cap * nmax]
@@ -85,6 +86,7 @@ struct Workspace {
   int* cslot = nullptr;       // [cap * ncull]
   int* ncand = nullptr;       // [cap]
   float* epart = nullptr;     // per-batch partial energies [cap * ncull * kEnergyBatches]
+  void* lmst = nullptr;       // LM state per candidate [cap * ncull]
   int* samples = nullptr;     // [cap * samples_cap]
   int* assoc = nullptr;       // [cap * ncull * samples_cap]
   // ranking / ICP
@@ -127,6 +129,7 @@ struct scr_scene_s {
   int64_t L = 0;
   int64_t cursor = 0;
   std::vector<int> node_base, leaf_base;
+  bool leaves16 = true;  // every tree has <= 65536 leaves (16-bit leaf ids in gleaf)
   int4* d_nodes = nullptr;
   short4* d_specs = nullptr;
   scr_entry* d_entries = nullptr;

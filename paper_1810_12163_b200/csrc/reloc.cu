@@ -30,6 +30,8 @@ struct GenParams {
   double min_sq_dist;
   float colour_thresh;
   double rigidity_tol;
+  int fast;  // per-pixel records usable (<= 5 trees, 16-bit leaf ids)
+  int leaf_base[kMaxTrees];
 };
 
 struct FrameRefs {  // per-batch views of the packed frames
@@ -40,6 +42,7 @@ struct FrameRefs {  // per-batch views of the packed frames
   const int* gslot;
   const int* gnm;
   const int4* grec;
+  const uint4* gleaf;
   const uint2* tex;
   int gmax, T;
 };
@@ -57,11 +60,17 @@ SCR_DEV int mode_index(const FrameRefs& fr, const int* pcount, size_t gbase, int
 // ================================ K4: hypothesis generation ================================
 // Generation slots are independent (slot s draws from Rng::stream(seed, s) and retries up
 // to max_iters; draw order and checks per DESIGN.md A1/A7), so lanes pull
-// slots from a per-frame atomic counter and never idle behind a slower lane. An attempt
-// reads the 16-byte per-pixel records written by K1 (pixel, depth, colour, per-tree mode
-// counts), so the colour check needs one slot + one colour load; the world points of the
-// other two modes are only fetched when it passes. Uniform draws use exact Barrett
-// reductions with precomputed reciprocals/thresholds (same values as the 64-bit modulo).
+// slots from a per-frame atomic counter and never idle behind a slower lane.
+// Latency is the cost here (most attempts are rejected), so an attempt is arranged as
+// few dependent memory hops as possible:
+//  * the 7 raw xoshiro outputs an attempt can consume are buffered; assuming no
+//    rejection-sampling retry inside uniform_int (probability ~1e-15, detected exactly and
+//    replayed on the exact sequential path), all three pixel indices are known up front
+//    and their 32-byte records (pixel, depth, colour, |M(u)|, per-tree mode counts, 16-bit
+//    leaf ids, written by K1) are loaded together;
+//  * mode indices come from the records (no slot lookup), so the colour check needs one
+//    more load and the other two modes' world points are fetched only when it passes;
+//  * uniform draws use exact Barrett reductions (same values as the 64-bit modulo).
 constexpr int kMaxModeUnion = kMaxTrees * kMaxModes;
 constexpr int kGenThreadsPerFrame = 2048;
 
@@ -72,16 +81,38 @@ SCR_DEV uint64_t draw(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
   }
 }
 
-SCR_DEV int pick_mode(const FrameRefs& fr, const int* pcount, size_t gb, uint32_t counts, bool fast, int pick) {
-  if (fast) {
-    for (int t = 0; t < fr.T; ++t) {
-      const int c = static_cast<int>((counts >> (6 * t)) & 63u);
-      if (pick < c) return fr.gslot[gb * fr.T + t] * kMaxModes + pick;
-      pick -= c;
-    }
-    return -1;
+struct RawBuf {  // next 7 raw outputs of the slot's stream
+  uint64_t b0, b1, b2, b3, b4, b5, b6;
+  SCR_DEV void fill(Rng& r) {
+    b0 = rng_next(r); b1 = rng_next(r); b2 = rng_next(r); b3 = rng_next(r);
+    b4 = rng_next(r); b5 = rng_next(r); b6 = rng_next(r);
   }
-  return mode_index(fr, pcount, gb, pick);
+  SCR_DEV uint64_t pop(Rng& r) {
+    const uint64_t v = b0;
+    b0 = b1; b1 = b2; b2 = b3; b3 = b4; b4 = b5; b5 = b6;
+    b6 = rng_next(r);
+    return v;
+  }
+  SCR_DEV uint64_t draw(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
+    for (;;) {
+      const uint64_t v = pop(r);
+      if (v >= thr) return mod_barrett(v, n, m);
+    }
+  }
+};
+
+// mode index of pick-th predicted mode of a pixel (union over trees in tree order)
+SCR_DEV int mode_from_record(const GenParams& gp, int T, uint32_t counts, uint4 lv, int pick) {
+  for (int t = 0; t < T; ++t) {
+    const int c = static_cast<int>((counts >> (6 * t)) & 63u);
+    if (pick < c) {
+      const uint32_t w = t < 2 ? lv.x : (t < 4 ? lv.y : (t < 6 ? lv.z : lv.w));
+      const int leaf = static_cast<int>((w >> (16 * (t & 1))) & 0xffffu);
+      return (gp.leaf_base[t] + leaf) * kMaxModes + pick;
+    }
+    pick -= c;
+  }
+  return -1;
 }
 
 // Kabsch (f64 SVD) runs only for triplets that passed every check; out of line so it does
@@ -89,9 +120,9 @@ SCR_DEV int pick_mode(const FrameRefs& fr, const int* pcount, size_t gb, uint32_
 __device__ __noinline__ bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return kabsch3(cm, w, *T); }
 
 __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
-                                                const uint64_t* __restrict__ seeds, int* __restrict__ slot_ctr,
-                                                Pose* __restrict__ hyp, int* __restrict__ hok,
-                                                int* __restrict__ hiters, unsigned long long* __restrict__ work) {
+                                                   const uint64_t* __restrict__ seeds, int* __restrict__ slot_ctr,
+                                                   Pose* __restrict__ hyp, int* __restrict__ hok,
+                                                   int* __restrict__ hiters, unsigned long long* __restrict__ work) {
   __shared__ uint64_t s_m[kMaxModeUnion + 1];    // Barrett reciprocal for mode counts 1..400
   __shared__ uint64_t s_thr[kMaxModeUnion + 1];  // rejection threshold (2^64 mod n)
   for (int i = threadIdx.x; i <= kMaxModeUnion; i += blockDim.x) {
@@ -106,37 +137,94 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
   const uint64_t G = static_cast<uint64_t>(fr.gcount[f]);
   const uint64_t mG = G ? barrett_m(G) : 1, tG = G ? mod_barrett(0 - G, G, mG) : 0;
   const uint64_t m3 = 0x5555555555555555ull, t3 = 1;  // floor((2^64-1)/3), 2^64 mod 3
-  const bool fast = fr.T <= 5;
+  const bool fast = gp.fast != 0;
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
   unsigned long long attempts_total = 0;
   for (int slot = atomicAdd(&slot_ctr[a], 1); slot < gp.nmax; slot = atomicAdd(&slot_ctr[a], 1)) {
     const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
     Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(slot));
+    RawBuf buf;
+    buf.fill(rng);
     int ok = 0, it = 0;
     Pose T;
     if (G > 0) {
       for (it = 0; it < gp.max_iters; ++it) {
-        int4 rec[3];
-        int pick[3], gix[3];
-        bool good = true;
-#pragma unroll 1
-        for (int k = 0; k < 3; ++k) {
-          const int gi = static_cast<int>(draw(rng, G, mG, tG));
-          gix[k] = gi;
-          rec[k] = fr.grec[fbase + gi];
-          const int nm = fast ? (static_cast<uint32_t>(rec[k].z) >> 24) : fr.gnm[fbase + gi];
-          if (nm == 0) {
-            good = false;
-            break;
+        int4 A[3];
+        uint4 Lv[3];
+        int pick[3], gix[3], cc = 0, consumed = 0;
+        bool proceed = false;
+        const bool spec = fast && buf.b0 >= tG && buf.b2 >= tG && buf.b4 >= tG;
+        bool slow = !spec;
+        if (spec) {
+          gix[0] = static_cast<int>(mod_barrett(buf.b0, G, mG));
+          gix[1] = static_cast<int>(mod_barrett(buf.b2, G, mG));
+          gix[2] = static_cast<int>(mod_barrett(buf.b4, G, mG));
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            A[k] = fr.grec[fbase + gix[k]];
+            Lv[k] = fr.gleaf[fbase + gix[k]];
           }
-          pick[k] = static_cast<int>(draw(rng, static_cast<uint64_t>(nm), s_m[nm], s_thr[nm]));
+          const int nm0 = static_cast<uint32_t>(A[0].z) >> 24;
+          const int nm1 = static_cast<uint32_t>(A[1].z) >> 24;
+          const int nm2 = static_cast<uint32_t>(A[2].z) >> 24;
+          if (nm0 == 0) {
+            consumed = 1;
+          } else if (buf.b1 < s_thr[nm0]) {
+            slow = true;
+          } else {
+            pick[0] = static_cast<int>(mod_barrett(buf.b1, nm0, s_m[nm0]));
+            if (nm1 == 0) {
+              consumed = 3;
+            } else if (buf.b3 < s_thr[nm1]) {
+              slow = true;
+            } else {
+              pick[1] = static_cast<int>(mod_barrett(buf.b3, nm1, s_m[nm1]));
+              if (nm2 == 0) {
+                consumed = 5;
+              } else if (buf.b5 < s_thr[nm2]) {
+                slow = true;
+              } else {
+                pick[2] = static_cast<int>(mod_barrett(buf.b5, nm2, s_m[nm2]));
+                if (buf.b6 < t3) {
+                  slow = true;
+                } else {
+                  cc = static_cast<int>(mod_barrett(buf.b6, 3, m3));
+                  consumed = 7;
+                  proceed = true;
+                }
+              }
+            }
+          }
         }
-        if (!good) continue;
-        const int cc = static_cast<int>(draw(rng, 3, m3, t3));
+        if (slow) {  // exact sequential replay of the attempt from the buffered stream
+          proceed = true;
+#pragma unroll 1
+          for (int k = 0; k < 3; ++k) {
+            gix[k] = static_cast<int>(buf.draw(rng, G, mG, tG));
+            A[k] = fr.grec[fbase + gix[k]];
+            Lv[k] = fr.gleaf[fbase + gix[k]];
+            const int nm = fast ? (static_cast<uint32_t>(A[k].z) >> 24) : fr.gnm[fbase + gix[k]];
+            if (nm == 0) {
+              proceed = false;
+              break;
+            }
+            pick[k] = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm), s_m[nm], s_thr[nm]));
+          }
+          if (proceed) cc = static_cast<int>(buf.draw(rng, 3, m3, t3));
+        } else {
+          switch (consumed) {  // advance the stream by the raw values this attempt used
+            case 1: buf.pop(rng); break;
+            case 3: buf.pop(rng); buf.pop(rng); buf.pop(rng); break;
+            case 5: buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); break;
+            default: buf.fill(rng); break;
+          }
+        }
+        if (!proceed) continue;
         int mi[3];
-        mi[cc] = pick_mode(fr, pv.count, fbase + gix[cc], static_cast<uint32_t>(rec[cc].w), fast, pick[cc]);
+        mi[cc] = fast ? mode_from_record(gp, fr.T, static_cast<uint32_t>(A[cc].w), Lv[cc], pick[cc])
+                      : mode_index(fr, pv.count, fbase + gix[cc], pick[cc]);
         {
-          const uint32_t col = static_cast<uint32_t>(rec[cc].z);
+          const uint32_t col = static_cast<uint32_t>(A[cc].z);
           const float4 mc = pv.col[mi[cc]];
           float linf = 0.0f;
           linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
@@ -146,7 +234,9 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
         }
 #pragma unroll
         for (int k = 0; k < 3; ++k)
-          if (k != cc) mi[k] = pick_mode(fr, pv.count, fbase + gix[k], static_cast<uint32_t>(rec[k].w), fast, pick[k]);
+          if (k != cc)
+            mi[k] = fast ? mode_from_record(gp, fr.T, static_cast<uint32_t>(A[k].w), Lv[k], pick[k])
+                         : mode_index(fr, pv.count, fbase + gix[k], pick[k]);
         double w[9], cm[9];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -154,8 +244,8 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
           w[3 * k + 0] = static_cast<double>(q0.x);
           w[3 * k + 1] = static_cast<double>(q0.y);
           w[3 * k + 2] = static_cast<double>(q0.z);
-          const int x = rec[k].x & 0xffff, y = rec[k].x >> 16;
-          const double dd = static_cast<double>(__int_as_float(rec[k].y));
+          const int x = A[k].x & 0xffff, y = A[k].x >> 16;
+          const double dd = static_cast<double>(__int_as_float(A[k].y));
           cm[3 * k + 0] = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
           cm[3 * k + 1] = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
           cm[3 * k + 2] = dd;
@@ -566,121 +656,200 @@ SCR_DEV void lm_accum(const Pose& H, const double x[3], const ModeGeom& mg, bool
   for (int a = 0; a < 6; ++a) acc[21 + a] = acc[21 + a] + ((J[0][a] * r[0] + J[1][a] * r[1]) + J[2][a] * r[2]);
 }
 
-__global__ void __launch_bounds__(128) k_lm(FrameRefs fr, PredView pv, LmArgs la, const int* __restrict__ samples,
-                                            Pose* __restrict__ cand, const int* __restrict__ ncand,
-                                            int* __restrict__ assoc, unsigned long long* __restrict__ work) {
+// LM state per (frame, candidate) lives in global memory so that each LM iteration can be
+// split into two well-shaped kernels:
+//  k_lm_assoc — warp per sample, lanes over hypotheses: nearest mode of H x (f32 metric of
+//               Eq. 5, or Euclidean without covariance) for every hypothesis that needs a
+//               fresh association; each mode is loaded once per warp (uniform load);
+//  k_lm_step  — warp per hypothesis, lanes over samples in the canonical 32-lane order:
+//               normal equations with the frozen association, damped solve, trial
+//               energy, accept/reject (identical on every lane).
+struct LmState {
+  double lambda;
+  int need_assoc, done;
+};
+
+__global__ void k_lm_init(const int* __restrict__ ncand, int n_out, int cand_stride, LmState* __restrict__ st) {
+  const int a = blockIdx.x, h = threadIdx.x;
+  if (h >= cand_stride) return;
+  LmState s;
+  s.lambda = 1e-3;
+  s.need_assoc = 1;
+  s.done = (ncand[a] <= n_out || h >= ncand[a]) ? 1 : 0;
+  st[static_cast<size_t>(a) * cand_stride + h] = s;
+}
+
+__global__ void __launch_bounds__(256) k_lm_assoc(FrameRefs fr, PredView pv, LmArgs la,
+                                                  const int* __restrict__ samples, const Pose* __restrict__ cand,
+                                                  const int* __restrict__ ncand, const LmState* __restrict__ st,
+                                                  int* __restrict__ assoc, unsigned long long* __restrict__ work) {
+  __shared__ float s_pose[kSmallHyps][12];
+  __shared__ int s_need[kSmallHyps];
+  __shared__ int s_any;
+  const int a = blockIdx.y;
+  const int n = ncand[a];
+  if (n <= la.n_out) return;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  for (int h = threadIdx.x; h < n; h += blockDim.x) {
+    const LmState ls = st[static_cast<size_t>(a) * la.cand_stride + h];
+    const int need = (!ls.done && ls.need_assoc) ? 1 : 0;
+    s_need[h] = need;
+    if (need) {
+      s_any = 1;
+      const Pose& P = cand[static_cast<size_t>(a) * la.cand_stride + h];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) s_pose[h][i] = static_cast<float>(P.R[i]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s_pose[h][9 + i] = static_cast<float>(P.t[i]);
+    }
+  }
+  __syncthreads();
+  if (!s_any) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (s >= la.ns) return;
+  const int h0 = lane, h1 = lane + 32;
+  const bool v0 = h0 < n && s_need[h0], v1 = h1 < n && s_need[h1];
+  const int f = fr.fidx[a];
+  const size_t gb = static_cast<size_t>(f) * fr.gmax + samples[static_cast<size_t>(a) * la.scap + s];
+  int best0 = -1, best1 = -1;
+  if (fr.gnm[gb] > 0 && (v0 || v1)) {
+    float R0[9], t0[3], R1[9], t1[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      R0[i] = v0 ? s_pose[h0][i] : 0.0f;
+      R1[i] = v1 ? s_pose[h1][i] : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      t0[i] = v0 ? s_pose[h0][9 + i] : 0.0f;
+      t1[i] = v1 ? s_pose[h1][9 + i] : 0.0f;
+    }
+    const float4 c = fr.gcam[gb];
+    float y0[3], y1[3];
+    xform_f32(R0, t0, c.x, c.y, c.z, y0);
+    xform_f32(R1, t1, c.x, c.y, c.z, y1);
+    float q0b = 0.0f, q1b = 0.0f;
+    for (int tt = 0; tt < fr.T; ++tt) {
+      const int slot = fr.gslot[gb * fr.T + tt];
+      const int cnt = pv.count[slot];
+      for (int m = 0; m < cnt; ++m) {
+        const int mi = slot * kMaxModes + m;
+        const float4 g0 = pv.geom[mi].q0;
+        float qa, qb;
+        const float a0 = __fsub_rn(y0[0], g0.x), a1 = __fsub_rn(y0[1], g0.y), a2 = __fsub_rn(y0[2], g0.z);
+        const float b0 = __fsub_rn(y1[0], g0.x), b1 = __fsub_rn(y1[1], g0.y), b2 = __fsub_rn(y1[2], g0.z);
+        if (la.use_cov) {
+          const float4 g1 = pv.geom[mi].q1, g2 = pv.geom[mi].q2;
+          qa = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, a0, a1, a2);
+          qb = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, b0, b1, b2);
+        } else {
+          qa = quad_eucl(a0, a1, a2);
+          qb = quad_eucl(b0, b1, b2);
+        }
+        if (best0 < 0 || qa < q0b) {  // first minimum wins ties
+          q0b = qa;
+          best0 = mi;
+        }
+        if (best1 < 0 || qb < q1b) {
+          q1b = qb;
+          best1 = mi;
+        }
+      }
+    }
+    if (work && lane == 0)
+      atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(fr.gnm[gb]) * static_cast<unsigned long long>(n));
+  }
+  if (v0) assoc[(static_cast<size_t>(a) * la.cand_stride + h0) * la.scap + s] = best0;
+  if (v1) assoc[(static_cast<size_t>(a) * la.cand_stride + h1) * la.scap + s] = best1;
+}
+
+// One LM iteration of one hypothesis, all lanes in lockstep.
+__device__ __noinline__ bool lm_solve(const double* acc, double lambda, double delta[6]) {
+  double M[36], rhs[6];
+  int k = 0;
+#pragma unroll 1
+  for (int p = 0; p < 6; ++p)
+#pragma unroll 1
+    for (int q = p; q < 6; ++q, ++k) {
+      M[6 * p + q] = acc[k];
+      M[6 * q + p] = acc[k];
+    }
+#pragma unroll 1
+  for (int p = 0; p < 6; ++p) {
+    M[6 * p + p] = M[6 * p + p] + lambda * M[6 * p + p];
+    rhs[p] = -acc[21 + p];
+  }
+  return chol6(M, rhs, delta);
+}
+
+__global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmArgs la,
+                                                 const int* __restrict__ samples, Pose* __restrict__ cand,
+                                                 const int* __restrict__ ncand, LmState* __restrict__ st,
+                                                 const int* __restrict__ assoc, unsigned long long* __restrict__ work) {
   const int a = blockIdx.y;
   const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int n = ncand[a];
   if (n <= la.n_out || h >= n) return;
+  const size_t hi = static_cast<size_t>(a) * la.cand_stride + h;
+  LmState ls = st[hi];
+  if (ls.done) return;
   const int f = fr.fidx[a];
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
   const int* smp = samples + static_cast<size_t>(a) * la.scap;
-  int* as = assoc + (static_cast<size_t>(a) * la.cand_stride + h) * la.scap;
-  Pose H = cand[static_cast<size_t>(a) * la.cand_stride + h];
-  double lambda = 1e-3;
-  bool need_assoc = true;
-  for (int it = 0; it < 10; ++it) {
-    if (need_assoc) {
-      float R[9], t[3];
+  const int* as = assoc + hi * la.scap;
+  Pose H = cand[hi];
+  double acc[28];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(H.R[i]);
+  for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+  int terms = 0;
+  for (int i = lane; i < la.ns; i += 32) {
+    const int mi = as[i];
+    if (mi < 0) continue;
+    const float4 c = fr.gcam[fbase + smp[i]];
+    const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
+    lm_accum(H, x, pv.geom[mi], la.use_cov != 0, acc, true);
+    ++terms;
+  }
+  if (work) atomicAdd(&work[W_LM_TERMS], static_cast<unsigned long long>(terms));
 #pragma unroll
-      for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(H.t[i]);
-      for (int i = lane; i < la.ns; i += 32) {
-        const size_t gb = fbase + smp[i];
-        int best_m = -1;
-        if (work && fr.gnm[gb] > 0) atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(fr.gnm[gb]));
-        if (fr.gnm[gb] > 0) {
-          const float4 c = fr.gcam[gb];
-          float y[3];
-          xform_f32(R, t, c.x, c.y, c.z, y);
-          float best = 0.0f;
-          for (int tt = 0; tt < fr.T; ++tt) {
-            const int slot = fr.gslot[gb * fr.T + tt];
-            const int cnt = pv.count[slot];
-            for (int m = 0; m < cnt; ++m) {
-              const int mi = slot * kMaxModes + m;
-              const float4 q0 = pv.geom[mi].q0;
-              const float d0 = __fsub_rn(y[0], q0.x), d1 = __fsub_rn(y[1], q0.y), d2 = __fsub_rn(y[2], q0.z);
-              float q;
-              if (la.use_cov) {
-                const float4 q1 = pv.geom[mi].q1, q2 = pv.geom[mi].q2;
-                q = quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, d0, d1, d2);
-              } else {
-                q = quad_eucl(d0, d1, d2);
-              }
-              if (best_m < 0 || q < best) {
-                best = q;
-                best_m = mi;
-              }
-            }
-          }
-        }
-        as[i] = best_m;
-      }
-      __syncwarp();
-      need_assoc = false;
-    }
-    double acc[28];
-#pragma unroll
-    for (int k = 0; k < 28; ++k) acc[k] = 0.0;
-    int terms = 0;
-    for (int i = lane; i < la.ns; i += 32) {
-      const int mi = as[i];
-      if (mi < 0) continue;
-      const float4 c = fr.gcam[fbase + smp[i]];
-      const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
-      lm_accum(H, x, pv.geom[mi], la.use_cov != 0, acc, true);
-      ++terms;
-    }
-    if (work) atomicAdd(&work[W_LM_TERMS], static_cast<unsigned long long>(terms));
-#pragma unroll
-    for (int k = 0; k < 28; ++k) acc[k] = warp_sum_xor(acc[k]);
-    const double E = acc[27];
-    if (!(E > 0.0)) break;
-    double M[36], rhs[6], delta[6];
-    int k = 0;
-#pragma unroll
-    for (int p = 0; p < 6; ++p)
-#pragma unroll
-      for (int q = p; q < 6; ++q, ++k) {
-        M[6 * p + q] = acc[k];
-        M[6 * q + p] = acc[k];
-      }
-#pragma unroll
-    for (int p = 0; p < 6; ++p) {
-      M[6 * p + p] = M[6 * p + p] + lambda * M[6 * p + p];
-      rhs[p] = -acc[21 + p];
-    }
-    if (!chol6(M, rhs, delta)) {
-      lambda = lambda * 10.0;
-      continue;
-    }
-    Pose D, Hn;
-    exp_se3(delta, D);
-    pose_compose(D, H, Hn);
-    double accn[28];
-    accn[27] = 0.0;
-    for (int i = lane; i < la.ns; i += 32) {
-      const int mi = as[i];
-      if (mi < 0) continue;
-      const float4 c = fr.gcam[fbase + smp[i]];
-      const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
-      lm_accum(Hn, x, pv.geom[mi], la.use_cov != 0, accn, false);
-    }
-    const double En = warp_sum_xor(accn[27]);
-    if (En < E) {
-      H = Hn;
-      lambda = lambda * 0.1;
-      need_assoc = true;
-      if ((E - En) / E < 1e-6) break;
+  for (int k = 0; k < 28; ++k) acc[k] = warp_sum_xor(acc[k]);
+  ls.need_assoc = 0;
+  const double E = acc[27];
+  if (!(E > 0.0)) {
+    ls.done = 1;
+  } else {
+    double delta[6];
+    if (!lm_solve(acc, ls.lambda, delta)) {
+      ls.lambda = ls.lambda * 10.0;
     } else {
-      lambda = lambda * 10.0;
+      Pose D, Hn;
+      exp_se3(delta, D);
+      pose_compose(D, H, Hn);
+      double accn[28];
+      accn[27] = 0.0;
+      for (int i = lane; i < la.ns; i += 32) {
+        const int mi = as[i];
+        if (mi < 0) continue;
+        const float4 c = fr.gcam[fbase + smp[i]];
+        const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
+        lm_accum(Hn, x, pv.geom[mi], la.use_cov != 0, accn, false);
+      }
+      const double En = warp_sum_xor(accn[27]);
+      if (En < E) {
+        H = Hn;
+        ls.lambda = ls.lambda * 0.1;
+        ls.need_assoc = 1;
+        if ((E - En) / E < 1e-6) ls.done = 1;
+        if (lane == 0) cand[hi] = H;
+      } else {
+        ls.lambda = ls.lambda * 10.0;
+      }
     }
   }
-  if (lane == 0) cand[static_cast<size_t>(a) * la.cand_stride + h] = H;
+  if (lane == 0) st[hi] = ls;
 }
 
 // ================================ K8-K10: ICP + raycast + depth-difference score ============
@@ -1096,6 +1265,7 @@ FrameRefs frame_refs(scr_scene s) {
   fr.gslot = s->ws.gslot;
   fr.gnm = s->ws.gnm;
   fr.grec = s->ws.grec;
+  fr.gleaf = s->ws.gleaf;
   fr.tex = s->ws.tex;
   fr.gmax = s->ws.gmax;
   fr.T = s->T;
@@ -1145,7 +1315,9 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   SCR_TRY(ensure_icp_ws(s, std::min(nA * jobs_per, 1024)));
   const FrameRefs fr = frame_refs(s);
   const PredView pv = s->pred_view();
-  GenParams gp{p.max_gen_iters, p.n_max, p.min_sq_dist, p.colour_thresh, p.rigidity_tol};
+  GenParams gp{p.max_gen_iters, p.n_max, p.min_sq_dist, p.colour_thresh, p.rigidity_tol,
+               (s->T <= 5 && s->leaves16) ? 1 : 0, {0}};
+  for (int t = 0; t < s->T && t < kMaxTrees; ++t) gp.leaf_base[t] = s->leaf_base[t];
   unsigned long long* wk = work_ptr(s);
   SCR_CUDA(cudaMemsetAsync(w.hctr, 0, nA * sizeof(int), s->stream));  // per-frame slot counters
   const int gen_threads = std::min(p.n_max, kGenThreadsPerFrame);
@@ -1175,9 +1347,14 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
     const int ns = p.eta * (k + 1);
     if (p.pose_update) {
       la.ns = ns;
-      SCR_LAUNCH(s, K_LM,
-                 (k_lm<<<dim3((p.n_cull + 3) / 4, nA), 128, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand,
-                                                                            w.assoc, wk)));
+      LmState* lmst = static_cast<LmState*>(w.lmst);
+      SCR_LAUNCH(s, K_LM, (k_lm_init<<<nA, w.ncull_cap, 0, s->stream>>>(w.ncand, p.n_out, w.ncull_cap, lmst)));
+      for (int it = 0; it < 10; ++it) {
+        SCR_LAUNCH(s, K_LM, (k_lm_assoc<<<dim3((ns + 7) / 8, nA), 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand,
+                                                                                      w.ncand, lmst, w.assoc, wk)));
+        SCR_LAUNCH(s, K_LM, (k_lm_step<<<dim3((p.n_cull + 3) / 4, nA), 128, 0, s->stream>>>(
+                                fr, pv, la, w.samples, w.cand, w.ncand, lmst, w.assoc, wk)));
+      }
     }
     // rescore (only frames still above n_out take part): per-batch partial energies, then
     // E(I_k) = E(I_{k-1}) + E_k without LM (poses unchanged), or the full batch sum with LM
@@ -1252,6 +1429,7 @@ scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int scap) {
     SCR_TRY(grow(&w.icp_rms, B * nc));
     SCR_TRY(grow(&w.icp_inl, B * nc));
     SCR_TRY(grow(&w.epart, B * nc * kEnergyBatches));
+    SCR_TRY(grow(reinterpret_cast<LmState**>(&w.lmst), B * nc));
     w.ncull_cap = nc;
     w.samples_cap = sc;
     if (w.henergy && static_cast<size_t>(w.nmax_cap) < static_cast<size_t>(nc)) {

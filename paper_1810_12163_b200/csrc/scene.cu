@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
                                                 const int* __restrict__ gcount, const int* __restrict__ gpx,
                                                 int gmax, int* __restrict__ gslot, int* __restrict__ gnm,
                                                 float4* __restrict__ gcam, int4* __restrict__ grec,
-                                                const int* __restrict__ pcount, unsigned long long* __restrict__ work) {
+                                                uint4* __restrict__ gleaf, const int* __restrict__ pcount,
+                                                unsigned long long* __restrict__ work) {
   __shared__ short4 sspec[kFeatures];
   for (int i = threadIdx.x; i < kFeatures; i += blockDim.x) sspec[i] = fv.specs[i];
   __syncthreads();
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
   const float d = __uint_as_float(c.x);
   int nm = 0, visits = 0;
   uint32_t counts = 0;
+  uint32_t lw[4] = {0u, 0u, 0u, 0u};  // 16-bit leaf ids of trees 0..7
   for (int t = 0; t < fv.T; ++t) {
     const int nb = fv.node_base[t];
     int node = nb;
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
     }
     const int slot = fv.leaf_base[t] + leaf;
     gslot[gidx * fv.T + t] = slot;
+    if (t < 8) lw[t >> 1] |= (static_cast<uint32_t>(leaf) & 0xffffu) << (16 * (t & 1));
     const int cnt = pcount ? pcount[slot] : 0;
     nm += cnt;
     if (t < 5) counts |= static_cast<uint32_t>(cnt) << (6 * t);
@@ -186,6 +189,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
   // per-tree mode counts (6 bits each, trees 0..4)
   grec[gidx] = make_int4(px, static_cast<int>(c.x), static_cast<int>((c.y & 0xffffffu) | (min(nm, 255) << 24)),
                          static_cast<int>(counts));
+  gleaf[gidx] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   if (work) atomicAdd(&work[W_NODE_VISITS], static_cast<unsigned long long>(visits));
   const double dd = static_cast<double>(d);
   const double X = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
@@ -659,6 +663,7 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   }
   std::vector<int4> nodes;
   std::vector<int> node_base, leaf_base;
+  bool leaves16 = true;
   int64_t L = 0;
   for (uint32_t t = 0; t < nt; ++t) {
     uint32_t nn;
@@ -689,6 +694,7 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
       nodes.push_back(v);
     }
     (void)first;
+    if (leaves > 65536) leaves16 = false;
     L += leaves;
   }
   if (off != n) return malformed("trailing bytes at offset " + std::to_string(off));
@@ -703,6 +709,7 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   s->L = L;
   s->node_base = node_base;
   s->leaf_base = leaf_base;
+  s->leaves16 = leaves16;
   s->geom.W = k->width;
   s->geom.H = k->height;
   s->geom.fx = static_cast<float>(k->fx);
@@ -748,6 +755,7 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   if ((st = dalloc(&w.gslot, B * w.gmax * s->T)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.grec, B * w.gmax)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.gleaf, B * w.gmax)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.fidx, B)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.status, B)) != SCR_OK) return fail(st);
@@ -778,7 +786,7 @@ void scr_scene_destroy(scr_scene s) {
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
-                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
+                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.gleaf, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
                   s->ws.ins_rank, s->ws.ins_total};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -881,7 +889,7 @@ scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_
   SCR_LAUNCH(s, K_LEAVES,
              (k_leaves<<<dim3((w.gmax + 127) / 128, n), 128, 0, s->stream>>>(
                  s->forest_view(), s->geom, w.tex, w.gcount, w.gpx, w.gmax, w.gslot, w.gnm, w.gcam, w.grec,
-                 s->d_count, work_ptr(s))));
+                 w.gleaf, s->d_count, work_ptr(s))));
   SCR_CUDA(cudaGetLastError());
   return SCR_OK;
 }
