@@ -101,23 +101,57 @@ struct RawBuf {  // next 7 raw outputs of the slot's stream
   }
 };
 
-// mode index of pick-th predicted mode of a pixel (union over trees in tree order)
-SCR_DEV int mode_from_record(const GenParams& gp, int T, uint32_t counts, uint4 lv, int pick) {
-  for (int t = 0; t < T; ++t) {
-    const int c = static_cast<int>((counts >> (6 * t)) & 63u);
-    if (pick < c) {
-      const uint32_t w = t < 2 ? lv.x : (t < 4 ? lv.y : (t < 6 ? lv.z : lv.w));
-      const int leaf = static_cast<int>((w >> (16 * (t & 1))) & 0xffffu);
-      return (gp.leaf_base[t] + leaf) * kMaxModes + pick;
-    }
-    pick -= c;
-  }
-  return -1;
+// Mode index of the pick-th predicted mode of a pixel (union over trees in tree order),
+// branch-free from the record: 6-bit per-tree counts and 16-bit leaf ids (trees 0..4).
+SCR_DEV int mode_from_record(const int* lbase, uint32_t counts, uint4 lv, int pick) {
+  const int c0 = counts & 63u, c1 = (counts >> 6) & 63u, c2 = (counts >> 12) & 63u, c3 = (counts >> 18) & 63u;
+  const int e0 = c0, e1 = e0 + c1, e2 = e1 + c2, e3 = e2 + c3;
+  const int t = (pick >= e0) + (pick >= e1) + (pick >= e2) + (pick >= e3);
+  const int before = t == 0 ? 0 : (t == 1 ? e0 : (t == 2 ? e1 : (t == 3 ? e2 : e3)));
+  const uint32_t w = t < 2 ? lv.x : (t < 4 ? lv.y : lv.z);
+  const int leaf = static_cast<int>((w >> (16 * (t & 1))) & 0xffffu);
+  return (lbase[t] + leaf) * kMaxModes + (pick - before);
 }
 
 // Kabsch (f64 SVD) runs only for triplets that passed every check; out of line so it does
 // not set the register budget of the retry loop.
 __device__ __noinline__ bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return kabsch3(cm, w, *T); }
+
+// Checks 2-3 (distances in f64) and Kabsch for a triplet whose colour check passed
+// (SPEC.md:441-446). Out of line: its f64 temporaries stay out of the retry loop.
+__device__ __noinline__ bool geometry_checks_cold(const GenParams& gp, const FrameGeom& g, const PredView& pv,
+                                                  int4 A0, int4 A1, int4 A2, int m0, int m1, int m2, Pose* T) {
+  const float4 w0 = pv.geom[m0].q0, w1 = pv.geom[m1].q0, w2 = pv.geom[m2].q0;
+  double w[9], cm[9];
+  w[0] = w0.x; w[1] = w0.y; w[2] = w0.z;
+  w[3] = w1.x; w[4] = w1.y; w[5] = w1.z;
+  w[6] = w2.x; w[7] = w2.y; w[8] = w2.z;
+  const int4 Ak[3] = {A0, A1, A2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int x = Ak[k].x & 0xffff, y = Ak[k].x >> 16;
+    const double dd = static_cast<double>(__int_as_float(Ak[k].y));
+    cm[3 * k + 0] = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
+    cm[3 * k + 1] = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
+    cm[3 * k + 2] = dd;
+  }
+  double dw2[3], dc2[3];
+  bool close = false;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
+    const double ax = w[3 * pa] - w[3 * pb], ay = w[3 * pa + 1] - w[3 * pb + 1], az = w[3 * pa + 2] - w[3 * pb + 2];
+    dw2[q] = (ax * ax + ay * ay) + az * az;
+    const double bx = cm[3 * pa] - cm[3 * pb], by = cm[3 * pa + 1] - cm[3 * pb + 1], bz = cm[3 * pa + 2] - cm[3 * pb + 2];
+    dc2[q] = (bx * bx + by * by) + bz * bz;
+    if (dw2[q] < gp.min_sq_dist) close = true;
+  }
+  if (close) return false;
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > gp.rigidity_tol) return false;
+  return kabsch3(cm, w, *T);
+}
 
 __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
                                                    const uint64_t* __restrict__ seeds, int* __restrict__ slot_ctr,
@@ -125,12 +159,14 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
                                                    int* __restrict__ hiters, unsigned long long* __restrict__ work) {
   __shared__ uint64_t s_m[kMaxModeUnion + 1];    // Barrett reciprocal for mode counts 1..400
   __shared__ uint64_t s_thr[kMaxModeUnion + 1];  // rejection threshold (2^64 mod n)
+  __shared__ int s_lbase[kMaxTrees];
   for (int i = threadIdx.x; i <= kMaxModeUnion; i += blockDim.x) {
     const uint64_t n = i ? static_cast<uint64_t>(i) : 1;
     const uint64_t m = barrett_m(n);
     s_m[i] = m;
     s_thr[i] = mod_barrett(0 - n, n, m);
   }
+  if (threadIdx.x < kMaxTrees) s_lbase[threadIdx.x] = gp.leaf_base[threadIdx.x];
   __syncthreads();
   const int a = blockIdx.y;
   const int f = fr.fidx[a];
@@ -149,42 +185,43 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
     Pose T;
     if (G > 0) {
       for (it = 0; it < gp.max_iters; ++it) {
-        int4 A[3];
-        uint4 Lv[3];
-        int pick[3], gix[3], cc = 0, consumed = 0;
+        int4 A0, A1, A2;
+        uint4 L0, L1, L2;
+        int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0, consumed = 0;
         bool proceed = false;
         const bool spec = fast && buf.b0 >= tG && buf.b2 >= tG && buf.b4 >= tG;
         bool slow = !spec;
         if (spec) {
-          gix[0] = static_cast<int>(mod_barrett(buf.b0, G, mG));
-          gix[1] = static_cast<int>(mod_barrett(buf.b2, G, mG));
-          gix[2] = static_cast<int>(mod_barrett(buf.b4, G, mG));
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            A[k] = fr.grec[fbase + gix[k]];
-            Lv[k] = fr.gleaf[fbase + gix[k]];
-          }
-          const int nm0 = static_cast<uint32_t>(A[0].z) >> 24;
-          const int nm1 = static_cast<uint32_t>(A[1].z) >> 24;
-          const int nm2 = static_cast<uint32_t>(A[2].z) >> 24;
+          g0 = static_cast<int>(mod_barrett(buf.b0, G, mG));
+          g1 = static_cast<int>(mod_barrett(buf.b2, G, mG));
+          g2 = static_cast<int>(mod_barrett(buf.b4, G, mG));
+          A0 = fr.grec[fbase + g0];
+          A1 = fr.grec[fbase + g1];
+          A2 = fr.grec[fbase + g2];
+          L0 = fr.gleaf[fbase + g0];
+          L1 = fr.gleaf[fbase + g1];
+          L2 = fr.gleaf[fbase + g2];
+          const int nm0 = static_cast<uint32_t>(A0.z) >> 24;
+          const int nm1 = static_cast<uint32_t>(A1.z) >> 24;
+          const int nm2 = static_cast<uint32_t>(A2.z) >> 24;
           if (nm0 == 0) {
             consumed = 1;
           } else if (buf.b1 < s_thr[nm0]) {
             slow = true;
           } else {
-            pick[0] = static_cast<int>(mod_barrett(buf.b1, nm0, s_m[nm0]));
+            p0 = static_cast<int>(mod_barrett(buf.b1, nm0, s_m[nm0]));
             if (nm1 == 0) {
               consumed = 3;
             } else if (buf.b3 < s_thr[nm1]) {
               slow = true;
             } else {
-              pick[1] = static_cast<int>(mod_barrett(buf.b3, nm1, s_m[nm1]));
+              p1 = static_cast<int>(mod_barrett(buf.b3, nm1, s_m[nm1]));
               if (nm2 == 0) {
                 consumed = 5;
               } else if (buf.b5 < s_thr[nm2]) {
                 slow = true;
               } else {
-                pick[2] = static_cast<int>(mod_barrett(buf.b5, nm2, s_m[nm2]));
+                p2 = static_cast<int>(mod_barrett(buf.b5, nm2, s_m[nm2]));
                 if (buf.b6 < t3) {
                   slow = true;
                 } else {
@@ -197,20 +234,30 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
           }
         }
         if (slow) {  // exact sequential replay of the attempt from the buffered stream
-          proceed = true;
-#pragma unroll 1
-          for (int k = 0; k < 3; ++k) {
-            gix[k] = static_cast<int>(buf.draw(rng, G, mG, tG));
-            A[k] = fr.grec[fbase + gix[k]];
-            Lv[k] = fr.gleaf[fbase + gix[k]];
-            const int nm = fast ? (static_cast<uint32_t>(A[k].z) >> 24) : fr.gnm[fbase + gix[k]];
-            if (nm == 0) {
-              proceed = false;
-              break;
+          proceed = false;
+          g0 = static_cast<int>(buf.draw(rng, G, mG, tG));
+          A0 = fr.grec[fbase + g0];
+          L0 = fr.gleaf[fbase + g0];
+          const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
+          if (nm0 > 0) {
+            p0 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
+            g1 = static_cast<int>(buf.draw(rng, G, mG, tG));
+            A1 = fr.grec[fbase + g1];
+            L1 = fr.gleaf[fbase + g1];
+            const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
+            if (nm1 > 0) {
+              p1 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
+              g2 = static_cast<int>(buf.draw(rng, G, mG, tG));
+              A2 = fr.grec[fbase + g2];
+              L2 = fr.gleaf[fbase + g2];
+              const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
+              if (nm2 > 0) {
+                p2 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
+                cc = static_cast<int>(buf.draw(rng, 3, m3, t3));
+                proceed = true;
+              }
             }
-            pick[k] = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm), s_m[nm], s_thr[nm]));
           }
-          if (proceed) cc = static_cast<int>(buf.draw(rng, 3, m3, t3));
         } else {
           switch (consumed) {  // advance the stream by the raw values this attempt used
             case 1: buf.pop(rng); break;
@@ -220,56 +267,26 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
           }
         }
         if (!proceed) continue;
-        int mi[3];
-        mi[cc] = fast ? mode_from_record(gp, fr.T, static_cast<uint32_t>(A[cc].w), Lv[cc], pick[cc])
-                      : mode_index(fr, pv.count, fbase + gix[cc], pick[cc]);
+        int m0, m1, m2;
+        if (fast) {
+          m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), L0, p0);
+          m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), L1, p1);
+          m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), L2, p2);
+        } else {
+          m0 = mode_index(fr, pv.count, fbase + g0, p0);
+          m1 = mode_index(fr, pv.count, fbase + g1, p1);
+          m2 = mode_index(fr, pv.count, fbase + g2, p2);
+        }
         {
-          const uint32_t col = static_cast<uint32_t>(A[cc].z);
-          const float4 mc = pv.col[mi[cc]];
+          const uint32_t col = static_cast<uint32_t>(cc == 0 ? A0.z : (cc == 1 ? A1.z : A2.z));
+          const float4 mc = pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)];
           float linf = 0.0f;
           linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
           linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 8) & 255u), mc.y)));
           linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 16) & 255u), mc.z)));
           if (linf > gp.colour_thresh) continue;
         }
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-          if (k != cc)
-            mi[k] = fast ? mode_from_record(gp, fr.T, static_cast<uint32_t>(A[k].w), Lv[k], pick[k])
-                         : mode_index(fr, pv.count, fbase + gix[k], pick[k]);
-        double w[9], cm[9];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const float4 q0 = pv.geom[mi[k]].q0;
-          w[3 * k + 0] = static_cast<double>(q0.x);
-          w[3 * k + 1] = static_cast<double>(q0.y);
-          w[3 * k + 2] = static_cast<double>(q0.z);
-          const int x = A[k].x & 0xffff, y = A[k].x >> 16;
-          const double dd = static_cast<double>(__int_as_float(A[k].y));
-          cm[3 * k + 0] = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
-          cm[3 * k + 1] = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
-          cm[3 * k + 2] = dd;
-        }
-        double dw2[3], dc2[3];
-        bool close = false;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
-          const double ax = w[3 * pa] - w[3 * pb], ay = w[3 * pa + 1] - w[3 * pb + 1],
-                       az = w[3 * pa + 2] - w[3 * pb + 2];
-          dw2[q] = (ax * ax + ay * ay) + az * az;
-          const double bx = cm[3 * pa] - cm[3 * pb], by = cm[3 * pa + 1] - cm[3 * pb + 1],
-                       bz = cm[3 * pa + 2] - cm[3 * pb + 2];
-          dc2[q] = (bx * bx + by * by) + bz * bz;
-          if (dw2[q] < gp.min_sq_dist) close = true;
-        }
-        if (close) continue;
-        bool nonrigid = false;
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > gp.rigidity_tol) nonrigid = true;
-        if (nonrigid) continue;
-        if (!kabsch3_cold(cm, w, &T)) continue;
+        if (!geometry_checks_cold(gp, g, pv, A0, A1, A2, m0, m1, m2, &T)) continue;
         ok = 1;
         break;
       }
@@ -1145,7 +1162,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
     }
     cluster.sync();
     if (rank != 0 && threadIdx.x == 0) stop_level = *cluster.map_shared_rank(&stop_level, 0);
-    __syncthreads();
+    cluster.sync();  // CTA 0 must not exit while the others still read its shared memory
     conv = stop_level;
   }
   double score = __longlong_as_double(0x7ff0000000000000ll);
