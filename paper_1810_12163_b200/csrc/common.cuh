@@ -463,6 +463,11 @@ SCR_DEV void ray_dir(const float R[9], float fx, float fy, float cx, float cy, i
   for (int i = 0; i < 3; ++i) d[i] = __fmaf_rn(R[3 * i + 0], dcx, __fmaf_rn(R[3 * i + 1], dcy, R[3 * i + 2]));
 }
 
+SCR_DEV void ray_dir_tab(const float R[9], float dcx, float dcy, float d[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) d[i] = __fmaf_rn(R[3 * i + 0], dcx, __fmaf_rn(R[3 * i + 1], dcy, R[3 * i + 2]));
+}
+
 SCR_DEV Hit raycast(const Prim* prims, int n, const float o[3], const float d[3]) {
   Hit h;
   h.t = __int_as_float(0x7f800000);

@@ -454,10 +454,56 @@ __global__ void __launch_bounds__(256) k_energy(EnergyArgs ea, FrameRefs fr, Pre
 // sequential sweep: samples without modes contribute +0).
 constexpr int kSmallHyps = 64;
 
+// Per-sample predicted-mode list (union over trees in tree order) for warp-cooperative
+// staging: lanes 0..T-1 fetch (slot, count) of their tree, shuffled to the whole warp.
+struct SampleModes {
+  int slot[kMaxTrees];
+  int end[kMaxTrees];  // cumulative counts
+};
+
+SCR_DEV void sample_modes(const FrameRefs& fr, const int* pcount, size_t gb, int lane, SampleModes& sm) {
+  int myslot = 0, mycnt = 0;
+  if (lane < fr.T) {
+    myslot = fr.gslot[gb * fr.T + lane];
+    mycnt = pcount[myslot];
+  }
+  int run = 0;
+#pragma unroll
+  for (int t = 0; t < kMaxTrees; ++t) {
+    const int sl = __shfl_sync(0xffffffffu, myslot, t);
+    const int c = __shfl_sync(0xffffffffu, mycnt, t);
+    run += (t < fr.T) ? c : 0;
+    sm.slot[t] = sl;
+    sm.end[t] = run;
+  }
+}
+
+// Lane l stages mode j0 + l of the sample into buf[3 l .. 3 l + 2] (coalesced fetch, one
+// L2 round trip per 32 modes); returns the global mode index it staged (-1 if none).
+SCR_DEV int stage_modes(const PredView& pv, const SampleModes& sm, int T, int nm, int j0, int lane, float4* buf) {
+  const int j = j0 + lane;
+  if (j >= nm) return -1;
+  int t = 0, before = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxTrees - 1; ++q)
+    if (q < T - 1 && j >= sm.end[q]) {
+      t = q + 1;
+      before = sm.end[q];
+    }
+  const int mi = sm.slot[t] * kMaxModes + (j - before);
+  const ModeGeom& g = pv.geom[mi];
+  buf[3 * lane + 0] = g.q0;
+  buf[3 * lane + 1] = g.q1;
+  buf[3 * lane + 2] = g.q2;
+  return mi;
+}
+
+
 __global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs fr, PredView pv,
                                                       unsigned long long* __restrict__ work) {
   extern __shared__ float es_e[];  // [kSmallHyps][eta + 1]
   __shared__ float s_pose[kSmallHyps][12];
+  __shared__ float4 s_modes[8 * 96];  // per-warp staging: 32 modes x 3 float4
   const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
   const int n = ea.nper ? ea.nper[a] : ea.stride;
   if (n <= ea.min_n) return;
@@ -488,6 +534,7 @@ __global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs f
   const int* smp = ea.samples + static_cast<size_t>(a) * ea.scap + static_cast<size_t>(b) * ea.eta;
   const int eta = ea.eta, ld = eta + 1;
   unsigned long long evals = 0, sevals = 0;
+  float4* wbuf = s_modes + wid * 96;
   for (int s = wid; s < eta; s += nw) {
     const size_t gb = fbase + smp[s];
     const int nm = fr.gnm[gb];
@@ -498,17 +545,20 @@ __global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs f
       xform_f32(R0, t0, c.x, c.y, c.z, y0);
       xform_f32(R1, t1, c.x, c.y, c.z, y1);
       float m0 = __int_as_float(0x7f800000), m1 = m0;
-      for (int tt = 0; tt < fr.T; ++tt) {
-        const int slot = fr.gslot[gb * fr.T + tt];
-        const int cnt = pv.count[slot];
-        const ModeGeom* mg = pv.geom + static_cast<size_t>(slot) * kMaxModes;
+      SampleModes sm;
+      sample_modes(fr, pv.count, gb, lane, sm);
+      for (int j0 = 0; j0 < nm; j0 += 32) {
+        stage_modes(pv, sm, fr.T, nm, j0, lane, wbuf);
+        __syncwarp();
+        const int cnt = min(32, nm - j0);
         for (int m = 0; m < cnt; ++m) {
-          const float4 q0 = mg[m].q0, q1 = mg[m].q1, q2 = mg[m].q2;
+          const float4 q0 = wbuf[3 * m], q1 = wbuf[3 * m + 1], q2 = wbuf[3 * m + 2];
           m0 = fminf(m0, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(y0[0], q0.x),
                                    __fsub_rn(y0[1], q0.y), __fsub_rn(y0[2], q0.z)));
           m1 = fminf(m1, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(y1[0], q0.x),
                                    __fsub_rn(y1[1], q0.y), __fsub_rn(y1[2], q0.z)));
         }
+        __syncwarp();
       }
       e0 = __fsqrt_rn(fmaxf(m0, 0.0f));
       e1 = __fsqrt_rn(fmaxf(m1, 0.0f));
@@ -703,6 +753,8 @@ __global__ void __launch_bounds__(256) k_lm_assoc(FrameRefs fr, PredView pv, LmA
   __shared__ float s_pose[kSmallHyps][12];
   __shared__ int s_need[kSmallHyps];
   __shared__ int s_any;
+  __shared__ float4 s_modes[8 * 96];
+  __shared__ int s_mi[8 * 32];
   const int a = blockIdx.y;
   const int n = ncand[a];
   if (n <= la.n_out) return;
@@ -731,7 +783,7 @@ __global__ void __launch_bounds__(256) k_lm_assoc(FrameRefs fr, PredView pv, LmA
   const int f = fr.fidx[a];
   const size_t gb = static_cast<size_t>(f) * fr.gmax + samples[static_cast<size_t>(a) * la.scap + s];
   int best0 = -1, best1 = -1;
-  if (fr.gnm[gb] > 0 && (v0 || v1)) {
+  if (fr.gnm[gb] > 0 && __any_sync(0xffffffffu, v0 || v1)) {  // warp-uniform: lanes cooperate below
     float R0[9], t0[3], R1[9], t1[3];
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
@@ -748,17 +800,23 @@ __global__ void __launch_bounds__(256) k_lm_assoc(FrameRefs fr, PredView pv, LmA
     xform_f32(R0, t0, c.x, c.y, c.z, y0);
     xform_f32(R1, t1, c.x, c.y, c.z, y1);
     float q0b = 0.0f, q1b = 0.0f;
-    for (int tt = 0; tt < fr.T; ++tt) {
-      const int slot = fr.gslot[gb * fr.T + tt];
-      const int cnt = pv.count[slot];
+    const int nm = fr.gnm[gb];
+    SampleModes sm;
+    sample_modes(fr, pv.count, gb, lane, sm);
+    float4* wbuf = s_modes + wid * 96;
+    int* wmi = s_mi + wid * 32;
+    for (int j0 = 0; j0 < nm; j0 += 32) {
+      wmi[lane] = stage_modes(pv, sm, fr.T, nm, j0, lane, wbuf);
+      __syncwarp();
+      const int cnt = min(32, nm - j0);
       for (int m = 0; m < cnt; ++m) {
-        const int mi = slot * kMaxModes + m;
-        const float4 g0 = pv.geom[mi].q0;
+        const float4 g0 = wbuf[3 * m];
+        const int mi = wmi[m];
         float qa, qb;
         const float a0 = __fsub_rn(y0[0], g0.x), a1 = __fsub_rn(y0[1], g0.y), a2 = __fsub_rn(y0[2], g0.z);
         const float b0 = __fsub_rn(y1[0], g0.x), b1 = __fsub_rn(y1[1], g0.y), b2 = __fsub_rn(y1[2], g0.z);
         if (la.use_cov) {
-          const float4 g1 = pv.geom[mi].q1, g2 = pv.geom[mi].q2;
+          const float4 g1 = wbuf[3 * m + 1], g2 = wbuf[3 * m + 2];
           qa = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, a0, a1, a2);
           qb = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, b0, b1, b2);
         } else {
@@ -774,6 +832,7 @@ __global__ void __launch_bounds__(256) k_lm_assoc(FrameRefs fr, PredView pv, LmA
           best1 = mi;
         }
       }
+      __syncwarp();
     }
     if (work && lane == 0)
       atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(fr.gnm[gb]) * static_cast<unsigned long long>(n));
@@ -905,6 +964,16 @@ __device__ __forceinline__ void cta_reduce_f32(const float* v, double (*red)[32]
   __syncthreads();
 }
 
+constexpr int kMaxImageW = 1280, kMaxImageH = 960;
+
+// Per-level normalised ray tables (x - cx) / fx and (y - cy) / fy (IEEE division, the
+// same values ray_dir computes per pixel).
+__device__ __forceinline__ void fill_ray_tables(int W, int H, float fx, float fy, float cx, float cy, float* dcx,
+                                                float* dcy) {
+  for (int x = threadIdx.x; x < W; x += blockDim.x) dcx[x] = __fdiv_rn(__fsub_rn(static_cast<float>(x), cx), fx);
+  for (int y = threadIdx.x; y < H; y += blockDim.x) dcy[y] = __fdiv_rn(__fsub_rn(static_cast<float>(y), cy), fy);
+}
+
 // Warp 0 builds the ascending list of primitives that can be seen from (R, o) with the
 // given intrinsics; the ray casts of the pass then only test those (identical hits).
 __device__ __forceinline__ void build_plist(const Prim* prims, int nprims, const float R[9], const float o[3],
@@ -976,6 +1045,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
   __shared__ int stop_level;
   __shared__ unsigned char s_plist[256];
   __shared__ int s_pn;
+  __shared__ float s_dcx[kMaxImageW], s_dcy[kMaxImageH];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int lane_id = rank * kIcpThreads + threadIdx.x;
@@ -1014,13 +1084,14 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       }
       // K8: model map of this level at the reference pose (split over the cluster)
       if (work && rank == 0 && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(Wl * Hl));
+      fill_ray_tables(Wl, Hl, fxl, fyl, cxl, cyl, s_dcx, s_dcy);  // synced by build_plist
       build_plist(prims, nprims, Rr, tr, fxl, fyl, cxl, cyl, Wl, Hl, s_plist, &s_pn);
       const int npl = s_pn;
       if (work && rank == 0 && threadIdx.x == 0)
         atomicAdd(&work[W_RAY_PRIMS], static_cast<unsigned long long>(Wl * Hl) * npl);
       for (int p = lane_id; p < Wl * Hl; p += kIcpLanes) {
         float d[3];
-        ray_dir(Rr, fxl, fyl, cxl, cyl, p % Wl, p / Wl, d);
+        ray_dir_tab(Rr, s_dcx[p % Wl], s_dcy[p / Wl], d);
         const Hit h = raycast_list(prims, s_plist, npl, tr, d);
         uint2 v = make_uint2(0u, 0xffffffffu);
         if (h.prim >= 0 && h.t <= kRenderMaxDepth) v = make_uint2(__float_as_uint(h.t), h.prim | (h.face << 16));
@@ -1045,8 +1116,8 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
           const float dl = __uint_as_float(tex[(y * fs) * g.W + x * fs].x);
           if (!depth_valid(dl)) continue;
           ++valid;
-          const float dcx = __fdiv_rn(__fsub_rn(static_cast<float>(x), cxl), fxl);
-          const float dcy = __fdiv_rn(__fsub_rn(static_cast<float>(y), cyl), fyl);
+          const float dcx = s_dcx[x];  // (x - cx) / fx, cached per level (same bits)
+          const float dcy = s_dcy[y];
           const float pc0 = __fmul_rn(dcx, dl), pc1 = __fmul_rn(dcy, dl);
           float pw[3], pr[3];
 #pragma unroll
@@ -1068,7 +1139,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
           if (mv.y == 0xffffffffu) continue;
           const float th = __uint_as_float(mv.x);
           float dm[3], m[3], nn[3];
-          ray_dir(Rr, fxl, fyl, cxl, cyl, ui, vi, dm);
+          ray_dir_tab(Rr, s_dcx[ui], s_dcy[vi], dm);
 #pragma unroll
           for (int i = 0; i < 3; ++i) m[i] = __fmaf_rn(th, dm[i], tr[i]);
           hit_normal(prims, static_cast<int>(mv.y & 0xffffu), static_cast<int>(mv.y >> 16), m, nn);
@@ -1176,13 +1247,15 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
     float sum = 0.0f;
     int mutual = 0, synth = 0;
     if (work && rank == 0 && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(g.W * g.H));
+    __syncthreads();
+    fill_ray_tables(g.W, g.H, g.fx, g.fy, g.cx, g.cy, s_dcx, s_dcy);
     build_plist(prims, nprims, R, t, g.fx, g.fy, g.cx, g.cy, g.W, g.H, s_plist, &s_pn);
     const int npl = s_pn;
     if (work && rank == 0 && threadIdx.x == 0)
       atomicAdd(&work[W_RAY_PRIMS], static_cast<unsigned long long>(g.W * g.H) * npl);
     for (int p = lane_id; p < g.W * g.H; p += kIcpLanes) {
       float d[3];
-      ray_dir(R, g.fx, g.fy, g.cx, g.cy, p % g.W, p / g.W, d);
+      ray_dir_tab(R, s_dcx[p % g.W], s_dcy[p / g.W], d);
       const Hit h = raycast_list(prims, s_plist, npl, t, d);
       if (h.prim < 0 || !(h.t <= kRenderMaxDepth) || !depth_valid(h.t)) continue;
       ++synth;
