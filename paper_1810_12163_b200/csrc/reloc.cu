@@ -322,138 +322,6 @@ __global__ void k_draw_samples(FrameRefs fr, const uint64_t* __restrict__ seeds,
 // staged in shared memory (chunked by a mode budget), then each thread owns one
 // hypothesis and sweeps the staged samples in order; all threads read the same staged
 // mode at the same time (shared-memory broadcast), so the inner loop is pure FP32.
-constexpr int kEnergyModeCap = 1024;    // staged modes per chunk: 1024 x 48 B = 48 KB
-constexpr int kEnergySampleCap = 512;   // eta <= 512 (Table 4)
-constexpr int kEnergyBatches = 8;       // sample batches per frame (1 + halvings)
-
-struct EnergyArgs {
-  const Pose* poses;
-  const int* ok;
-  int stride;
-  const int* nper;
-  int min_n;
-  const int* samples;
-  int scap, eta, batch0;
-  float* out;
-  int kb;  // 0: out[a*stride + h] = E_b; else out[(a*stride + h)*kb + b] = E_b
-};
-
-__global__ void __launch_bounds__(256) k_energy(EnergyArgs ea, FrameRefs fr, PredView pv,
-                                                unsigned long long* __restrict__ work) {
-  extern __shared__ float4 es_mode[];  // kEnergyModeCap * 3
-  __shared__ float4 es_cam[kEnergySampleCap];
-  __shared__ int es_off[kEnergySampleCap + 1];
-  const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
-  const int n = ea.nper ? ea.nper[a] : ea.stride;
-  if (n <= ea.min_n) return;
-  const int h0 = blockIdx.x * blockDim.x;
-  if (h0 >= n) return;
-  const int h = h0 + threadIdx.x;
-  const size_t idx = static_cast<size_t>(a) * ea.stride + h;
-  const bool active = h < n && (!ea.ok || ea.ok[idx]);
-  float R[9], t[3];
-  if (active) {
-    const Pose& P = ea.poses[idx];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(P.R[i]);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(P.t[i]);
-  }
-  const int f = fr.fidx[a];
-  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
-  const int* smp = ea.samples + static_cast<size_t>(a) * ea.scap + static_cast<size_t>(b) * ea.eta;
-  const int eta = ea.eta;
-  for (int s = threadIdx.x; s < eta; s += blockDim.x) es_off[s] = fr.gnm[fbase + smp[s]];
-  __syncthreads();
-  if (threadIdx.x < 32) {  // exclusive prefix of the per-sample mode counts
-    const int lane = threadIdx.x;
-    const int per = (eta + 31) / 32;
-    const int s0 = min(eta, lane * per), s1 = min(eta, s0 + per);
-    int local = 0;
-    for (int s = s0; s < s1; ++s) local += es_off[s];
-    int incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    int run = incl - local;
-    for (int s = s0; s < s1; ++s) {
-      const int c = es_off[s];
-      es_off[s] = run;
-      run += c;
-    }
-    if (lane == 31) es_off[eta] = incl;
-  }
-  __syncthreads();
-  float E = 0.0f;
-  unsigned long long evals = 0, sevals = 0;
-  int s0 = 0;
-  while (s0 < eta) {
-    int lo = s0 + 1, hi = eta;  // largest s1 whose modes fit the staging budget
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (es_off[mid] - es_off[s0] <= kEnergyModeCap) lo = mid;
-      else hi = mid - 1;
-    }
-    const int s1 = lo;
-    for (int s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
-      const size_t gb = fbase + smp[s];
-      es_cam[s - s0] = fr.gcam[gb];
-      int base = es_off[s] - es_off[s0];
-      for (int tt = 0; tt < fr.T; ++tt) {
-        const int slot = fr.gslot[gb * fr.T + tt];
-        const int cnt = pv.count[slot];
-        const ModeGeom* mg = pv.geom + static_cast<size_t>(slot) * kMaxModes;
-        for (int m = 0; m < cnt; ++m, ++base) {
-          es_mode[3 * base + 0] = mg[m].q0;
-          es_mode[3 * base + 1] = mg[m].q1;
-          es_mode[3 * base + 2] = mg[m].q2;
-        }
-      }
-    }
-    __syncthreads();
-    if (active) {
-      const int cbase = es_off[s0];
-      for (int s = s0; s < s1; ++s) {
-        const int m0 = es_off[s] - cbase, m1 = es_off[s + 1] - cbase;
-        if (m1 == m0) continue;
-        const float4 c = es_cam[s - s0];
-        float y[3];
-        xform_f32(R, t, c.x, c.y, c.z, y);
-        float qmin = __int_as_float(0x7f800000);
-        for (int m = m0; m < m1; ++m) {
-          const float4 q0 = es_mode[3 * m + 0], q1 = es_mode[3 * m + 1], q2 = es_mode[3 * m + 2];
-          const float q = quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(y[0], q0.x), __fsub_rn(y[1], q0.y),
-                                    __fsub_rn(y[2], q0.z));
-          qmin = fminf(qmin, q);
-        }
-        E = __fadd_rn(E, __fsqrt_rn(fmaxf(qmin, 0.0f)));
-        evals += static_cast<unsigned long long>(m1 - m0);
-        ++sevals;
-      }
-    }
-    __syncthreads();
-    s0 = s1;
-  }
-  if (h < n) {
-    const float v = active ? E : __int_as_float(0x7f800000);
-    if (ea.kb == 0) ea.out[idx] = v;
-    else ea.out[idx * ea.kb + b] = v;
-  }
-  if (work && active) {
-    atomicAdd(&work[W_MODE_EVALS], evals);
-    atomicAdd(&work[W_SAMPLE_EVALS], sevals);
-  }
-}
-
-// Re-scoring the <= 64 surviving hypotheses on one sample batch: warp per sample, lane l
-// owns hypotheses l and l + 32, so each predicted mode is loaded once per warp (uniform
-// load) and used for 2 x 32 hypotheses. Per-sample energies e[h][s] go to shared memory;
-// thread h then adds its row in sample order (the batch energy E_b, same bits as a
-// sequential sweep: samples without modes contribute +0).
-constexpr int kSmallHyps = 64;
-
 // Per-sample predicted-mode list (union over trees in tree order) for warp-cooperative
 // staging: lanes 0..T-1 fetch (slot, count) of their tree, shuffled to the whole warp.
 struct SampleModes {
@@ -498,6 +366,144 @@ SCR_DEV int stage_modes(const PredView& pv, const SampleModes& sm, int T, int nm
   return mi;
 }
 
+
+constexpr int kEnergyModeCap = 1024;    // staged modes per chunk: 1024 x 48 B = 48 KB
+constexpr int kEnergySampleCap = 512;   // eta <= 512 (Table 4)
+constexpr int kEnergyBatches = 8;       // sample batches per frame (1 + halvings)
+
+struct EnergyArgs {
+  const Pose* poses;
+  const int* ok;
+  int stride;
+  const int* nper;
+  int min_n;
+  const int* samples;
+  int scap, eta, batch0;
+  float* out;
+  int kb;  // 0: out[a*stride + h] = E_b; else out[(a*stride + h)*kb + b] = E_b
+};
+
+__global__ void __launch_bounds__(256) k_energy(EnergyArgs ea, FrameRefs fr, PredView pv,
+                                                unsigned long long* __restrict__ work) {
+  extern __shared__ float4 es_mode[];  // kEnergyModeCap * 3
+  __shared__ float4 es_cam[kEnergySampleCap];
+  __shared__ int es_off[kEnergySampleCap + 1];
+  const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
+  const int n = ea.nper ? ea.nper[a] : ea.stride;
+  if (n <= ea.min_n) return;
+  const int h0 = blockIdx.x * (2 * blockDim.x);  // each thread owns hypotheses h and h + blockDim
+  if (h0 >= n) return;
+  const int ha = h0 + threadIdx.x, hb = ha + blockDim.x;
+  const size_t ia = static_cast<size_t>(a) * ea.stride + ha, ib = static_cast<size_t>(a) * ea.stride + hb;
+  const bool act_a = ha < n && (!ea.ok || ea.ok[ia]);
+  const bool act_b = hb < n && (!ea.ok || ea.ok[ib]);
+  float Ra[9], ta[3], Rb[9], tb[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    Ra[i] = act_a ? static_cast<float>(ea.poses[ia].R[i]) : 0.0f;
+    Rb[i] = act_b ? static_cast<float>(ea.poses[ib].R[i]) : 0.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    ta[i] = act_a ? static_cast<float>(ea.poses[ia].t[i]) : 0.0f;
+    tb[i] = act_b ? static_cast<float>(ea.poses[ib].t[i]) : 0.0f;
+  }
+  const int f = fr.fidx[a];
+  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  const int* smp = ea.samples + static_cast<size_t>(a) * ea.scap + static_cast<size_t>(b) * ea.eta;
+  const int eta = ea.eta;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int s = threadIdx.x; s < eta; s += blockDim.x) es_off[s] = fr.gnm[fbase + smp[s]];
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive prefix of the per-sample mode counts
+    const int per = (eta + 31) / 32;
+    const int s0 = min(eta, lane * per), s1 = min(eta, s0 + per);
+    int local = 0;
+    for (int s = s0; s < s1; ++s) local += es_off[s];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - local;
+    for (int s = s0; s < s1; ++s) {
+      const int c = es_off[s];
+      es_off[s] = run;
+      run += c;
+    }
+    if (lane == 31) es_off[eta] = incl;
+  }
+  __syncthreads();
+  float Ea = 0.0f, Eb = 0.0f;
+  unsigned long long evals = 0, sevals = 0;
+  int s0 = 0;
+  while (s0 < eta) {
+    int lo = s0 + 1, hi = eta;  // largest s1 whose modes fit the staging budget
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (es_off[mid] - es_off[s0] <= kEnergyModeCap) lo = mid;
+      else hi = mid - 1;
+    }
+    const int s1 = lo;
+    // warp-cooperative staging: one warp per sample, lanes fetch 32 modes at a time
+    for (int s = s0 + wid; s < s1; s += nwarps) {
+      const size_t gb = fbase + smp[s];
+      if (lane == 0) es_cam[s - s0] = fr.gcam[gb];
+      const int nm = es_off[s + 1] - es_off[s];
+      if (nm == 0) continue;
+      SampleModes sm;
+      sample_modes(fr, pv.count, gb, lane, sm);
+      float4* dst = es_mode + 3 * (es_off[s] - es_off[s0]);
+      for (int j0 = 0; j0 < nm; j0 += 32) stage_modes(pv, sm, fr.T, nm, j0, lane, dst + 3 * j0);
+    }
+    __syncthreads();
+    const int cbase = es_off[s0];
+    for (int s = s0; s < s1; ++s) {
+      const int m0 = es_off[s] - cbase, m1 = es_off[s + 1] - cbase;
+      if (m1 == m0) continue;
+      const float4 c = es_cam[s - s0];
+      float ya[3], yb[3];
+      xform_f32(Ra, ta, c.x, c.y, c.z, ya);
+      xform_f32(Rb, tb, c.x, c.y, c.z, yb);
+      float qa = __int_as_float(0x7f800000), qb = qa;
+      for (int m = m0; m < m1; ++m) {
+        const float4 q0 = es_mode[3 * m + 0], q1 = es_mode[3 * m + 1], q2 = es_mode[3 * m + 2];
+        qa = fminf(qa, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(ya[0], q0.x), __fsub_rn(ya[1], q0.y),
+                                 __fsub_rn(ya[2], q0.z)));
+        qb = fminf(qb, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(yb[0], q0.x), __fsub_rn(yb[1], q0.y),
+                                 __fsub_rn(yb[2], q0.z)));
+      }
+      Ea = __fadd_rn(Ea, __fsqrt_rn(fmaxf(qa, 0.0f)));
+      Eb = __fadd_rn(Eb, __fsqrt_rn(fmaxf(qb, 0.0f)));
+      evals += static_cast<unsigned long long>(m1 - m0) * ((act_a ? 1u : 0u) + (act_b ? 1u : 0u));
+      sevals += (act_a ? 1u : 0u) + (act_b ? 1u : 0u);
+    }
+    __syncthreads();
+    s0 = s1;
+  }
+  if (ha < n) {
+    const float v = act_a ? Ea : __int_as_float(0x7f800000);
+    if (ea.kb == 0) ea.out[ia] = v;
+    else ea.out[ia * ea.kb + b] = v;
+  }
+  if (hb < n) {
+    const float v = act_b ? Eb : __int_as_float(0x7f800000);
+    if (ea.kb == 0) ea.out[ib] = v;
+    else ea.out[ib * ea.kb + b] = v;
+  }
+  if (work && (act_a || act_b)) {
+    atomicAdd(&work[W_MODE_EVALS], evals);
+    atomicAdd(&work[W_SAMPLE_EVALS], sevals);
+  }
+}
+
+// Re-scoring the <= 64 surviving hypotheses on one sample batch: warp per sample, lane l
+// owns hypotheses l and l + 32, so each predicted mode is loaded once per warp (uniform
+// load) and used for 2 x 32 hypotheses. Per-sample energies e[h][s] go to shared memory;
+// thread h then adds its row in sample order (the batch energy E_b, same bits as a
+// sequential sweep: samples without modes contribute +0).
+constexpr int kSmallHyps = 64;
 
 __global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs fr, PredView pv,
                                                       unsigned long long* __restrict__ work) {
@@ -1421,7 +1427,7 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   const size_t esmem = static_cast<size_t>(kEnergyModeCap) * 3 * sizeof(float4);
   {
     EnergyArgs ea{w.hyp, w.hok, p.n_max, nullptr, -1, w.samples, w.samples_cap, p.eta, 0, w.henergy, 0};
-    SCR_LAUNCH(s, K_ENERGY, (k_energy<<<dim3((p.n_max + 255) / 256, 1, nA), 256, esmem, s->stream>>>(ea, fr, pv, wk)));
+    SCR_LAUNCH(s, K_ENERGY, (k_energy<<<dim3((p.n_max + 511) / 512, 1, nA), 256, esmem, s->stream>>>(ea, fr, pv, wk)));
   }
   int P = 1;
   while (P < p.n_max) P <<= 1;
