@@ -195,3 +195,27 @@ def test_batch_invariance(world, gscene):
     single = [gscene.relocalise_batch(world.Dt[i:i + 1], world.RGBt[i:i + 1], p, 1, [5 + i])[0] for i in range(4)]
     for a, b in zip(full, single):
         assert bytes(a.pose) == bytes(b.pose) and a.score == b.score
+
+
+def test_features_match_reference_golden(gpu_device):
+    """GPU feature vectors on the reference-generated golden frame (tests/golden) — bit-exact."""
+    import os
+
+    import paper_1810_12163_b200 as P
+
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+    depth, rgb = G["frame_depth"], G["frame_rgb"]
+    h, w = depth.shape
+    blob = P.generate_random_forest(42, 3, 0.4, 1, 25)  # spec table = reference specs (seed 42, r 25)
+    s = P.Scene(gpu_device, blob, P.forest_params("default"), P.intrinsics(w, h, 60.0, 60.0), max_batch=1)
+    px, ref, st = G["feature_px"], G["feature_values"], G["feature_status"]
+    ok = px[st == 0]
+    got = s.debug_features(depth, rgb, ok)
+    assert np.array_equal(got.view(np.uint32), ref[st == 0].view(np.uint32))
+    import paper_1810_12163_b200.native as N
+
+    bad = px[st != 0][:1]
+    with pytest.raises(N.InvalidCentrePixel):
+        s.debug_features(depth, rgb, bad)
+    gpx, _ = s.debug_leaves(depth, rgb)
+    assert np.array_equal(gpx, G["grid_4"])
