@@ -1,0 +1,231 @@
+// screloc::gpu — header-only C++17 drop-in for the reference relocaliser API
+// (namespace screloc, proj/include/screloc/*.hpp + SPEC.md ops), backed by the B200 C ABI
+// in include/screloc_gpu.h. Names and argument order follow the reference:
+//   integrate_frame(state, forest, frame, pose)
+//   update_leaves_round_robin(state, leaves_per_call)
+//   clear_adaptation(state)
+//   relocalise(profile, frame, state, forest, model, mode) SPEC.md:646-654
+//   run_cascade(config, frame, ...)
+//   generate_random_forest / serialize_forest              forest.hpp:104-112
+// Errors are thrown as the reference's exception classes (core.hpp:24-72). Eigen value
+// types are replaced by POD RigidTransform / Intrinsics (Eigen is not a dependency here).
+#ifndef SCRELOC_GPU_RELOCALISER_HPP
+#define SCRELOC_GPU_RELOCALISER_HPP
+
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../screloc_gpu.h"
+
+namespace screloc {
+namespace gpu {
+
+// ---- exceptions (core.hpp:24-72) --------------------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& w) : std::runtime_error(w) {}
+};
+#define SCRELOC_GPU_ERROR(Name) \
+  class Name : public Error {   \
+   public:                      \
+    using Error::Error;         \
+  };
+SCRELOC_GPU_ERROR(InvalidDepth)
+SCRELOC_GPU_ERROR(InvalidCentrePixel)
+SCRELOC_GPU_ERROR(UnreliablePose)
+SCRELOC_GPU_ERROR(NoHypotheses)
+SCRELOC_GPU_ERROR(AllCandidatesFailed)
+SCRELOC_GPU_ERROR(DimensionMismatch)
+SCRELOC_GPU_ERROR(MalformedData)
+SCRELOC_GPU_ERROR(CudaError)
+#undef SCRELOC_GPU_ERROR
+
+inline void check(scr_status s, const char* what) {
+  if (s == SCR_OK) return;
+  const std::string msg = std::string(what) + ": " + scr_last_error();
+  switch (s) {
+    case SCR_E_INVALID_DEPTH: throw InvalidDepth(msg);
+    case SCR_E_INVALID_CENTRE_PIXEL: throw InvalidCentrePixel(msg);
+    case SCR_E_UNRELIABLE_POSE: throw UnreliablePose(msg);
+    case SCR_E_NO_HYPOTHESES: throw NoHypotheses(msg);
+    case SCR_E_ALL_CANDIDATES_FAILED: throw AllCandidatesFailed(msg);
+    case SCR_E_DIMENSION_MISMATCH: throw DimensionMismatch(msg);
+    case SCR_E_MALFORMED_DATA: throw MalformedData(msg);
+    case SCR_E_CUDA:
+    case SCR_E_OOM: throw CudaError(msg);
+    default: throw Error(msg);
+  }
+}
+
+// ---- value types -------------------------------------------------------------------------
+using RigidTransform = scr_pose;      // camera -> world, row-major R (geometry.hpp:14-42)
+using PinholeIntrinsics = scr_intrinsics;
+using RansacParams = scr_ransac_params;
+using ForestParams = scr_forest_params;
+
+inline RigidTransform identity_transform() {
+  RigidTransform T{};
+  T.R[0] = T.R[4] = T.R[8] = 1.0;
+  return T;
+}
+
+// RgbdFrame (features.hpp:31-44) as a borrowed view: depth metres (0/NaN invalid),
+// colour RGB8 interleaved, both row-major with x the column.
+struct RgbdFrame {
+  const float* depth = nullptr;
+  const uint8_t* colour = nullptr;
+  bool pose_reliable = true;
+  scr_frame c() const { return scr_frame{depth, colour, pose_reliable ? 1 : 0, 0}; }
+};
+
+enum class Mode : int { Raw = SCR_MODE_RAW, Icp = SCR_MODE_ICP, Ranked = SCR_MODE_RANKED };
+
+// Table 4; colour 30 / rigidity 0.05 m are SPEC.md:501-502 defaults.
+inline RansacParams profile(const std::string& name) {
+  RansacParams p{};
+  p.colour_thresh = 30.0f;
+  p.rigidity_tol = 0.05;
+  p.n_cull = 64;
+  if (name == "default") { p.max_gen_iters = 6000; p.n_max = 1024; p.eta = 512; p.pose_update = 1; p.use_cov = 1; p.min_sq_dist = 0.09; p.n_out = 16; }
+  else if (name == "fast") { p.max_gen_iters = 500; p.n_max = 2048; p.eta = 256; p.pose_update = 0; p.use_cov = 0; p.min_sq_dist = 0.0; p.n_out = 1; }
+  else if (name == "intermediate") { p.max_gen_iters = 1000; p.n_max = 2048; p.eta = 256; p.pose_update = 1; p.use_cov = 0; p.min_sq_dist = 0.09; p.n_out = 1; }
+  else if (name == "slow") { p.max_gen_iters = 250; p.n_max = 2048; p.eta = 256; p.pose_update = 1; p.use_cov = 0; p.min_sq_dist = 0.0225; p.n_out = 16; }
+  else throw Error("unknown relocaliser profile " + name);
+  return p;
+}
+inline ForestParams forest_profile(bool cascade) {
+  return cascade ? ForestParams{0.1f, 0.2f, 50, 5, 2048} : ForestParams{0.1f, 0.05f, 50, 20, 1024};
+}
+
+// CascadeConfig
+struct CascadeConfig {
+  std::vector<RansacParams> stages;
+  std::vector<Mode> modes;
+  std::vector<double> fallback_thresholds;  // stages.size() - 1, metres
+  static CascadeConfig paper_three_stage() {  // F(5 cm) -> I(7.5 cm) -> S
+    return {{profile("fast"), profile("intermediate"), profile("slow")}, {Mode::Icp, Mode::Icp, Mode::Ranked},
+            {0.05, 0.075}};
+  }
+};
+
+// RelocalisationResult
+struct RelocalisationResult {
+  std::optional<RigidTransform> final_pose;
+  double best_score = std::numeric_limits<double>::infinity();
+  int stage_used = 0;
+  int status = 0;
+  float stage_ms[4] = {0, 0, 0, 0};
+  static RelocalisationResult from(const scr_result& r) {
+    RelocalisationResult o;
+    if (r.has_pose) o.final_pose = r.pose;
+    o.best_score = r.score;
+    o.stage_used = r.stage_used;
+    o.status = r.status;
+    std::memcpy(o.stage_ms, r.stage_ms, sizeof(o.stage_ms));
+    return o;
+  }
+};
+
+// generate_random_forest + serialize_forest (forest.hpp:104-112)
+inline std::vector<uint8_t> generate_random_forest(uint64_t seed, int height = 14, double p_depth = 0.4,
+                                                   int trees = 5, int radius = 130) {
+  const size_t n = scr_generate_random_forest(seed, height, p_depth, trees, radius, nullptr, 0);
+  if (!n) throw Error("generate_random_forest: bad arguments");
+  std::vector<uint8_t> b(n);
+  scr_generate_random_forest(seed, height, p_depth, trees, radius, b.data(), n);
+  return b;
+}
+
+// ---- device + relocaliser (forest + adaptation state + scene model on one GPU) ------------
+class Device {
+ public:
+  explicit Device(int ordinal = 0) { check(scr_device_open(ordinal, &d_), "scr_device_open"); }
+  ~Device() { scr_device_close(d_); }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+  scr_device handle() const { return d_; }
+
+ private:
+  scr_device d_ = nullptr;
+};
+
+class Relocaliser {
+ public:
+  Relocaliser(Device& dev, const std::vector<uint8_t>& forest_blob, const ForestParams& fp,
+              const PinholeIntrinsics& k, uint64_t adapt_seed = 7, int max_batch = 64) {
+    check(scr_scene_create(dev.handle(), forest_blob.data(), forest_blob.size(), &fp, &k, adapt_seed, max_batch, &s_),
+          "deserialize_forest / scene create");
+  }
+  ~Relocaliser() { scr_scene_destroy(s_); }
+  Relocaliser(const Relocaliser&) = delete;
+  Relocaliser& operator=(const Relocaliser&) = delete;
+
+  void set_scene_model(const std::vector<scr_prim>& prims) {
+    check(scr_scene_set_analytic_model(s_, prims.data(), static_cast<int>(prims.size())), "set_scene_model");
+  }
+  // integrate_frame: throws UnreliablePose if !frame.pose_reliable
+  void integrate_frame(const RgbdFrame& frame, const RigidTransform& pose) {
+    const scr_frame f = frame.c();
+    check(scr_train(s_, &f, &pose), "integrate_frame");
+  }
+  void update_leaves_round_robin(int64_t leaves_per_call = 256) {
+    check(scr_update(s_, leaves_per_call), "update_leaves_round_robin");
+  }
+  void clear_adaptation() { check(scr_reset(s_), "clear_adaptation"); }
+  int64_t total_leaf_count() const { return scr_scene_total_leaves(s_); }
+
+  // relocalise; NoHypotheses / AllCandidatesFailed come back as a result
+  // without a pose (status set), exactly as the reference facade reports them.
+  RelocalisationResult relocalise(const RansacParams& p, const RgbdFrame& frame, Mode mode, uint64_t seed) {
+    return relocalise_batch(p, std::vector<RgbdFrame>{frame}, mode, std::vector<uint64_t>{seed}).front();
+  }
+  std::vector<RelocalisationResult> relocalise_batch(const RansacParams& p, const std::vector<RgbdFrame>& frames,
+                                                     Mode mode, const std::vector<uint64_t>& seeds) {
+    if (seeds.size() != frames.size()) throw DimensionMismatch("relocalise_batch: one seed per frame");
+    std::vector<scr_frame> f;
+    for (const auto& fr : frames) f.push_back(fr.c());
+    std::vector<scr_result> r(frames.size());
+    check(scr_relocalise_batch(s_, f.data(), static_cast<int>(f.size()), &p, static_cast<int>(mode), seeds.data(),
+                               r.data()),
+          "relocalise");
+    std::vector<RelocalisationResult> out;
+    for (const auto& x : r) out.push_back(RelocalisationResult::from(x));
+    return out;
+  }
+  // run_cascade
+  std::vector<RelocalisationResult> run_cascade_batch(const CascadeConfig& cfg, const std::vector<RgbdFrame>& frames,
+                                                      const std::vector<uint64_t>& seeds) {
+    if (cfg.fallback_thresholds.size() + 1 != cfg.stages.size() || cfg.modes.size() != cfg.stages.size())
+      throw DimensionMismatch("run_cascade: thresholds.length must be stages.length - 1");
+    if (seeds.size() != frames.size()) throw DimensionMismatch("run_cascade: one seed per frame");
+    std::vector<scr_frame> f;
+    for (const auto& fr : frames) f.push_back(fr.c());
+    std::vector<int32_t> modes;
+    for (Mode m : cfg.modes) modes.push_back(static_cast<int32_t>(m));
+    std::vector<scr_result> r(frames.size());
+    check(scr_cascade_batch(s_, f.data(), static_cast<int>(f.size()), cfg.stages.data(), modes.data(),
+                            cfg.fallback_thresholds.data(), static_cast<int>(cfg.stages.size()), seeds.data(),
+                            r.data()),
+          "run_cascade");
+    std::vector<RelocalisationResult> out;
+    for (const auto& x : r) out.push_back(RelocalisationResult::from(x));
+    return out;
+  }
+  RelocalisationResult run_cascade(const CascadeConfig& cfg, const RgbdFrame& frame, uint64_t seed) {
+    return run_cascade_batch(cfg, std::vector<RgbdFrame>{frame}, std::vector<uint64_t>{seed}).front();
+  }
+  scr_scene handle() const { return s_; }
+
+ private:
+  scr_scene s_ = nullptr;
+};
+
+}  // namespace gpu
+}  // namespace screloc
+
+#endif
