@@ -19,6 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
+# extra -D tuning knobs for experiments (e.g. SCR_NVCC_DEFS="-DSCR_HYPGEN_MINB=4")
+FLAGS += os.environ.get("SCR_NVCC_DEFS", "").split()
 
 
 def sources():

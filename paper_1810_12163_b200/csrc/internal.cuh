@@ -75,6 +75,7 @@ struct Workspace {
   int* gnm = nullptr;         // [cap * gmax] number of modes (union over trees)
   int4* grec = nullptr;       // [cap * gmax] {x|y<<16, depth bits, rgb | nm<<24, 6-bit counts of trees 0..4}
   uint4* gleaf = nullptr;     // [cap * gmax] 16-bit leaf ids of trees 0..7
+  double4* gcamd = nullptr;   // [cap * gmax] f64 camera point (backproject)
   // RANSAC (grown on demand)
   int nmax_cap = 0, ncull_cap = 0, samples_cap = 0;
   Pose* hyp = nullptr;        // [cap * nmax]

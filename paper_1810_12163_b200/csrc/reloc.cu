@@ -43,6 +43,7 @@ struct FrameRefs {  // per-batch views of the packed frames
   const int* gnm;
   const int4* grec;
   const uint4* gleaf;
+  const double4* gcamd;
   const uint2* tex;
   int gmax, T;
 };
@@ -117,24 +118,17 @@ SCR_DEV int mode_from_record(const int* lbase, uint32_t counts, uint4 lv, int pi
 // not set the register budget of the retry loop.
 __device__ __noinline__ bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return kabsch3(cm, w, *T); }
 
-// Checks 2-3 (distances in f64) and Kabsch for a triplet whose colour check passed
-// (SPEC.md:441-446). Out of line: its f64 temporaries stay out of the retry loop.
-__device__ __noinline__ bool geometry_checks_cold(const GenParams& gp, const FrameGeom& g, const PredView& pv,
-                                                  int4 A0, int4 A1, int4 A2, int m0, int m1, int m2, Pose* T) {
-  const float4 w0 = pv.geom[m0].q0, w1 = pv.geom[m1].q0, w2 = pv.geom[m2].q0;
-  double w[9], cm[9];
-  w[0] = w0.x; w[1] = w0.y; w[2] = w0.z;
-  w[3] = w1.x; w[4] = w1.y; w[5] = w1.z;
-  w[6] = w2.x; w[7] = w2.y; w[8] = w2.z;
-  const int4 Ak[3] = {A0, A1, A2};
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const int x = Ak[k].x & 0xffff, y = Ak[k].x >> 16;
-    const double dd = static_cast<double>(__int_as_float(Ak[k].y));
-    cm[3 * k + 0] = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
-    cm[3 * k + 1] = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
-    cm[3 * k + 2] = dd;
-  }
+// Checks 2-3 (distances in f64) and Kabsch for a triplet whose colour
+// check passed. Camera points come precomputed (f64 backprojection, K1).
+// Scalars and pointers only: passing the kernel-parameter structs by reference would force
+// copies of them into local memory.
+__device__ __noinline__ bool geometry_checks(double min_sq_dist, double rigidity_tol, const double4* gcamd,
+                                             const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1, int m2,
+                                             Pose* T) {
+  const float4 w0 = geom[m0].q0, w1 = geom[m1].q0, w2 = geom[m2].q0;
+  const double4 c0 = gcamd[g0], c1 = gcamd[g1], c2 = gcamd[g2];
+  double w[9] = {w0.x, w0.y, w0.z, w1.x, w1.y, w1.z, w2.x, w2.y, w2.z};
+  double cm[9] = {c0.x, c0.y, c0.z, c1.x, c1.y, c1.z, c2.x, c2.y, c2.z};
   double dw2[3], dc2[3];
   bool close = false;
 #pragma unroll
@@ -144,22 +138,37 @@ __device__ __noinline__ bool geometry_checks_cold(const GenParams& gp, const Fra
     dw2[q] = (ax * ax + ay * ay) + az * az;
     const double bx = cm[3 * pa] - cm[3 * pb], by = cm[3 * pa + 1] - cm[3 * pb + 1], bz = cm[3 * pa + 2] - cm[3 * pb + 2];
     dc2[q] = (bx * bx + by * by) + bz * bz;
-    if (dw2[q] < gp.min_sq_dist) close = true;
+    if (dw2[q] < min_sq_dist) close = true;
   }
   if (close) return false;
 #pragma unroll
   for (int q = 0; q < 3; ++q)
-    if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > gp.rigidity_tol) return false;
-  return kabsch3(cm, w, *T);
+    if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > rigidity_tol) return false;
+  return kabsch3_cold(cm, w, T);
 }
 
-__global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
+// Per-warp queue of colour-check survivors, evaluated 32 at a time at full SIMD width.
+#ifndef SCR_HYPGEN_MINB
+#define SCR_HYPGEN_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
+constexpr int kGenWarps = 4;
+constexpr int kGenQ = 64;
+struct GenCand {
+  int slot, owner_att;  // owner lane | attempt << 5
+  int g0, g1, g2, m0, m1, m2;
+};
+
+__global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
                                                    const uint64_t* __restrict__ seeds, int* __restrict__ slot_ctr,
                                                    Pose* __restrict__ hyp, int* __restrict__ hok,
                                                    int* __restrict__ hiters, unsigned long long* __restrict__ work) {
   __shared__ uint64_t s_m[kMaxModeUnion + 1];    // Barrett reciprocal for mode counts 1..400
   __shared__ uint64_t s_thr[kMaxModeUnion + 1];  // rejection threshold (2^64 mod n)
   __shared__ int s_lbase[kMaxTrees];
+  __shared__ GenCand s_q[kGenWarps][kGenQ];
+  __shared__ int s_best[kGenWarps][32];  // smallest passing attempt of the lane's slot
+  __shared__ int s_pend[kGenWarps][32];  // queued, unevaluated candidates of the lane's slot
+  __shared__ int s_cur[kGenWarps][32];   // slot the lane currently owns
   for (int i = threadIdx.x; i <= kMaxModeUnion; i += blockDim.x) {
     const uint64_t n = i ? static_cast<uint64_t>(i) : 1;
     const uint64_t m = barrett_m(n);
@@ -167,6 +176,10 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
     s_thr[i] = mod_barrett(0 - n, n, m);
   }
   if (threadIdx.x < kMaxTrees) s_lbase[threadIdx.x] = gp.leaf_base[threadIdx.x];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  s_best[wid][lane] = 0x7fffffff;
+  s_pend[wid][lane] = 0;
+  s_cur[wid][lane] = -1;
   __syncthreads();
   const int a = blockIdx.y;
   const int f = fr.fidx[a];
@@ -175,98 +188,118 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
   const uint64_t m3 = 0x5555555555555555ull, t3 = 1;  // floor((2^64-1)/3), 2^64 mod 3
   const bool fast = gp.fast != 0;
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  GenCand* q = s_q[wid];
+  int qn = 0;  // warp-uniform queue length
   unsigned long long attempts_total = 0;
-  for (int slot = atomicAdd(&slot_ctr[a], 1); slot < gp.nmax; slot = atomicAdd(&slot_ctr[a], 1)) {
-    const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
-    Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(slot));
-    RawBuf buf;
-    buf.fill(rng);
-    int ok = 0, it = 0;
-    Pose T;
-    if (G > 0) {
-      for (it = 0; it < gp.max_iters; ++it) {
-        int4 A0, A1, A2;
-        uint4 L0, L1, L2;
-        int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0, consumed = 0;
-        bool proceed = false;
-        const bool spec = fast && buf.b0 >= tG && buf.b2 >= tG && buf.b4 >= tG;
-        bool slow = !spec;
-        if (spec) {
-          g0 = static_cast<int>(mod_barrett(buf.b0, G, mG));
-          g1 = static_cast<int>(mod_barrett(buf.b2, G, mG));
-          g2 = static_cast<int>(mod_barrett(buf.b4, G, mG));
-          A0 = fr.grec[fbase + g0];
-          A1 = fr.grec[fbase + g1];
-          A2 = fr.grec[fbase + g2];
-          L0 = fr.gleaf[fbase + g0];
-          L1 = fr.gleaf[fbase + g1];
-          L2 = fr.gleaf[fbase + g2];
-          const int nm0 = static_cast<uint32_t>(A0.z) >> 24;
-          const int nm1 = static_cast<uint32_t>(A1.z) >> 24;
-          const int nm2 = static_cast<uint32_t>(A2.z) >> 24;
-          if (nm0 == 0) {
-            consumed = 1;
-          } else if (buf.b1 < s_thr[nm0]) {
+  int slot = -1, it = 0;
+  bool exhausted = false;
+  Rng rng;
+  RawBuf buf;
+  for (;;) {
+    if (slot < 0 && !exhausted) {
+      slot = atomicAdd(&slot_ctr[a], 1);
+      if (slot >= gp.nmax) {
+        slot = -1;
+        exhausted = true;
+      } else if (G == 0) {  // no valid pixels: the slot fails without drawing
+        const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
+        hok[out] = 0;
+        hiters[out] = gp.max_iters;
+        slot = -1;
+      } else {
+        rng = rng_stream(seeds[a], static_cast<uint64_t>(slot));
+        buf.fill(rng);
+        it = 0;
+        s_cur[wid][lane] = slot;
+      }
+    }
+    if (__all_sync(0xffffffffu, exhausted) && qn == 0) break;
+    // ---- one attempt per lane that still has attempts left
+    bool push = false;
+    GenCand c;
+    if (slot >= 0 && it < gp.max_iters) {
+      int4 A0, A1, A2;
+      uint4 L0, L1, L2;
+      int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0, consumed = 0;
+      bool proceed = false;
+      const bool spec = fast && buf.b0 >= tG && buf.b2 >= tG && buf.b4 >= tG;
+      bool slow = !spec;
+      if (spec) {
+        g0 = static_cast<int>(mod_barrett(buf.b0, G, mG));
+        g1 = static_cast<int>(mod_barrett(buf.b2, G, mG));
+        g2 = static_cast<int>(mod_barrett(buf.b4, G, mG));
+        A0 = fr.grec[fbase + g0];
+        A1 = fr.grec[fbase + g1];
+        A2 = fr.grec[fbase + g2];
+        L0 = fr.gleaf[fbase + g0];
+        L1 = fr.gleaf[fbase + g1];
+        L2 = fr.gleaf[fbase + g2];
+        const int nm0 = static_cast<uint32_t>(A0.z) >> 24;
+        const int nm1 = static_cast<uint32_t>(A1.z) >> 24;
+        const int nm2 = static_cast<uint32_t>(A2.z) >> 24;
+        if (nm0 == 0) {
+          consumed = 1;
+        } else if (buf.b1 < s_thr[nm0]) {
+          slow = true;
+        } else {
+          p0 = static_cast<int>(mod_barrett(buf.b1, nm0, s_m[nm0]));
+          if (nm1 == 0) {
+            consumed = 3;
+          } else if (buf.b3 < s_thr[nm1]) {
             slow = true;
           } else {
-            p0 = static_cast<int>(mod_barrett(buf.b1, nm0, s_m[nm0]));
-            if (nm1 == 0) {
-              consumed = 3;
-            } else if (buf.b3 < s_thr[nm1]) {
+            p1 = static_cast<int>(mod_barrett(buf.b3, nm1, s_m[nm1]));
+            if (nm2 == 0) {
+              consumed = 5;
+            } else if (buf.b5 < s_thr[nm2]) {
               slow = true;
             } else {
-              p1 = static_cast<int>(mod_barrett(buf.b3, nm1, s_m[nm1]));
-              if (nm2 == 0) {
-                consumed = 5;
-              } else if (buf.b5 < s_thr[nm2]) {
+              p2 = static_cast<int>(mod_barrett(buf.b5, nm2, s_m[nm2]));
+              if (buf.b6 < t3) {
                 slow = true;
               } else {
-                p2 = static_cast<int>(mod_barrett(buf.b5, nm2, s_m[nm2]));
-                if (buf.b6 < t3) {
-                  slow = true;
-                } else {
-                  cc = static_cast<int>(mod_barrett(buf.b6, 3, m3));
-                  consumed = 7;
-                  proceed = true;
-                }
-              }
-            }
-          }
-        }
-        if (slow) {  // exact sequential replay of the attempt from the buffered stream
-          proceed = false;
-          g0 = static_cast<int>(buf.draw(rng, G, mG, tG));
-          A0 = fr.grec[fbase + g0];
-          L0 = fr.gleaf[fbase + g0];
-          const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
-          if (nm0 > 0) {
-            p0 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
-            g1 = static_cast<int>(buf.draw(rng, G, mG, tG));
-            A1 = fr.grec[fbase + g1];
-            L1 = fr.gleaf[fbase + g1];
-            const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
-            if (nm1 > 0) {
-              p1 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
-              g2 = static_cast<int>(buf.draw(rng, G, mG, tG));
-              A2 = fr.grec[fbase + g2];
-              L2 = fr.gleaf[fbase + g2];
-              const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
-              if (nm2 > 0) {
-                p2 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
-                cc = static_cast<int>(buf.draw(rng, 3, m3, t3));
+                cc = static_cast<int>(mod_barrett(buf.b6, 3, m3));
+                consumed = 7;
                 proceed = true;
               }
             }
           }
-        } else {
-          switch (consumed) {  // advance the stream by the raw values this attempt used
-            case 1: buf.pop(rng); break;
-            case 3: buf.pop(rng); buf.pop(rng); buf.pop(rng); break;
-            case 5: buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); break;
-            default: buf.fill(rng); break;
+        }
+      }
+      if (slow) {  // exact sequential replay of the attempt from the buffered stream
+        proceed = false;
+        g0 = static_cast<int>(buf.draw(rng, G, mG, tG));
+        A0 = fr.grec[fbase + g0];
+        L0 = fr.gleaf[fbase + g0];
+        const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
+        if (nm0 > 0) {
+          p0 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
+          g1 = static_cast<int>(buf.draw(rng, G, mG, tG));
+          A1 = fr.grec[fbase + g1];
+          L1 = fr.gleaf[fbase + g1];
+          const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
+          if (nm1 > 0) {
+            p1 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
+            g2 = static_cast<int>(buf.draw(rng, G, mG, tG));
+            A2 = fr.grec[fbase + g2];
+            L2 = fr.gleaf[fbase + g2];
+            const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
+            if (nm2 > 0) {
+              p2 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
+              cc = static_cast<int>(buf.draw(rng, 3, m3, t3));
+              proceed = true;
+            }
           }
         }
-        if (!proceed) continue;
+      } else {
+        switch (consumed) {  // advance the stream by the raw values this attempt used
+          case 1: buf.pop(rng); break;
+          case 3: buf.pop(rng); buf.pop(rng); buf.pop(rng); break;
+          case 5: buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); break;
+          default: buf.fill(rng); break;
+        }
+      }
+      if (proceed) {
         int m0, m1, m2;
         if (fast) {
           m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), L0, p0);
@@ -277,24 +310,85 @@ __global__ void __launch_bounds__(128, 8) k_hypgen(GenParams gp, FrameGeom g, Fr
           m1 = mode_index(fr, pv.count, fbase + g1, p1);
           m2 = mode_index(fr, pv.count, fbase + g2, p2);
         }
-        {
-          const uint32_t col = static_cast<uint32_t>(cc == 0 ? A0.z : (cc == 1 ? A1.z : A2.z));
-          const float4 mc = pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)];
-          float linf = 0.0f;
-          linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
-          linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 8) & 255u), mc.y)));
-          linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 16) & 255u), mc.z)));
-          if (linf > gp.colour_thresh) continue;
+        const uint32_t col = static_cast<uint32_t>(cc == 0 ? A0.z : (cc == 1 ? A1.z : A2.z));
+        const float4 mc = pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)];
+        float linf = 0.0f;
+        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
+        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 8) & 255u), mc.y)));
+        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 16) & 255u), mc.z)));
+        if (!(linf > gp.colour_thresh)) {
+          push = true;
+          c.slot = slot;
+          c.owner_att = lane | (it << 5);
+          c.g0 = g0; c.g1 = g1; c.g2 = g2;
+          c.m0 = m0; c.m1 = m1; c.m2 = m2;
+          s_pend[wid][lane] += 1;
         }
-        if (!geometry_checks_cold(gp, g, pv, A0, A1, A2, m0, m1, m2, &T)) continue;
-        ok = 1;
-        break;
       }
+      ++it;
     }
-    if (ok) hyp[out] = T;
-    hok[out] = ok;
-    hiters[out] = ok ? it + 1 : gp.max_iters;
-    attempts_total += static_cast<unsigned long long>(ok ? it + 1 : (G > 0 ? gp.max_iters : 0));
+    const unsigned pm = __ballot_sync(0xffffffffu, push);
+    if (push) q[qn + __popc(pm & ((1u << lane) - 1u))] = c;
+    qn += __popc(pm);
+    // slots that used all attempts with nothing pending have failed
+    if (slot >= 0 && it >= gp.max_iters && s_pend[wid][lane] == 0) {
+      const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
+      hok[out] = 0;
+      hiters[out] = gp.max_iters;
+      attempts_total += static_cast<unsigned long long>(gp.max_iters);
+      s_cur[wid][lane] = -1;
+      slot = -1;
+    }
+    __syncwarp();
+    const bool waiting = slot >= 0 && it >= gp.max_iters;
+    const bool idle = slot < 0 && exhausted;
+    if (qn >= 32 || (qn > 0 && (__any_sync(0xffffffffu, waiting) || __all_sync(0xffffffffu, idle)))) {
+      // ---- evaluate the oldest <= 32 candidates, one per lane
+      const int nproc = qn < 32 ? qn : 32;
+      bool pass = false;
+      int owner = 0, att = 0, eslot = -1;
+      Pose T;
+      if (lane < nproc) {
+        const GenCand e = q[lane];
+        owner = e.owner_att & 31;
+        att = e.owner_att >> 5;
+        eslot = e.slot;
+        if (s_cur[wid][owner] == eslot) {  // stale if the owner's slot was already resolved
+          pass = geometry_checks(gp.min_sq_dist, gp.rigidity_tol, fr.gcamd + fbase, pv.geom, e.g0, e.g1, e.g2, e.m0, e.m1, e.m2, &T);
+          atomicSub(&s_pend[wid][owner], 1);
+          if (pass) atomicMin(&s_best[wid][owner], att);
+        }
+      }
+      __syncwarp();
+      if (pass && s_best[wid][owner] == att) hyp[static_cast<size_t>(a) * gp.nmax + eslot] = T;
+      // drop the evaluated entries
+      GenCand keep;
+      const int rest = qn - nproc;
+      if (lane < rest) keep = q[nproc + lane];
+      __syncwarp();
+      if (lane < rest) q[lane] = keep;
+      qn = rest;
+      // owners whose slot now has a winner
+      if (slot >= 0 && s_best[wid][lane] != 0x7fffffff) {
+        const int best = s_best[wid][lane];
+        const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
+        hok[out] = 1;
+        hiters[out] = best + 1;
+        attempts_total += static_cast<unsigned long long>(best + 1);
+        s_best[wid][lane] = 0x7fffffff;
+        s_pend[wid][lane] = 0;
+        s_cur[wid][lane] = -1;
+        slot = -1;
+      } else if (slot >= 0 && it >= gp.max_iters && s_pend[wid][lane] == 0) {
+        const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
+        hok[out] = 0;
+        hiters[out] = gp.max_iters;
+        attempts_total += static_cast<unsigned long long>(gp.max_iters);
+        s_cur[wid][lane] = -1;
+        slot = -1;
+      }
+      __syncwarp();
+    }
   }
   if (work) atomicAdd(&work[W_GEN_ATTEMPTS], attempts_total);
 }
@@ -1362,6 +1456,7 @@ FrameRefs frame_refs(scr_scene s) {
   fr.gnm = s->ws.gnm;
   fr.grec = s->ws.grec;
   fr.gleaf = s->ws.gleaf;
+  fr.gcamd = s->ws.gcamd;
   fr.tex = s->ws.tex;
   fr.gmax = s->ws.gmax;
   fr.T = s->T;

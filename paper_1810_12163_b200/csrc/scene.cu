@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
                                                 const int* __restrict__ gcount, const int* __restrict__ gpx,
                                                 int gmax, int* __restrict__ gslot, int* __restrict__ gnm,
                                                 float4* __restrict__ gcam, int4* __restrict__ grec,
-                                                uint4* __restrict__ gleaf, const int* __restrict__ pcount,
-                                                unsigned long long* __restrict__ work) {
+                                                uint4* __restrict__ gleaf, double4* __restrict__ gcamd,
+                                                const int* __restrict__ pcount, unsigned long long* __restrict__ work) {
   __shared__ short4 sspec[kFeatures];
   for (int i = threadIdx.x; i < kFeatures; i += blockDim.x) sspec[i] = fv.specs[i];
   __syncthreads();
@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
   const double X = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
   const double Y = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
   gcam[gidx] = make_float4(static_cast<float>(X), static_cast<float>(Y), static_cast<float>(dd), 0.0f);
+  gcamd[gidx] = make_double4(X, Y, dd, 0.0);  // backproject (geometry.hpp:198) in f64 for the generation checks
 }
 
 // Debug: full 256-D feature vectors at given pixels (features.cpp:60-65).
@@ -756,6 +757,7 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.grec, B * w.gmax)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.gleaf, B * w.gmax)) != SCR_OK) return fail(st);
+  if ((st = dalloc(&w.gcamd, B * w.gmax)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.fidx, B)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return fail(st);
   if ((st = dalloc(&w.status, B)) != SCR_OK) return fail(st);
@@ -786,7 +788,7 @@ void scr_scene_destroy(scr_scene s) {
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
-                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.gleaf, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
+                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.gleaf, s->ws.gcamd, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
                   s->ws.ins_rank, s->ws.ins_total};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -889,7 +891,7 @@ scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_
   SCR_LAUNCH(s, K_LEAVES,
              (k_leaves<<<dim3((w.gmax + 127) / 128, n), 128, 0, s->stream>>>(
                  s->forest_view(), s->geom, w.tex, w.gcount, w.gpx, w.gmax, w.gslot, w.gnm, w.gcam, w.grec,
-                 w.gleaf, s->d_count, work_ptr(s))));
+                 w.gleaf, w.gcamd, s->d_count, work_ptr(s))));
   SCR_CUDA(cudaGetLastError());
   return SCR_OK;
 }
