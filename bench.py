@@ -90,6 +90,8 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.window = None
+        self.window_note = "timed region"
 
     def __enter__(self):
         try:
@@ -104,7 +106,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, t0: float, t1: float):
+        """Restrict the summary to samples taken inside [t0, t1] (wall clock)."""
+        self.window = (t0, t1)
 
     def __exit__(self, *exc):
         if self.proc:
@@ -117,7 +123,14 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if self.window is not None:
+            inside = [x for x in lines if self.window[0] - 0.06 <= x[0] <= self.window[1] + 0.06]
+            if not inside:  # very short timed region: include the (equally loaded) warm-up just before it
+                inside = [x for x in lines if self.window[0] - 2.0 <= x[0] <= self.window[1] + 0.06]
+                self.window_note = "timed region + 2 s of warm-up before it"
+            lines = inside
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -130,7 +143,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": self.window_note if self.window else "whole run"}
 
 
 def measured_peaks() -> dict:
@@ -147,6 +160,30 @@ def measured_peaks() -> dict:
 # point-to-plane terms = 110 per live pixel-iteration; analytic ray cast = 25 flops per
 # primitive tested per ray.
 FLOPS = {"mode_eval": 18, "sample_eval": 24, "lm_term": 170, "icp_term": 110, "ray_prim": 25}
+
+
+# ALU-op model of one hypothesis-generation attempt, 32-bit lane ops:
+# 7 xoshiro256** outputs at ~21 ops each + 7 exact 64-bit Barrett reductions with rejection
+# test at ~23 ops each, 3 mode lookups from the pixel record (~14 each), the colour check
+# (~12) and the 6 record addresses (~12). K4 is issue-bound (integer ALU), not FP or HBM.
+GEN_OPS_PER_ATTEMPT = 7 * 21 + 7 * 23 + 3 * 14 + 12 + 12
+
+
+def kernel_model(name: str, work: dict) -> tuple | None:
+    """(algorithmic work, bound, unit scale) of a kernel from the device work counters."""
+    if name == "k_hypgen":
+        return GEN_OPS_PER_ATTEMPT * work["gen_attempts"], "alu"
+    f = kernel_flops(name, work, 0)
+    return (f, "fp32") if f is not None else None
+
+
+def ncu_traffic() -> dict:
+    """DRAM bytes per launch from the committed `ncu --set full` summary (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "ncu_kernels.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f).get("kernels", {})
 
 
 def kernel_flops(name: str, work: dict, n_prims: int) -> float | None:
@@ -233,6 +270,7 @@ def run_ours(args):
         return idx, [seeds_all[i] for i in idx]
 
     stream = torch.cuda.ExternalStream(scene.stream, device=dev_t)
+    clk = ClockSampler(local).__enter__()  # nvidia-smi needs ~1 s to start: launch it before warm-up
     for w in range(args.warmup):
         idx, sd = batch_at(w)
         fs.cascade(idx, cfg, sd)
@@ -244,18 +282,21 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for st in range(args.steps):
-            idx, sd = batch_at(args.warmup + st)
-            res = fs.cascade(idx, cfg, sd)
-            results.append((idx, res))
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    tw0 = time.time()
+    ev0.record(stream)
+    for st in range(args.steps):
+        idx, sd = batch_at(args.warmup + st)
+        res = fs.cascade(idx, cfg, sd)
+        results.append((idx, res))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    if dist is not None:
+        dist.barrier()
+    clk.mark(tw0, tw1)
+    clk.__exit__(None, None, None)
     elapsed_ms = ev0.elapsed_time(ev1)
     launches = scene.kernel_launches - launches0
     elapsed_max = max_over_ranks(elapsed_ms, dist, dev_t)
@@ -316,20 +357,38 @@ def run_ours(args):
     h2d = B * (k.width * k.height * 4 + k.width * k.height * 3)
     d2h = B * 136
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel (+ the other modelled kernels)
     peaks = measured_peaks()
     kern = prof["kernels"]
     dom = max(kern, key=lambda n: kern[n]["ms"])
-    n_prims = len(prims)
-    flops = kernel_flops(dom, prof["work"], n_prims)
-    fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
-    roofline = {"kernel": dom, "bound": "fp32", "unit": "TFLOP/s", "peak": round(fp32_peak, 2),
-                "peak_source": "nominal FP32 FMA pipe 148 SM x 128 FMA/clk x 2 at sm_max_mhz of MEASURED_PEAKS.json",
-                "traffic": None, "kernel_ms": round(kern[dom]["ms"], 3), "launches": kern[dom]["launches"]}
-    if flops is not None and kern[dom]["ms"] > 0:
-        ach = flops / (kern[dom]["ms"] / 1e3) / 1e12
-        roofline.update({"achieved": round(ach, 3), "frac": round(ach / fp32_peak, 4),
-                         "flops_per_launch": flops / max(1, kern[dom]["launches"])})
+    clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_of = {"fp32": (148 * 128 * 2 * clk_mhz * 1e6 / 1e12, "TFLOP/s",
+                        "nominal FP32 FMA pipe: 148 SM x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS.json)"),
+               "alu": (148 * 128 * clk_mhz * 1e6 / 1e12, "Tops/s",
+                       "nominal 32-bit ALU issue: 148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)")}
+    traffic = ncu_traffic()
+
+    def roof(name):
+        k = kern[name]
+        m = kernel_model(name, prof["work"])
+        r = {"kernel": name, "kernel_ms": round(k["ms"], 3), "launches": k["launches"],
+             "traffic": traffic.get(name, {}).get("dram_bytes_per_launch")}
+        if m is None or k["ms"] <= 0:
+            r.update({"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None})
+            return r
+        work_units, bound = m
+        pk, unit, src = peak_of[bound]
+        ach = work_units / (k["ms"] / 1e3) / 1e12
+        r.update({"bound": bound, "achieved": round(ach, 3), "peak": round(pk, 2), "unit": unit,
+                  "frac": round(ach / pk, 4), "peak_source": src,
+                  "work_per_launch": work_units / max(1, k["launches"])})
+        if r["traffic"] is not None:
+            r["traffic_source"] = "profiles/ncu_kernels.json (ncu --set full, dram__bytes_read+write per launch)"
+        return r
+
+    roofline = roof(dom)
+    rooflines = {n: roof(n) for n in sorted(kern, key=lambda n: -kern[n]["ms"])[:5]
+                 if n != dom and kernel_model(n, prof["work"]) is not None}
     share = {n: round(v["ms"] / max(1e-9, sum(x["ms"] for x in kern.values())), 4) for n, v in kern.items() if v["ms"] > 0}
 
     out = {
@@ -344,6 +403,7 @@ def run_ours(args):
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(sum_over_ranks(float(launches), dist, dev_t)),
         "roofline": roofline,
+        "rooflines_other": rooflines,
         "clocks": clk.summary(),
         "accuracy": {"success_5cm_5deg": round(succ, 4), "frames": n_res, "stage_mix": stage_hist},
         "kernel_share": share,

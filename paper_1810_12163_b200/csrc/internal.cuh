@@ -21,7 +21,7 @@ scr_status cuda_fail(cudaError_t e, const char* what);
 // ---- in-library profiler: CUDA events around every launch on the scene stream --------
 enum KernelId {
   K_PACK, K_GRID, K_LEAVES, K_HYPGEN, K_SAMPLES, K_ENERGY, K_SELECT, K_LM, K_ICP, K_FINALIZE, K_INSERT, K_RQS,
-  K_RENDER, K_COUNT
+  K_RENDER, K_COMPACT, K_COUNT
 };
 // device work counters (u64), indexed by W_*; meaning documented in DESIGN.md "Roofline"
 enum WorkId {
@@ -82,6 +82,9 @@ struct Workspace {
   float* henergy = nullptr;   // [cap * nmax]
   int* hok = nullptr;         // [cap * nmax]
   int* hiters = nullptr;      // [cap * nmax]
+  Pose* hypc = nullptr;       // generated hypotheses compacted in slot order [cap * nmax]
+  int* hslot = nullptr;       // their generation slots [cap * nmax]
+  int* hvalid = nullptr;      // number generated per frame [cap]
   Pose* cand = nullptr;       // [cap * ncull]
   float* cenergy = nullptr;   // [cap * ncull]
   int* cslot = nullptr;       // [cap * ncull]

@@ -122,7 +122,12 @@ __device__ __noinline__ bool kabsch3_cold(const double* cm, const double* w, Pos
 // check passed. Camera points come precomputed (f64 backprojection, K1).
 // Scalars and pointers only: passing the kernel-parameter structs by reference would force
 // copies of them into local memory.
-__device__ __noinline__ bool geometry_checks(double min_sq_dist, double rigidity_tol, const double4* gcamd,
+#ifdef SCR_GEOM_NOINLINE
+__device__ __noinline__
+#else
+SCR_DEV
+#endif
+bool geometry_checks(double min_sq_dist, double rigidity_tol, const double4* gcamd,
                                              const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1, int m2,
                                              Pose* T) {
   const float4 w0 = geom[m0].q0, w1 = geom[m1].q0, w2 = geom[m2].q0;
@@ -440,6 +445,56 @@ SCR_DEV void sample_modes(const FrameRefs& fr, const int* pcount, size_t gb, int
   }
 }
 
+// ================================ K4b: compaction of generated hypotheses ===================
+// Most generation slots exhaust their attempts (hok = 0); scoring only the generated ones,
+// in slot order with their slot kept as the tie-break key, selects exactly what scoring all
+// n_max slots with +inf for the failed ones would.
+constexpr int kCompactThreads = 1024;
+
+__global__ void __launch_bounds__(kCompactThreads) k_compact(const Pose* __restrict__ hyp, const int* __restrict__ hok,
+                                                            int nmax, Pose* __restrict__ hypc, int* __restrict__ hslot,
+                                                            int* __restrict__ hvalid) {
+  __shared__ int s_warp[kCompactThreads / 32];
+  const int a = blockIdx.x;
+  const size_t base = static_cast<size_t>(a) * nmax;
+  const int per = (nmax + kCompactThreads - 1) / kCompactThreads;  // consecutive slots per thread (<= 4)
+  const int i0 = min(nmax, threadIdx.x * per), i1 = min(nmax, i0 + per);
+  int mask = 0, cnt = 0;
+  for (int i = i0; i < i1; ++i)
+    if (hok[base + i]) {
+      mask |= 1 << (i - i0);
+      ++cnt;
+    }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int w = s_warp[lane];
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    s_warp[lane] = wi - w;
+    if (lane == 31) hvalid[a] = wi;
+  }
+  __syncthreads();
+  int pos = s_warp[wid] + incl - cnt;
+  for (int i = i0; i < i1; ++i)
+    if (mask >> (i - i0) & 1) {
+      hypc[base + pos] = hyp[base + i];
+      hslot[base + pos] = i;
+      ++pos;
+    }
+}
+
 // Lane l stages mode j0 + l of the sample into buf[3 l .. 3 l + 2] (coalesced fetch, one
 // L2 round trip per 32 modes); returns the global mode index it staged (-1 if none).
 SCR_DEV int stage_modes(const PredView& pv, const SampleModes& sm, int T, int nm, int j0, int lane, float4* buf) {
@@ -461,7 +516,6 @@ SCR_DEV int stage_modes(const PredView& pv, const SampleModes& sm, int T, int nm
 }
 
 
-constexpr int kEnergyModeCap = 1024;    // staged modes per chunk: 1024 x 48 B = 48 KB
 constexpr int kEnergySampleCap = 512;   // eta <= 512 (Table 4)
 constexpr int kEnergyBatches = 8;       // sample batches per frame (1 + halvings)
 
@@ -477,126 +531,13 @@ struct EnergyArgs {
   int kb;  // 0: out[a*stride + h] = E_b; else out[(a*stride + h)*kb + b] = E_b
 };
 
-__global__ void __launch_bounds__(256) k_energy(EnergyArgs ea, FrameRefs fr, PredView pv,
-                                                unsigned long long* __restrict__ work) {
-  extern __shared__ float4 es_mode[];  // kEnergyModeCap * 3
-  __shared__ float4 es_cam[kEnergySampleCap];
-  __shared__ int es_off[kEnergySampleCap + 1];
-  const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
-  const int n = ea.nper ? ea.nper[a] : ea.stride;
-  if (n <= ea.min_n) return;
-  const int h0 = blockIdx.x * (2 * blockDim.x);  // each thread owns hypotheses h and h + blockDim
-  if (h0 >= n) return;
-  const int ha = h0 + threadIdx.x, hb = ha + blockDim.x;
-  const size_t ia = static_cast<size_t>(a) * ea.stride + ha, ib = static_cast<size_t>(a) * ea.stride + hb;
-  const bool act_a = ha < n && (!ea.ok || ea.ok[ia]);
-  const bool act_b = hb < n && (!ea.ok || ea.ok[ib]);
-  float Ra[9], ta[3], Rb[9], tb[3];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    Ra[i] = act_a ? static_cast<float>(ea.poses[ia].R[i]) : 0.0f;
-    Rb[i] = act_b ? static_cast<float>(ea.poses[ib].R[i]) : 0.0f;
-  }
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    ta[i] = act_a ? static_cast<float>(ea.poses[ia].t[i]) : 0.0f;
-    tb[i] = act_b ? static_cast<float>(ea.poses[ib].t[i]) : 0.0f;
-  }
-  const int f = fr.fidx[a];
-  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
-  const int* smp = ea.samples + static_cast<size_t>(a) * ea.scap + static_cast<size_t>(b) * ea.eta;
-  const int eta = ea.eta;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int s = threadIdx.x; s < eta; s += blockDim.x) es_off[s] = fr.gnm[fbase + smp[s]];
-  __syncthreads();
-  if (threadIdx.x < 32) {  // exclusive prefix of the per-sample mode counts
-    const int per = (eta + 31) / 32;
-    const int s0 = min(eta, lane * per), s1 = min(eta, s0 + per);
-    int local = 0;
-    for (int s = s0; s < s1; ++s) local += es_off[s];
-    int incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    int run = incl - local;
-    for (int s = s0; s < s1; ++s) {
-      const int c = es_off[s];
-      es_off[s] = run;
-      run += c;
-    }
-    if (lane == 31) es_off[eta] = incl;
-  }
-  __syncthreads();
-  float Ea = 0.0f, Eb = 0.0f;
-  unsigned long long evals = 0, sevals = 0;
-  int s0 = 0;
-  while (s0 < eta) {
-    int lo = s0 + 1, hi = eta;  // largest s1 whose modes fit the staging budget
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (es_off[mid] - es_off[s0] <= kEnergyModeCap) lo = mid;
-      else hi = mid - 1;
-    }
-    const int s1 = lo;
-    // warp-cooperative staging: one warp per sample, lanes fetch 32 modes at a time
-    for (int s = s0 + wid; s < s1; s += nwarps) {
-      const size_t gb = fbase + smp[s];
-      if (lane == 0) es_cam[s - s0] = fr.gcam[gb];
-      const int nm = es_off[s + 1] - es_off[s];
-      if (nm == 0) continue;
-      SampleModes sm;
-      sample_modes(fr, pv.count, gb, lane, sm);
-      float4* dst = es_mode + 3 * (es_off[s] - es_off[s0]);
-      for (int j0 = 0; j0 < nm; j0 += 32) stage_modes(pv, sm, fr.T, nm, j0, lane, dst + 3 * j0);
-    }
-    __syncthreads();
-    const int cbase = es_off[s0];
-    for (int s = s0; s < s1; ++s) {
-      const int m0 = es_off[s] - cbase, m1 = es_off[s + 1] - cbase;
-      if (m1 == m0) continue;
-      const float4 c = es_cam[s - s0];
-      float ya[3], yb[3];
-      xform_f32(Ra, ta, c.x, c.y, c.z, ya);
-      xform_f32(Rb, tb, c.x, c.y, c.z, yb);
-      float qa = __int_as_float(0x7f800000), qb = qa;
-      for (int m = m0; m < m1; ++m) {
-        const float4 q0 = es_mode[3 * m + 0], q1 = es_mode[3 * m + 1], q2 = es_mode[3 * m + 2];
-        qa = fminf(qa, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(ya[0], q0.x), __fsub_rn(ya[1], q0.y),
-                                 __fsub_rn(ya[2], q0.z)));
-        qb = fminf(qb, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(yb[0], q0.x), __fsub_rn(yb[1], q0.y),
-                                 __fsub_rn(yb[2], q0.z)));
-      }
-      Ea = __fadd_rn(Ea, __fsqrt_rn(fmaxf(qa, 0.0f)));
-      Eb = __fadd_rn(Eb, __fsqrt_rn(fmaxf(qb, 0.0f)));
-      evals += static_cast<unsigned long long>(m1 - m0) * ((act_a ? 1u : 0u) + (act_b ? 1u : 0u));
-      sevals += (act_a ? 1u : 0u) + (act_b ? 1u : 0u);
-    }
-    __syncthreads();
-    s0 = s1;
-  }
-  if (ha < n) {
-    const float v = act_a ? Ea : __int_as_float(0x7f800000);
-    if (ea.kb == 0) ea.out[ia] = v;
-    else ea.out[ia * ea.kb + b] = v;
-  }
-  if (hb < n) {
-    const float v = act_b ? Eb : __int_as_float(0x7f800000);
-    if (ea.kb == 0) ea.out[ib] = v;
-    else ea.out[ib * ea.kb + b] = v;
-  }
-  if (work && (act_a || act_b)) {
-    atomicAdd(&work[W_MODE_EVALS], evals);
-    atomicAdd(&work[W_SAMPLE_EVALS], sevals);
-  }
-}
-
-// Re-scoring the <= 64 surviving hypotheses on one sample batch: warp per sample, lane l
-// owns hypotheses l and l + 32, so each predicted mode is loaded once per warp (uniform
-// load) and used for 2 x 32 hypotheses. Per-sample energies e[h][s] go to shared memory;
-// thread h then adds its row in sample order (the batch energy E_b, same bits as a
-// sequential sweep: samples without modes contribute +0).
+// Energies of 64 hypotheses [64 x, 64 x + 64) on one sample batch: warp per sample, lane l
+// owns hypotheses l and l + 32, so each predicted mode is loaded once per warp (coalesced
+// staging) and used for 2 x 32 hypotheses. Per-sample energies e[h][s] go to shared
+// memory; thread h then adds its row in sample order (the batch energy E_b, same bits as a
+// sequential sweep: samples without modes contribute +0). Used for the first scoring of
+// the generated hypotheses (grid.x = n_max / 64, blocks past the generated count exit) and
+// for the re-scoring of the <= 64 survivors.
 constexpr int kSmallHyps = 64;
 
 __global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs fr, PredView pv,
@@ -605,10 +546,15 @@ __global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs f
   __shared__ float s_pose[kSmallHyps][12];
   __shared__ float4 s_modes[8 * 96];  // per-warp staging: 32 modes x 3 float4
   const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
-  const int n = ea.nper ? ea.nper[a] : ea.stride;
-  if (n <= ea.min_n) return;
+  const int n_all = ea.nper ? ea.nper[a] : ea.stride;
+  if (n_all <= ea.min_n) return;
+  const int hbase = blockIdx.x * kSmallHyps;
+  if (hbase >= n_all) return;
+  const int n = min(kSmallHyps, n_all - hbase);
+  const Pose* poses = ea.poses + hbase;
+  float* out = ea.out + hbase * (ea.kb ? ea.kb : 1);
   for (int h = threadIdx.x; h < n; h += blockDim.x) {
-    const Pose& P = ea.poses[static_cast<size_t>(a) * ea.stride + h];
+    const Pose& P = poses[static_cast<size_t>(a) * ea.stride + h];
 #pragma unroll
     for (int i = 0; i < 9; ++i) s_pose[h][i] = static_cast<float>(P.R[i]);
 #pragma unroll
@@ -676,8 +622,8 @@ __global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs f
     float E = 0.0f;
     for (int s = 0; s < eta; ++s) E = __fadd_rn(E, es_e[h * ld + s]);
     const size_t idx = static_cast<size_t>(a) * ea.stride + h;
-    if (ea.kb == 0) ea.out[idx] = E;
-    else ea.out[idx * ea.kb + b] = E;
+    if (ea.kb == 0) out[idx] = E;
+    else out[idx * ea.kb + b] = E;
   }
   if (work && lane == 0 && sevals) {
     atomicAdd(&work[W_MODE_EVALS], evals);
@@ -1519,16 +1465,19 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   SCR_LAUNCH(s, K_SAMPLES,
              (k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, 0, w.samples_cap,
                                                                    w.samples)));
-  const size_t esmem = static_cast<size_t>(kEnergyModeCap) * 3 * sizeof(float4);
+  SCR_LAUNCH(s, K_COMPACT,
+             (k_compact<<<nA, kCompactThreads, 0, s->stream>>>(w.hyp, w.hok, p.n_max, w.hypc, w.hslot, w.hvalid)));
   {
-    EnergyArgs ea{w.hyp, w.hok, p.n_max, nullptr, -1, w.samples, w.samples_cap, p.eta, 0, w.henergy, 0};
-    SCR_LAUNCH(s, K_ENERGY, (k_energy<<<dim3((p.n_max + 511) / 512, 1, nA), 256, esmem, s->stream>>>(ea, fr, pv, wk)));
+    EnergyArgs ea{w.hypc, nullptr, p.n_max, w.hvalid, 0, w.samples, w.samples_cap, p.eta, 0, w.henergy, 0};
+    const size_t smem = static_cast<size_t>(kSmallHyps) * (p.eta + 1) * sizeof(float);
+    SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<dim3((p.n_max + kSmallHyps - 1) / kSmallHyps, 1, nA), 256, smem,
+                                               s->stream>>>(ea, fr, pv, wk)));
   }
   int P = 1;
   while (P < p.n_max) P <<= 1;
   SCR_LAUNCH(s, K_SELECT,
              (k_select<<<nA, 1024, P * sizeof(unsigned long long), s->stream>>>(
-                 w.hyp, w.henergy, w.hok, nullptr, p.n_max, nullptr, p.n_max, p.n_cull, p.n_out, 0, w.cand,
+                 w.hypc, w.henergy, nullptr, w.hslot, p.n_max, w.hvalid, 0, p.n_cull, p.n_out, 0, w.cand,
                  w.cenergy, w.cslot, w.ncand, w.ncull_cap)));
   LmArgs la{0, w.samples_cap, w.ncull_cap, p.n_out, p.use_cov};
   for (int k = 1; k <= K; ++k) {
@@ -1589,8 +1538,6 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
 }  // namespace
 
 scr_status reloc_init() {
-  SCR_CUDA(cudaFuncSetAttribute(k_energy, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kEnergyModeCap * 3 * sizeof(float4))));
   SCR_CUDA(cudaFuncSetAttribute(k_energy_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kSmallHyps * (kEnergySampleCap + 1) * sizeof(float))));
   return SCR_OK;
@@ -1604,6 +1551,9 @@ scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int scap) {
     SCR_TRY(grow(&w.henergy, B * std::max(nmax, 64)));
     SCR_TRY(grow(&w.hok, B * nmax));
     SCR_TRY(grow(&w.hiters, B * nmax));
+    SCR_TRY(grow(&w.hypc, B * nmax));
+    SCR_TRY(grow(&w.hslot, B * nmax));
+    SCR_TRY(grow(&w.hvalid, B));
     w.nmax_cap = nmax;
   }
   if (ncull > w.ncull_cap || scap > w.samples_cap) {

@@ -52,7 +52,7 @@ void prof_flush(scr_scene s) {
 
 const char* const kKernelNames[K_COUNT] = {"k_pack", "k_grid", "k_leaves", "k_hypgen", "k_draw_samples", "k_energy",
                                            "k_select", "k_lm", "k_icp_score", "k_finalize", "k_insert", "k_rqs",
-                                           "k_render"};
+                                           "k_render", "k_compact"};
 scr_status cuda_fail(cudaError_t e, const char* what) {
   g_err = std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what;
   return e == cudaErrorMemoryAllocation ? SCR_E_OOM : SCR_E_CUDA;
@@ -788,7 +788,7 @@ void scr_scene_destroy(scr_scene s) {
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
-                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.gleaf, s->ws.gcamd, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
+                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.gleaf, s->ws.gcamd, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
                   s->ws.ins_rank, s->ws.ins_total};
   for (void* p : ptrs)
     if (p) cudaFree(p);
