@@ -284,6 +284,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    if args.profile_window:
+        torch.cuda.cudart().cudaProfilerStart()
     tw0 = time.time()
     ev0.record(stream)
     for st in range(args.steps):
@@ -293,6 +295,8 @@ def run_ours(args):
     ev1.record(stream)
     torch.cuda.synchronize()
     tw1 = time.time()
+    if args.profile_window:
+        torch.cuda.cudart().cudaProfilerStop()
     if dist is not None:
         dist.barrier()
     clk.mark(tw0, tw1)
@@ -560,6 +564,8 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-batch", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-window", action="store_true",
+                    help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

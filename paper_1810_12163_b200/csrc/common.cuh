@@ -86,6 +86,14 @@ SCR_DEV uint64_t mod_barrett(uint64_t v, uint64_t n, uint64_t m) {
   if (r >= n) r -= n;
   return r;
 }
+// Same remainder for n < 2^30: r = v - q n < 3 n fits 32 bits, so the tail is 32-bit.
+SCR_DEV uint32_t mod_barrett32(uint64_t v, uint32_t n, uint64_t m) {
+  const uint64_t q = __umul64hi(v, m);
+  uint32_t r = static_cast<uint32_t>(v) - static_cast<uint32_t>(q) * n;
+  if (r >= n) r -= n;
+  if (r >= n) r -= n;
+  return r;
+}
 SCR_DEV uint64_t rng_uniform_int_m(Rng& r, uint64_t n, uint64_t m) {
   const uint64_t threshold = mod_barrett(0 - n, n, m);
   for (;;) {

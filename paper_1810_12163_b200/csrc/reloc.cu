@@ -114,6 +114,16 @@ SCR_DEV int mode_from_record(const int* lbase, uint32_t counts, uint4 lv, int pi
   return (lbase[t] + leaf) * kMaxModes + (pick - before);
 }
 
+// Colour check: L-inf distance of the pixel's RGB to the mode's mean
+// colour within the threshold.
+SCR_DEV bool colour_ok(uint32_t col, float4 mc, float thresh) {
+  float linf = 0.0f;
+  linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
+  linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 8) & 255u), mc.y)));
+  linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 16) & 255u), mc.z)));
+  return !(linf > thresh);
+}
+
 // Kabsch (f64 SVD) runs only for triplets that passed every check; out of line so it does
 // not set the register budget of the retry loop.
 __device__ __noinline__ bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return kabsch3(cm, w, *T); }
@@ -190,6 +200,7 @@ __global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, F
   const int f = fr.fidx[a];
   const uint64_t G = static_cast<uint64_t>(fr.gcount[f]);
   const uint64_t mG = G ? barrett_m(G) : 1, tG = G ? mod_barrett(0 - G, G, mG) : 0;
+  const uint32_t G32 = static_cast<uint32_t>(G);
   const uint64_t m3 = 0x5555555555555555ull, t3 = 1;  // floor((2^64-1)/3), 2^64 mod 3
   const bool fast = gp.fast != 0;
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
@@ -223,56 +234,54 @@ __global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, F
     bool push = false;
     GenCand c;
     if (slot >= 0 && it < gp.max_iters) {
-      int4 A0, A1, A2;
-      uint4 L0, L1, L2;
-      int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0, consumed = 0;
-      bool proceed = false;
-      const bool spec = fast && buf.b0 >= tG && buf.b2 >= tG && buf.b4 >= tG;
-      bool slow = !spec;
+      // Fast path: none of the 7 buffered raw values can be rejected (every rejection
+      // threshold is < 2^32, so a non-zero high word always passes; otherwise replay the
+      // attempt exactly below). Pixel indices and the colour-check index are then known up
+      // front; only the mode the colour check needs is resolved before the check.
+      const bool spec = fast && (buf.b0 >> 32) != 0 && (buf.b1 >> 32) != 0 && (buf.b2 >> 32) != 0 &&
+                        (buf.b3 >> 32) != 0 && (buf.b4 >> 32) != 0 && (buf.b5 >> 32) != 0 && (buf.b6 >> 32) != 0;
       if (spec) {
-        g0 = static_cast<int>(mod_barrett(buf.b0, G, mG));
-        g1 = static_cast<int>(mod_barrett(buf.b2, G, mG));
-        g2 = static_cast<int>(mod_barrett(buf.b4, G, mG));
-        A0 = fr.grec[fbase + g0];
-        A1 = fr.grec[fbase + g1];
-        A2 = fr.grec[fbase + g2];
-        L0 = fr.gleaf[fbase + g0];
-        L1 = fr.gleaf[fbase + g1];
-        L2 = fr.gleaf[fbase + g2];
-        const int nm0 = static_cast<uint32_t>(A0.z) >> 24;
-        const int nm1 = static_cast<uint32_t>(A1.z) >> 24;
-        const int nm2 = static_cast<uint32_t>(A2.z) >> 24;
+        const int g0 = static_cast<int>(mod_barrett32(buf.b0, G32, mG));
+        const int g1 = static_cast<int>(mod_barrett32(buf.b2, G32, mG));
+        const int g2 = static_cast<int>(mod_barrett32(buf.b4, G32, mG));
+        const int cc = static_cast<int>(mod_barrett32(buf.b6, 3u, m3));
+        const uint64_t r0 = buf.b1, r1 = buf.b3, r2 = buf.b5;
+        const int gc = cc == 0 ? g0 : (cc == 1 ? g1 : g2);
+        const int4 A0 = fr.grec[fbase + g0], A1 = fr.grec[fbase + g1], A2 = fr.grec[fbase + g2];
+        const uint4 Lc = fr.gleaf[fbase + gc];  // issued together with the records
+        const uint32_t nm0 = static_cast<uint32_t>(A0.z) >> 24, nm1 = static_cast<uint32_t>(A1.z) >> 24,
+                       nm2 = static_cast<uint32_t>(A2.z) >> 24;
         if (nm0 == 0) {
-          consumed = 1;
-        } else if (buf.b1 < s_thr[nm0]) {
-          slow = true;
+          buf.pop(rng);
+        } else if (nm1 == 0) {
+          buf.pop(rng); buf.pop(rng); buf.pop(rng);
+        } else if (nm2 == 0) {
+          buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng);
         } else {
-          p0 = static_cast<int>(mod_barrett(buf.b1, nm0, s_m[nm0]));
-          if (nm1 == 0) {
-            consumed = 3;
-          } else if (buf.b3 < s_thr[nm1]) {
-            slow = true;
-          } else {
-            p1 = static_cast<int>(mod_barrett(buf.b3, nm1, s_m[nm1]));
-            if (nm2 == 0) {
-              consumed = 5;
-            } else if (buf.b5 < s_thr[nm2]) {
-              slow = true;
-            } else {
-              p2 = static_cast<int>(mod_barrett(buf.b5, nm2, s_m[nm2]));
-              if (buf.b6 < t3) {
-                slow = true;
-              } else {
-                cc = static_cast<int>(mod_barrett(buf.b6, 3, m3));
-                consumed = 7;
-                proceed = true;
-              }
-            }
+          buf.fill(rng);
+          const int4 Ac = cc == 0 ? A0 : (cc == 1 ? A1 : A2);
+          const uint64_t rc = cc == 0 ? r0 : (cc == 1 ? r1 : r2);
+          const uint32_t nmc = static_cast<uint32_t>(Ac.z) >> 24;
+          const int pc = static_cast<int>(mod_barrett32(rc, nmc, s_m[nmc]));
+          const int mcc = mode_from_record(s_lbase, static_cast<uint32_t>(Ac.w), Lc, pc);
+          if (colour_ok(static_cast<uint32_t>(Ac.z), pv.col[mcc], gp.colour_thresh)) {
+            const int p0 = static_cast<int>(mod_barrett32(r0, nm0, s_m[nm0]));
+            const int p1 = static_cast<int>(mod_barrett32(r1, nm1, s_m[nm1]));
+            const int p2 = static_cast<int>(mod_barrett32(r2, nm2, s_m[nm2]));
+            push = true;
+            c.slot = slot;
+            c.owner_att = lane | (it << 5);
+            c.g0 = g0; c.g1 = g1; c.g2 = g2;
+            c.m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), fr.gleaf[fbase + g0], p0);
+            c.m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), fr.gleaf[fbase + g1], p1);
+            c.m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), fr.gleaf[fbase + g2], p2);
           }
         }
-      }
-      if (slow) {  // exact sequential replay of the attempt from the buffered stream
-        proceed = false;
+      } else {  // exact sequential replay of the attempt from the buffered stream
+        int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0;
+        int4 A0, A1, A2;
+        uint4 L0, L1, L2;
+        bool proceed = false;
         g0 = static_cast<int>(buf.draw(rng, G, mG, tG));
         A0 = fr.grec[fbase + g0];
         L0 = fr.gleaf[fbase + g0];
@@ -296,40 +305,28 @@ __global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, F
             }
           }
         }
-      } else {
-        switch (consumed) {  // advance the stream by the raw values this attempt used
-          case 1: buf.pop(rng); break;
-          case 3: buf.pop(rng); buf.pop(rng); buf.pop(rng); break;
-          case 5: buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); break;
-          default: buf.fill(rng); break;
+        if (proceed) {
+          int m0, m1, m2;
+          if (fast) {
+            m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), L0, p0);
+            m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), L1, p1);
+            m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), L2, p2);
+          } else {
+            m0 = mode_index(fr, pv.count, fbase + g0, p0);
+            m1 = mode_index(fr, pv.count, fbase + g1, p1);
+            m2 = mode_index(fr, pv.count, fbase + g2, p2);
+          }
+          const uint32_t col = static_cast<uint32_t>(cc == 0 ? A0.z : (cc == 1 ? A1.z : A2.z));
+          if (colour_ok(col, pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)], gp.colour_thresh)) {
+            push = true;
+            c.slot = slot;
+            c.owner_att = lane | (it << 5);
+            c.g0 = g0; c.g1 = g1; c.g2 = g2;
+            c.m0 = m0; c.m1 = m1; c.m2 = m2;
+          }
         }
       }
-      if (proceed) {
-        int m0, m1, m2;
-        if (fast) {
-          m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), L0, p0);
-          m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), L1, p1);
-          m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), L2, p2);
-        } else {
-          m0 = mode_index(fr, pv.count, fbase + g0, p0);
-          m1 = mode_index(fr, pv.count, fbase + g1, p1);
-          m2 = mode_index(fr, pv.count, fbase + g2, p2);
-        }
-        const uint32_t col = static_cast<uint32_t>(cc == 0 ? A0.z : (cc == 1 ? A1.z : A2.z));
-        const float4 mc = pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)];
-        float linf = 0.0f;
-        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>(col & 255u), mc.x)));
-        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 8) & 255u), mc.y)));
-        linf = fmaxf(linf, fabsf(__fsub_rn(static_cast<float>((col >> 16) & 255u), mc.z)));
-        if (!(linf > gp.colour_thresh)) {
-          push = true;
-          c.slot = slot;
-          c.owner_att = lane | (it << 5);
-          c.g0 = g0; c.g1 = g1; c.g2 = g2;
-          c.m0 = m0; c.m1 = m1; c.m2 = m2;
-          s_pend[wid][lane] += 1;
-        }
-      }
+      if (push) s_pend[wid][lane] += 1;
       ++it;
     }
     const unsigned pm = __ballot_sync(0xffffffffu, push);
@@ -1078,7 +1075,15 @@ __device__ __noinline__ bool icp_step(const double* tot, Pose* T) {
   return true;
 }
 
-__global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 3)
+struct IcpPix {  // one live pixel of the association loop in flight
+  int x, y, q;
+  float dl, pw[3];
+};
+
+#ifndef SCR_ICP_MINB
+#define SCR_ICP_MINB 3
+#endif
+__global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, SCR_ICP_MINB)
     k_icp_score(IcpArgs ia, FrameGeom g, FrameRefs fr, const Prim* __restrict__ prims, int nprims,
                 const Pose* __restrict__ cand, const int* __restrict__ ncand, uint2* __restrict__ maps,
                 Pose* __restrict__ out_pose, int* __restrict__ out_conv, double* __restrict__ out_rms,
@@ -1156,55 +1161,75 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
 #pragma unroll
         for (int k = 0; k < 28; ++k) acc[k] = 0.0f;
         int inl = 0, valid = 0;
-        // K9: projective point-to-plane association + normal equations
-        for (int p = lane_id; p < Wl * Hl; p += kIcpLanes) {
-          const int x = p % Wl, y = p / Wl;
-          const float dl = __uint_as_float(tex[(y * fs) * g.W + x * fs].x);
-          if (!depth_valid(dl)) continue;
-          ++valid;
-          const float dcx = s_dcx[x];  // (x - cx) / fx, cached per level (same bits)
-          const float dcy = s_dcy[y];
-          const float pc0 = __fmul_rn(dcx, dl), pc1 = __fmul_rn(dcy, dl);
-          float pw[3], pr[3];
+        // K9: projective point-to-plane association + normal equations. Two pixels of the
+        // lane (p, p + kIcpLanes) are in flight at once: both depth loads, then both model-map
+        // loads, then both accumulated in pixel order (same per-lane order as one at a time).
+        const int npx = Wl * Hl;
+        for (int p = lane_id; p < npx; p += 2 * kIcpLanes) {
+          IcpPix px[2];
 #pragma unroll
-          for (int i = 0; i < 3; ++i)
-            pw[i] = __fmaf_rn(R[3 * i + 0], pc0, __fmaf_rn(R[3 * i + 1], pc1, __fmaf_rn(R[3 * i + 2], dl, t[i])));
+          for (int u = 0; u < 2; ++u) {
+            const int pp = p + u * kIcpLanes;
+            px[u].x = pp % Wl;
+            px[u].y = pp / Wl;
+            px[u].dl = pp < npx ? __uint_as_float(tex[(px[u].y * fs) * g.W + px[u].x * fs].x) : 0.0f;
+          }
 #pragma unroll
-          for (int i = 0; i < 3; ++i)
-            pr[i] = __fmaf_rn(Ri[3 * i + 0], pw[0], __fmaf_rn(Ri[3 * i + 1], pw[1], __fmaf_rn(Ri[3 * i + 2], pw[2], ti[i])));
-          if (!(pr[2] > 0.0f)) continue;
-          const float uf = __fmaf_rn(fxl, __fdiv_rn(pr[0], pr[2]), cxl);
-          const float vf = __fmaf_rn(fyl, __fdiv_rn(pr[1], pr[2]), cyl);
-          if (!(uf > -0.5f && vf > -0.5f && uf < __fsub_rn(static_cast<float>(Wl), 0.5f) &&
-                vf < __fsub_rn(static_cast<float>(Hl), 0.5f)))
-            continue;
-          const int ui = static_cast<int>(floorf(__fadd_rn(uf, 0.5f)));
-          const int vi = static_cast<int>(floorf(__fadd_rn(vf, 0.5f)));
-          if (ui < 0 || vi < 0 || ui >= Wl || vi >= Hl) continue;
-          const uint2 mv = map[vi * Wl + ui];
-          if (mv.y == 0xffffffffu) continue;
-          const float th = __uint_as_float(mv.x);
-          float dm[3], m[3], nn[3];
-          ray_dir_tab(Rr, s_dcx[ui], s_dcy[vi], dm);
+          for (int u = 0; u < 2; ++u) {
+            px[u].q = -1;
+            if (!depth_valid(px[u].dl)) continue;
+            ++valid;
+            const float pc0 = __fmul_rn(s_dcx[px[u].x], px[u].dl), pc1 = __fmul_rn(s_dcy[px[u].y], px[u].dl);
+            float pr[3];
 #pragma unroll
-          for (int i = 0; i < 3; ++i) m[i] = __fmaf_rn(th, dm[i], tr[i]);
-          hit_normal(prims, static_cast<int>(mv.y & 0xffffu), static_cast<int>(mv.y >> 16), m, nn);
-          const float df0 = __fsub_rn(pw[0], m[0]), df1 = __fsub_rn(pw[1], m[1]), df2 = __fsub_rn(pw[2], m[2]);
-          const float dist2 = __fmaf_rn(df0, df0, __fmaf_rn(df1, df1, __fmul_rn(df2, df2)));
-          if (!(dist2 <= 0.01f)) continue;
-          const float r = __fmaf_rn(nn[0], df0, __fmaf_rn(nn[1], df1, __fmul_rn(nn[2], df2)));
-          const float J[6] = {__fmaf_rn(pw[1], nn[2], -__fmul_rn(pw[2], nn[1])),
-                              __fmaf_rn(pw[2], nn[0], -__fmul_rn(pw[0], nn[2])),
-                              __fmaf_rn(pw[0], nn[1], -__fmul_rn(pw[1], nn[0])), nn[0], nn[1], nn[2]};
-          int k = 0;
+            for (int i = 0; i < 3; ++i)
+              px[u].pw[i] = __fmaf_rn(R[3 * i + 0], pc0, __fmaf_rn(R[3 * i + 1], pc1, __fmaf_rn(R[3 * i + 2], px[u].dl, t[i])));
 #pragma unroll
-          for (int aa = 0; aa < 6; ++aa)
+            for (int i = 0; i < 3; ++i)
+              pr[i] = __fmaf_rn(Ri[3 * i + 0], px[u].pw[0],
+                                __fmaf_rn(Ri[3 * i + 1], px[u].pw[1], __fmaf_rn(Ri[3 * i + 2], px[u].pw[2], ti[i])));
+            if (!(pr[2] > 0.0f)) continue;
+            const float uf = __fmaf_rn(fxl, __fdiv_rn(pr[0], pr[2]), cxl);
+            const float vf = __fmaf_rn(fyl, __fdiv_rn(pr[1], pr[2]), cyl);
+            if (!(uf > -0.5f && vf > -0.5f && uf < __fsub_rn(static_cast<float>(Wl), 0.5f) &&
+                  vf < __fsub_rn(static_cast<float>(Hl), 0.5f)))
+              continue;
+            const int ui = static_cast<int>(floorf(__fadd_rn(uf, 0.5f)));
+            const int vi = static_cast<int>(floorf(__fadd_rn(vf, 0.5f)));
+            if (ui < 0 || vi < 0 || ui >= Wl || vi >= Hl) continue;
+            px[u].q = vi * Wl + ui;
+          }
+          uint2 mv[2];
 #pragma unroll
-            for (int bb = aa; bb < 6; ++bb, ++k) acc[k] = __fmaf_rn(J[aa], J[bb], acc[k]);
+          for (int u = 0; u < 2; ++u) mv[u] = px[u].q >= 0 ? map[px[u].q] : make_uint2(0u, 0xffffffffu);
 #pragma unroll
-          for (int aa = 0; aa < 6; ++aa) acc[21 + aa] = __fmaf_rn(J[aa], r, acc[21 + aa]);
-          acc[27] = __fmaf_rn(r, r, acc[27]);
-          ++inl;
+          for (int u = 0; u < 2; ++u) {
+            if (mv[u].y == 0xffffffffu) continue;
+            const float th = __uint_as_float(mv[u].x);
+            const int ui = px[u].q % Wl, vi = px[u].q / Wl;
+            float dm[3], m[3], nn[3];
+            ray_dir_tab(Rr, s_dcx[ui], s_dcy[vi], dm);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) m[i] = __fmaf_rn(th, dm[i], tr[i]);
+            hit_normal(prims, static_cast<int>(mv[u].y & 0xffffu), static_cast<int>(mv[u].y >> 16), m, nn);
+            const float* pw = px[u].pw;
+            const float df0 = __fsub_rn(pw[0], m[0]), df1 = __fsub_rn(pw[1], m[1]), df2 = __fsub_rn(pw[2], m[2]);
+            const float dist2 = __fmaf_rn(df0, df0, __fmaf_rn(df1, df1, __fmul_rn(df2, df2)));
+            if (!(dist2 <= 0.01f)) continue;
+            const float r = __fmaf_rn(nn[0], df0, __fmaf_rn(nn[1], df1, __fmul_rn(nn[2], df2)));
+            const float J[6] = {__fmaf_rn(pw[1], nn[2], -__fmul_rn(pw[2], nn[1])),
+                                __fmaf_rn(pw[2], nn[0], -__fmul_rn(pw[0], nn[2])),
+                                __fmaf_rn(pw[0], nn[1], -__fmul_rn(pw[1], nn[0])), nn[0], nn[1], nn[2]};
+            int k = 0;
+#pragma unroll
+            for (int aa = 0; aa < 6; ++aa)
+#pragma unroll
+              for (int bb = aa; bb < 6; ++bb, ++k) acc[k] = __fmaf_rn(J[aa], J[bb], acc[k]);
+#pragma unroll
+            for (int aa = 0; aa < 6; ++aa) acc[21 + aa] = __fmaf_rn(J[aa], r, acc[21 + aa]);
+            acc[27] = __fmaf_rn(r, r, acc[27]);
+            ++inl;
+          }
         }
         cta_reduce_f32<28>(acc, red, part);
         const int inl_c = cta_isum(inl, ired);

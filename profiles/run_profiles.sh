@@ -1,14 +1,23 @@
 #!/usr/bin/env bash
-# Run on a B200 (gpurun): plain bench, then the ncu launch list of the same command, then one
-# `--set full` capture per top kernel. Outputs land in gpurun_out/ (scratch); summaries are
-# extracted into profiles/ by profiles/summarise.py.
+# On a B200 (gpurun), one ncu tool per call:
+#   bash profiles/run_profiles.sh plain     # bench without ncu (must exit 0 first)
+#   bash profiles/run_profiles.sh launches  # ncu launch list of the timed region
+#   bash profiles/run_profiles.sh full      # ncu --set full of the top kernels, first timed step
+# Outputs land in gpurun_out/; profiles/summarise.py turns them into tracked summaries.
 set -uo pipefail
-CMD="python bench.py --steps 3 --warmup 3 --batch 128 --test-frames 256 --no-cpu"
-$CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || { echo "plain run failed"; exit 1; }
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD \
-    > gpurun_out/ncu_launch.log 2>&1
-for k in k_hypgen k_energy k_icp_score k_energy_small k_leaves; do
-  ncu --set full --clock-control none --import-source on -k regex:"^${k}\$|::${k}\(" -s 2 -c 1 \
-      -o gpurun_out/full_${k} $CMD > gpurun_out/ncu_full_${k}.log 2>&1
-done
-ls -la gpurun_out/
+mkdir -p gpurun_out
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu --profile-window"
+case "${1:-plain}" in
+  plain) $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err; tail -c 600 gpurun_out/prof_plain.json ;;
+  launches)
+    $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || { echo "plain run failed"; exit 1; }
+    ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+    tail -3 gpurun_out/ncu_launch.log ;;
+  full)
+    $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || { echo "plain run failed"; exit 1; }
+    ncu --profile-from-start off --set full --clock-control none --import-source on \
+        -k regex:"k_hypgen|k_icp_score|k_energy_small|k_leaves" -c ${NCU_COUNT:-10} \
+        -o gpurun_out/full_top $CMD > gpurun_out/ncu_full.log 2>&1
+    tail -3 gpurun_out/ncu_full.log ;;
+esac

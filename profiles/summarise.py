@@ -117,9 +117,15 @@ def full(reps: list[str], tag: str) -> str:
           "same bench command exited 0 without ncu. Durations are replayed (cold) single-launch times.", ""]
     js_path = os.path.join(HERE, "ncu_kernels.json")
     js = json.load(open(js_path)) if os.path.exists(js_path) else {"kernels": {}}
-    for rep in reps:
+    picked = {}
+    for rep in reps:  # per kernel, the longest captured launch
         for d in raw_rows(rep):
             name = kernel_short(d.get("Kernel Name", ("?", ""))[0])
+            dur = value(d, "gpu__time_duration.sum") or 0.0
+            if name not in picked or dur > picked[name][0]:
+                picked[name] = (dur, d, rep)
+    for name, (_, d, rep) in sorted(picked.items(), key=lambda x: -x[1][0]):
+        if True:
             md.append(f"## {name}  ({os.path.basename(rep)})")
             md.append("| metric | value |")
             md.append("|---|---|")
