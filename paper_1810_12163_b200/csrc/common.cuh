@@ -566,11 +566,59 @@ SCR_DEV Hit raycast_list(const Prim* prims, const unsigned char* list, int nl, c
   return h;
 }
 
-// Conservative view-frustum test of a primitive's bounding sphere for a camera
-// (R cam->world, origin o) and an image of W x H pixels: false only if no ray of the
-// image can reach the primitive in front of the camera.
-SCR_DEV bool prim_in_view(const Prim& q, const float R[9], const float o[3], float fx, float fy, float cx, float cy,
-                          int W, int H) {
+// Same search over the list entries selected by a bitmask (bit j = list[j]; ascending).
+SCR_DEV Hit raycast_mask(const Prim* prims, const unsigned char* list, uint32_t mask, const float o[3],
+                         const float d[3]) {
+  Hit h;
+  h.t = __int_as_float(0x7f800000);
+  h.prim = -1;
+  h.face = -1;
+  const float inv0 = __fdiv_rn(1.0f, d[0]), inv1 = __fdiv_rn(1.0f, d[1]), inv2 = __fdiv_rn(1.0f, d[2]);
+  const float aa = __fmaf_rn(d[0], d[0], __fmaf_rn(d[1], d[1], __fmul_rn(d[2], d[2])));
+  while (mask) {
+    const int p = list[__ffs(mask) - 1];
+    mask &= mask - 1u;
+    const Prim& q = prims[p];
+    if (q.type == 0) {
+      const float t10 = __fmul_rn(__fsub_rn(q.a[0], o[0]), inv0), t20 = __fmul_rn(__fsub_rn(q.b[0], o[0]), inv0);
+      const float t11 = __fmul_rn(__fsub_rn(q.a[1], o[1]), inv1), t21 = __fmul_rn(__fsub_rn(q.b[1], o[1]), inv1);
+      const float t12 = __fmul_rn(__fsub_rn(q.a[2], o[2]), inv2), t22 = __fmul_rn(__fsub_rn(q.b[2], o[2]), inv2);
+      const float lo0 = fminf(t10, t20), lo1 = fminf(t11, t21), lo2 = fminf(t12, t22);
+      const float hi0 = fmaxf(t10, t20), hi1 = fmaxf(t11, t21), hi2 = fmaxf(t12, t22);
+      const float tn = fmaxf(fmaxf(lo0, lo1), lo2);
+      const float tx = fminf(fminf(hi0, hi1), hi2);
+      if (tn <= tx && tn > 1e-4f && tn < h.t) {
+        const int axis = (tn == lo0) ? 0 : ((tn == lo1) ? 1 : 2);
+        const float da = axis == 0 ? d[0] : (axis == 1 ? d[1] : d[2]);
+        h.t = tn;
+        h.prim = p;
+        h.face = axis * 2 + (da > 0.0f ? 0 : 1);
+      }
+    } else {
+      const float oc0 = __fsub_rn(o[0], q.a[0]), oc1 = __fsub_rn(o[1], q.a[1]), oc2 = __fsub_rn(o[2], q.a[2]);
+      const float bb = __fmaf_rn(oc0, d[0], __fmaf_rn(oc1, d[1], __fmul_rn(oc2, d[2])));
+      const float cc =
+          __fsub_rn(__fmaf_rn(oc0, oc0, __fmaf_rn(oc1, oc1, __fmul_rn(oc2, oc2))), __fmul_rn(q.b[0], q.b[0]));
+      const float disc = __fsub_rn(__fmul_rn(bb, bb), __fmul_rn(aa, cc));
+      if (disc >= 0.0f) {
+        const float t = __fdiv_rn(__fsub_rn(-bb, __fsqrt_rn(disc)), aa);
+        if (t > 1e-4f && t < h.t) {
+          h.t = t;
+          h.prim = p;
+          h.face = 6;
+        }
+      }
+    }
+  }
+  return h;
+}
+
+// Conservative frustum test of a primitive's bounding sphere against the rays of the pixel
+// rectangle [px0, px1] x [py0, py1] (pixel-centre coordinates, already widened by half a
+// pixel) for a camera (R cam->world, origin o): false only if no such ray can reach the
+// primitive in front of the camera.
+SCR_DEV bool prim_in_frustum(const Prim& q, const float R[9], const float o[3], float fx, float fy, float cx,
+                             float cy, float px0, float px1, float py0, float py1) {
   float c[3], r;
   if (q.type == 0) {
     float e2 = 0.0f;
@@ -593,13 +641,17 @@ SCR_DEV bool prim_in_view(const Prim& q, const float R[9], const float o[3], flo
   const float py = R[1] * v[0] + R[4] * v[1] + R[7] * v[2];
   const float pz = R[2] * v[0] + R[5] * v[1] + R[8] * v[2];
   if (pz + r <= 0.0f) return false;
-  const float xl = (-0.5f - cx) / fx, xh = (W - 0.5f - cx) / fx;
-  const float yl = (-0.5f - cy) / fy, yh = (H - 0.5f - cy) / fy;
+  const float xl = (px0 - cx) / fx, xh = (px1 - cx) / fx;
+  const float yl = (py0 - cy) / fy, yh = (py1 - cy) / fy;
   if ((px - xl * pz) < -r * sqrtf(1.0f + xl * xl)) return false;
   if ((xh * pz - px) < -r * sqrtf(1.0f + xh * xh)) return false;
   if ((py - yl * pz) < -r * sqrtf(1.0f + yl * yl)) return false;
   if ((yh * pz - py) < -r * sqrtf(1.0f + yh * yh)) return false;
   return true;
+}
+SCR_DEV bool prim_in_view(const Prim& q, const float R[9], const float o[3], float fx, float fy, float cx, float cy,
+                          int W, int H) {
+  return prim_in_frustum(q, R, o, fx, fy, cx, cy, -0.5f, W - 0.5f, -0.5f, H - 0.5f);
 }
 
 SCR_DEV void hit_normal(const Prim* prims, int prim, int face, const float p[3], float n[3]) {

@@ -73,7 +73,10 @@ SCR_DEV int mode_index(const FrameRefs& fr, const int* pcount, size_t gbase, int
 //    more load and the other two modes' world points are fetched only when it passes;
 //  * uniform draws use exact Barrett reductions (same values as the 64-bit modulo).
 constexpr int kMaxModeUnion = kMaxTrees * kMaxModes;
-constexpr int kGenThreadsPerFrame = 2048;
+#ifndef SCR_GEN_TPF
+#define SCR_GEN_TPF 2048
+#endif
+constexpr int kGenThreadsPerFrame = SCR_GEN_TPF;  // generation threads per frame (slots pulled dynamically)
 
 SCR_DEV uint64_t draw(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
   for (;;) {
@@ -107,10 +110,14 @@ struct RawBuf {  // next 7 raw outputs of the slot's stream
 SCR_DEV int mode_from_record(const int* lbase, uint32_t counts, uint4 lv, int pick) {
   const int c0 = counts & 63u, c1 = (counts >> 6) & 63u, c2 = (counts >> 12) & 63u, c3 = (counts >> 18) & 63u;
   const int e0 = c0, e1 = e0 + c1, e2 = e1 + c2, e3 = e2 + c3;
-  const int t = (pick >= e0) + (pick >= e1) + (pick >= e2) + (pick >= e3);
-  const int before = t == 0 ? 0 : (t == 1 ? e0 : (t == 2 ? e1 : (t == 3 ? e2 : e3)));
-  const uint32_t w = t < 2 ? lv.x : (t < 4 ? lv.y : lv.z);
-  const int leaf = static_cast<int>((w >> (16 * (t & 1))) & 0xffffu);
+  // branch-free: t = trees whose cumulative count is <= pick, before = their modes
+  const int s0 = pick >= e0, s1 = pick >= e1, s2 = pick >= e2, s3 = pick >= e3;
+  const int t = s0 + s1 + s2 + s3;
+  const int before = s0 * c0 + s1 * c1 + s2 * c2 + s3 * c3;
+  uint32_t w = lv.x;
+  w = s1 ? lv.y : w;  // t >= 2
+  w = s3 ? lv.z : w;  // t >= 4
+  const int leaf = static_cast<int>((w >> ((t & 1) << 4)) & 0xffffu);
   return (lbase[t] + leaf) * kMaxModes + (pick - before);
 }
 
@@ -251,31 +258,37 @@ __global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, F
         const uint4 Lc = fr.gleaf[fbase + gc];  // issued together with the records
         const uint32_t nm0 = static_cast<uint32_t>(A0.z) >> 24, nm1 = static_cast<uint32_t>(A1.z) >> 24,
                        nm2 = static_cast<uint32_t>(A2.z) >> 24;
-        if (nm0 == 0) {
-          buf.pop(rng);
-        } else if (nm1 == 0) {
-          buf.pop(rng); buf.pop(rng); buf.pop(rng);
-        } else if (nm2 == 0) {
-          buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng);
-        } else {
-          buf.fill(rng);
-          const int4 Ac = cc == 0 ? A0 : (cc == 1 ? A1 : A2);
+        const bool full = nm0 != 0 && nm1 != 0 && nm2 != 0;  // all 7 raw values consumed
+        // the colour check's mode is resolved and its colour load issued before the stream
+        // refill, so the load's latency hides behind the xoshiro work
+        const int4 Ac = cc == 0 ? A0 : (cc == 1 ? A1 : A2);
+        float4 mcol = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (full) {
           const uint64_t rc = cc == 0 ? r0 : (cc == 1 ? r1 : r2);
           const uint32_t nmc = static_cast<uint32_t>(Ac.z) >> 24;
           const int pc = static_cast<int>(mod_barrett32(rc, nmc, s_m[nmc]));
-          const int mcc = mode_from_record(s_lbase, static_cast<uint32_t>(Ac.w), Lc, pc);
-          if (colour_ok(static_cast<uint32_t>(Ac.z), pv.col[mcc], gp.colour_thresh)) {
-            const int p0 = static_cast<int>(mod_barrett32(r0, nm0, s_m[nm0]));
-            const int p1 = static_cast<int>(mod_barrett32(r1, nm1, s_m[nm1]));
-            const int p2 = static_cast<int>(mod_barrett32(r2, nm2, s_m[nm2]));
-            push = true;
-            c.slot = slot;
-            c.owner_att = lane | (it << 5);
-            c.g0 = g0; c.g1 = g1; c.g2 = g2;
-            c.m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), fr.gleaf[fbase + g0], p0);
-            c.m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), fr.gleaf[fbase + g1], p1);
-            c.m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), fr.gleaf[fbase + g2], p2);
-          }
+          mcol = pv.col[mode_from_record(s_lbase, static_cast<uint32_t>(Ac.w), Lc, pc)];
+        }
+        if (full) {
+          buf.fill(rng);
+        } else if (nm0 == 0) {
+          buf.pop(rng);
+        } else if (nm1 == 0) {
+          buf.pop(rng); buf.pop(rng); buf.pop(rng);
+        } else {
+          buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng);
+        }
+        if (full && colour_ok(static_cast<uint32_t>(Ac.z), mcol, gp.colour_thresh)) {
+          const int p0 = static_cast<int>(mod_barrett32(r0, nm0, s_m[nm0]));
+          const int p1 = static_cast<int>(mod_barrett32(r1, nm1, s_m[nm1]));
+          const int p2 = static_cast<int>(mod_barrett32(r2, nm2, s_m[nm2]));
+          push = true;
+          c.slot = slot;
+          c.owner_att = lane | (it << 5);
+          c.g0 = g0; c.g1 = g1; c.g2 = g2;
+          c.m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), fr.gleaf[fbase + g0], p0);
+          c.m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), fr.gleaf[fbase + g1], p1);
+          c.m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), fr.gleaf[fbase + g2], p2);
         }
       } else {  // exact sequential replay of the attempt from the buffered stream
         int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0;
@@ -1037,6 +1050,32 @@ __device__ __forceinline__ void build_plist(const Prim* prims, int nprims, const
   __syncthreads();
 }
 
+// Per-tile visibility masks: the image is cut into 32 x 8 pixel tiles (a warp's 32
+// consecutive pixels of a row always fall in one tile: every level's width is a multiple
+// of 32), and bit j of a tile's mask says whether list entry j can be hit by any ray of
+// the tile (conservative frustum test). The ray casts then test only those primitives,
+// still in ascending order, so hits are identical to testing the whole list.
+constexpr int kTileW = 32, kTileH = 8;
+constexpr int kMaxTiles = (kMaxImageW / kTileW) * (kMaxImageH / kTileH);
+
+__device__ __forceinline__ void build_tile_masks(const Prim* prims, const unsigned char* list, int nl,
+                                                 const float R[9], const float o[3], float fx, float fy, float cx,
+                                                 float cy, int W, int H, uint32_t* masks) {
+  const int tw = (W + kTileW - 1) / kTileW, th = (H + kTileH - 1) / kTileH;
+  for (int t = threadIdx.x; t < tw * th; t += blockDim.x) {
+    const int tx = t % tw, ty = t / tw;
+    const float x0 = static_cast<float>(tx * kTileW) - 0.5f;
+    const float x1 = static_cast<float>(min(W, tx * kTileW + kTileW) - 1) + 0.5f;
+    const float y0 = static_cast<float>(ty * kTileH) - 0.5f;
+    const float y1 = static_cast<float>(min(H, ty * kTileH + kTileH) - 1) + 0.5f;
+    uint32_t m = 0;
+    for (int j = 0; j < nl; ++j)
+      if (prim_in_frustum(prims[list[j]], R, o, fx, fy, cx, cy, x0, x1, y0, y1)) m |= 1u << j;
+    masks[t] = m;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ int cta_isum(int v, int* ired) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   v = warp_isum(v);
@@ -1076,9 +1115,25 @@ __device__ __noinline__ bool icp_step(const double* tot, Pose* T) {
 }
 
 struct IcpPix {  // one live pixel of the association loop in flight
-  int x, y, q;
+  int x, y, q, ui, vi;
   float dl, pw[3];
 };
+
+// p -> (p mod W, p div W) for 0 <= p < 2^24 without an integer division: the float
+// quotient is within one of the true one, fixed by one correction step.
+SCR_DEV void divmod_w(int p, int W, float invW, int& x, int& y) {
+  int q = __float2int_rz(__fmul_rn(__int2float_rn(p), invW));
+  int r = p - q * W;
+  if (r < 0) {
+    --q;
+    r += W;
+  } else if (r >= W) {
+    ++q;
+    r -= W;
+  }
+  x = r;
+  y = q;
+}
 
 #ifndef SCR_ICP_MINB
 #define SCR_ICP_MINB 3
@@ -1089,14 +1144,17 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
                 Pose* __restrict__ out_pose, int* __restrict__ out_conv, double* __restrict__ out_rms,
                 double* __restrict__ out_inl, double* __restrict__ out_score, unsigned long long* __restrict__ work) {
   __shared__ double red[kIcpThreads / 32][32];
-  __shared__ double part[32];   // this CTA's f64 partials (read by CTA 0 over DSMEM)
-  __shared__ int ipart[4];
+  __shared__ double part2[2][32];  // this CTA's f64 partials, double-buffered by iteration parity
+  __shared__ int ipart2[2][4];     // (read by every CTA of the cluster over DSMEM)
+  double* part = part2[0];
+  int* ipart = ipart2[0];
   __shared__ int ired[kIcpThreads / 32];
   __shared__ Pose Ts;           // current estimate (authoritative copy in CTA 0)
   __shared__ int stop_level;
   __shared__ unsigned char s_plist[256];
   __shared__ int s_pn;
   __shared__ float s_dcx[kMaxImageW], s_dcy[kMaxImageH];
+  __shared__ uint32_t s_tmask[kMaxTiles];
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int lane_id = rank * kIcpThreads + threadIdx.x;
@@ -1113,6 +1171,9 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
   int last_inl = 0, last_valid = 0;
   double last_r2 = 0.0;
   bool have_stats = false;
+  __shared__ int lstat[2];
+  __shared__ double lstat_r2;
+  int pbuf = 0;
   if (ia.do_icp) {
     for (int level = 2; level >= 0; --level) {
       const int fs = 1 << level;
@@ -1138,16 +1199,30 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       fill_ray_tables(Wl, Hl, fxl, fyl, cxl, cyl, s_dcx, s_dcy);  // synced by build_plist
       build_plist(prims, nprims, Rr, tr, fxl, fyl, cxl, cyl, Wl, Hl, s_plist, &s_pn);
       const int npl = s_pn;
-      if (work && rank == 0 && threadIdx.x == 0)
-        atomicAdd(&work[W_RAY_PRIMS], static_cast<unsigned long long>(Wl * Hl) * npl);
+      const bool tiled = npl <= 32 && (Wl % kTileW) == 0;
+      if (tiled) build_tile_masks(prims, s_plist, npl, Rr, tr, fxl, fyl, cxl, cyl, Wl, Hl, s_tmask);
+      unsigned long long tests = 0;
+      const int twl = Wl / kTileW;
+      const float invWl = __fdiv_rn(1.0f, static_cast<float>(Wl));
       for (int p = lane_id; p < Wl * Hl; p += kIcpLanes) {
+        int x, y;
+        divmod_w(p, Wl, invWl, x, y);
         float d[3];
-        ray_dir_tab(Rr, s_dcx[p % Wl], s_dcy[p / Wl], d);
-        const Hit h = raycast_list(prims, s_plist, npl, tr, d);
+        ray_dir_tab(Rr, s_dcx[x], s_dcy[y], d);
+        Hit h;
+        if (tiled) {
+          const uint32_t m = s_tmask[(y / kTileH) * twl + x / kTileW];
+          tests += __popc(m);
+          h = raycast_mask(prims, s_plist, m, tr, d);
+        } else {
+          tests += npl;
+          h = raycast_list(prims, s_plist, npl, tr, d);
+        }
         uint2 v = make_uint2(0u, 0xffffffffu);
         if (h.prim >= 0 && h.t <= kRenderMaxDepth) v = make_uint2(__float_as_uint(h.t), h.prim | (h.face << 16));
         map[p] = v;
       }
+      if (work) atomicAdd(&work[W_RAY_PRIMS], tests);
       cluster.sync();  // map complete and visible to the whole cluster
       const int iters = level == 2 ? 10 : (level == 1 ? 5 : 4);
       for (int it = 0; it < iters; ++it) {
@@ -1170,8 +1245,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int pp = p + u * kIcpLanes;
-            px[u].x = pp % Wl;
-            px[u].y = pp / Wl;
+            divmod_w(pp, Wl, invWl, px[u].x, px[u].y);
             px[u].dl = pp < npx ? __uint_as_float(tex[(px[u].y * fs) * g.W + px[u].x * fs].x) : 0.0f;
           }
 #pragma unroll
@@ -1198,6 +1272,8 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
             const int vi = static_cast<int>(floorf(__fadd_rn(vf, 0.5f)));
             if (ui < 0 || vi < 0 || ui >= Wl || vi >= Hl) continue;
             px[u].q = vi * Wl + ui;
+            px[u].ui = ui;
+            px[u].vi = vi;
           }
           uint2 mv[2];
 #pragma unroll
@@ -1206,7 +1282,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
           for (int u = 0; u < 2; ++u) {
             if (mv[u].y == 0xffffffffu) continue;
             const float th = __uint_as_float(mv[u].x);
-            const int ui = px[u].q % Wl, vi = px[u].q / Wl;
+            const int ui = px[u].ui, vi = px[u].vi;
             float dm[3], m[3], nn[3];
             ray_dir_tab(Rr, s_dcx[ui], s_dcy[vi], dm);
 #pragma unroll
@@ -1231,54 +1307,52 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
             ++inl;
           }
         }
-        cta_reduce_f32<28>(acc, red, part);
+        // One cluster barrier per iteration: every CTA reads the 8 partials over DSMEM, sums
+        // them in CTA order and takes the (identical, deterministic) Gauss-Newton step
+        // itself. Partials alternate between two buffers, so a CTA that runs ahead into the
+        // next iteration never overwrites what a slower CTA is still reading.
+        double* pb = part2[pbuf];
+        int* ib = ipart2[pbuf];
+        cta_reduce_f32<28>(acc, red, pb);
         const int inl_c = cta_isum(inl, ired);
         const int valid_c = cta_isum(valid, ired);
         if (threadIdx.x == 0) {
-          ipart[0] = inl_c;
-          ipart[1] = valid_c;
+          ib[0] = inl_c;
+          ib[1] = valid_c;
         }
-        cluster.sync();  // [A] all CTA partials written
-        if (rank == 0) {
-          if (threadIdx.x < 28) {
-            double tot = part[threadIdx.x];
-            for (int r = 1; r < kIcpCtas; ++r) tot = tot + cluster.map_shared_rank(part, r)[threadIdx.x];
-            red[0][threadIdx.x] = tot;
-          }
-          if (threadIdx.x == 32) {
-            int inl_t = 0, valid_t = 0;
-            for (int r = 0; r < kIcpCtas; ++r) {
-              inl_t += cluster.map_shared_rank(ipart, r)[0];
-              valid_t += cluster.map_shared_rank(ipart, r)[1];
-            }
-            ired[0] = inl_t;
-            ired[1] = valid_t;
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            const double* tot = red[0];
-            const int inl_t = ired[0];
-            if (work) atomicAdd(&work[W_ICP_TERMS], static_cast<unsigned long long>(ired[1]));
-            if (level == 0) {
-              ipart[2] = inl_t;
-              ipart[3] = ired[1];
-              part[28] = tot[27];
-            }
-            stop_level = (inl_t < 6 || !icp_step(tot, &Ts)) ? 1 : 0;
-          }
+        cluster.sync();  // all CTA partials of this iteration written
+        if (threadIdx.x < 28) {
+          double tot = cluster.map_shared_rank(pb, 0)[threadIdx.x];
+          for (int r = 1; r < kIcpCtas; ++r) tot = tot + cluster.map_shared_rank(pb, r)[threadIdx.x];
+          red[0][threadIdx.x] = tot;
         }
-        cluster.sync();  // [B] pose / stop flag published by CTA 0
-        if (rank != 0) {
-          if (threadIdx.x == 0) {
-            Ts = *cluster.map_shared_rank(&Ts, 0);
-            stop_level = *cluster.map_shared_rank(&stop_level, 0);
+        if (threadIdx.x == 32) {
+          int inl_t = 0, valid_t = 0;
+          for (int r = 0; r < kIcpCtas; ++r) {
+            inl_t += cluster.map_shared_rank(ib, r)[0];
+            valid_t += cluster.map_shared_rank(ib, r)[1];
           }
-          __syncthreads();
+          ired[0] = inl_t;
+          ired[1] = valid_t;
         }
-        if (level == 0 && rank == 0) {
-          last_inl = ipart[2];
-          last_valid = ipart[3];
-          last_r2 = part[28];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const double* tot = red[0];
+          const int inl_t = ired[0];
+          if (work && rank == 0) atomicAdd(&work[W_ICP_TERMS], static_cast<unsigned long long>(ired[1]));
+          if (level == 0) {
+            lstat[0] = inl_t;
+            lstat[1] = ired[1];
+            lstat_r2 = tot[27];
+          }
+          stop_level = (inl_t < 6 || !icp_step(tot, &Ts)) ? 1 : 0;
+        }
+        __syncthreads();
+        pbuf ^= 1;
+        if (level == 0) {
+          last_inl = lstat[0];
+          last_valid = lstat[1];
+          last_r2 = lstat_r2;
           have_stats = true;
         }
         if (stop_level) break;
@@ -1289,23 +1363,17 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
   const Pose Tf = Ts;
   int conv = 1;
   double rms = 0.0, inlf = 0.0;
-  if (ia.do_icp) {  // only CTA 0 holds the statistics; broadcast the decision
-    if (rank == 0) {
-      if (have_stats && last_valid > 0 && last_inl > 0) {
-        inlf = static_cast<double>(last_inl) / static_cast<double>(last_valid);
-        rms = sqrt(last_r2 / static_cast<double>(last_inl));
-        conv = (inlf >= 0.5 && rms <= 0.02) ? 1 : 0;
-      } else {
-        inlf = 0.0;
-        rms = __longlong_as_double(0x7ff0000000000000ll);
-        conv = 0;
-      }
-      if (threadIdx.x == 0) stop_level = conv;
+  if (ia.do_icp) {  // every CTA holds the same statistics
+    if (have_stats && last_valid > 0 && last_inl > 0) {
+      inlf = static_cast<double>(last_inl) / static_cast<double>(last_valid);
+      rms = sqrt(last_r2 / static_cast<double>(last_inl));
+      conv = (inlf >= 0.5 && rms <= 0.02) ? 1 : 0;
+    } else {
+      inlf = 0.0;
+      rms = __longlong_as_double(0x7ff0000000000000ll);
+      conv = 0;
     }
-    cluster.sync();
-    if (rank != 0 && threadIdx.x == 0) stop_level = *cluster.map_shared_rank(&stop_level, 0);
-    cluster.sync();  // CTA 0 must not exit while the others still read its shared memory
-    conv = stop_level;
+    cluster.sync();  // no CTA exits or reuses its partials while another may still read them
   }
   double score = __longlong_as_double(0x7ff0000000000000ll);
   if (conv) {
@@ -1322,12 +1390,25 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
     fill_ray_tables(g.W, g.H, g.fx, g.fy, g.cx, g.cy, s_dcx, s_dcy);
     build_plist(prims, nprims, R, t, g.fx, g.fy, g.cx, g.cy, g.W, g.H, s_plist, &s_pn);
     const int npl = s_pn;
-    if (work && rank == 0 && threadIdx.x == 0)
-      atomicAdd(&work[W_RAY_PRIMS], static_cast<unsigned long long>(g.W * g.H) * npl);
+    const bool tiled = npl <= 32 && (g.W % kTileW) == 0;
+    if (tiled) build_tile_masks(prims, s_plist, npl, R, t, g.fx, g.fy, g.cx, g.cy, g.W, g.H, s_tmask);
+    unsigned long long tests = 0;
+    const int tw0 = g.W / kTileW;
+    const float invW = __fdiv_rn(1.0f, static_cast<float>(g.W));
     for (int p = lane_id; p < g.W * g.H; p += kIcpLanes) {
+      int x, y;
+      divmod_w(p, g.W, invW, x, y);
       float d[3];
-      ray_dir_tab(R, s_dcx[p % g.W], s_dcy[p / g.W], d);
-      const Hit h = raycast_list(prims, s_plist, npl, t, d);
+      ray_dir_tab(R, s_dcx[x], s_dcy[y], d);
+      Hit h;
+      if (tiled) {
+        const uint32_t m = s_tmask[(y / kTileH) * tw0 + x / kTileW];
+        tests += __popc(m);
+        h = raycast_mask(prims, s_plist, m, t, d);
+      } else {
+        tests += npl;
+        h = raycast_list(prims, s_plist, npl, t, d);
+      }
       if (h.prim < 0 || !(h.t <= kRenderMaxDepth) || !depth_valid(h.t)) continue;
       ++synth;
       const float dl = __uint_as_float(tex[p].x);
@@ -1335,6 +1416,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       ++mutual;
       sum = __fadd_rn(sum, fabsf(__fsub_rn(dl, h.t)));
     }
+    if (work) atomicAdd(&work[W_RAY_PRIMS], tests);
     cta_reduce_f32<1>(&sum, red, part);
     const int mutual_c = cta_isum(mutual, ired);
     const int synth_c = cta_isum(synth, ired);
