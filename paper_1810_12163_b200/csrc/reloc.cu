@@ -641,6 +641,101 @@ __global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs f
   }
 }
 
+// Re-scoring of at most 2 L candidates (L < 32 lanes per sample): a warp works on 32 / L
+// samples at once, lane j of a sample's group owning candidates j and j + L, so the warp's
+// instruction stream is shared by 32 / L samples instead of one. Each lane walks its
+// sample's predicted modes tree by tree with direct loads (the group's lanes read the same
+// addresses); the per-sample minimum does not depend on the mode order, and the batch sum
+// is taken in sample order exactly as in k_energy_small.
+template <int L>
+__global__ void __launch_bounds__(256) k_energy_grouped(EnergyArgs ea, FrameRefs fr, PredView pv,
+                                                        unsigned long long* __restrict__ work) {
+  constexpr int G = 32 / L;
+  extern __shared__ float es_e[];  // [2 L][eta + 1]
+  __shared__ float s_pose[2 * L][12];
+  const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
+  const int n = ea.nper ? ea.nper[a] : ea.stride;
+  if (n <= ea.min_n) return;
+  for (int h = threadIdx.x; h < n && h < 2 * L; h += blockDim.x) {
+    const Pose& P = ea.poses[static_cast<size_t>(a) * ea.stride + h];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) s_pose[h][i] = static_cast<float>(P.R[i]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s_pose[h][9 + i] = static_cast<float>(P.t[i]);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int grp = lane / L, j = lane % L;
+  const int hA = j, hB = j + L;
+  const bool vA = hA < n, vB = hB < n;
+  float RA[9], tA[3], RB[9], tB[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    RA[i] = vA ? s_pose[hA][i] : 0.0f;
+    RB[i] = vB ? s_pose[hB][i] : 0.0f;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    tA[i] = vA ? s_pose[hA][9 + i] : 0.0f;
+    tB[i] = vB ? s_pose[hB][9 + i] : 0.0f;
+  }
+  const int f = fr.fidx[a];
+  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  const int* smp = ea.samples + static_cast<size_t>(a) * ea.scap + static_cast<size_t>(b) * ea.eta;
+  const int eta = ea.eta, ld = eta + 1;
+  unsigned long long evals = 0, sevals = 0;
+  for (int s = wid * G + grp; s < eta; s += nw * G) {
+    const size_t gb = fbase + smp[s];
+    const int nm = fr.gnm[gb];
+    float eA = 0.0f, eB = 0.0f;
+    if (nm > 0) {
+      int slot[kMaxTrees], cnt[kMaxTrees];
+#pragma unroll
+      for (int t = 0; t < kMaxTrees; ++t) slot[t] = t < fr.T ? fr.gslot[gb * fr.T + t] : 0;
+#pragma unroll
+      for (int t = 0; t < kMaxTrees; ++t) cnt[t] = t < fr.T ? pv.count[slot[t]] : 0;
+      const float4 c = fr.gcam[gb];
+      float yA[3], yB[3];
+      xform_f32(RA, tA, c.x, c.y, c.z, yA);
+      xform_f32(RB, tB, c.x, c.y, c.z, yB);
+      float mA = __int_as_float(0x7f800000), mB = mA;
+#pragma unroll
+      for (int t = 0; t < kMaxTrees; ++t) {
+        const ModeGeom* mg = pv.geom + static_cast<size_t>(slot[t]) * kMaxModes;
+#pragma unroll 2
+        for (int q = 0; q < cnt[t]; ++q) {
+          const float4 q0 = mg[q].q0, q1 = mg[q].q1, q2 = mg[q].q2;
+          mA = fminf(mA, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(yA[0], q0.x), __fsub_rn(yA[1], q0.y),
+                                   __fsub_rn(yA[2], q0.z)));
+          mB = fminf(mB, quad_icov(q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, __fsub_rn(yB[0], q0.x), __fsub_rn(yB[1], q0.y),
+                                   __fsub_rn(yB[2], q0.z)));
+        }
+      }
+      eA = __fsqrt_rn(fmaxf(mA, 0.0f));
+      eB = __fsqrt_rn(fmaxf(mB, 0.0f));
+      if (j == 0) {
+        evals += static_cast<unsigned long long>(nm) * static_cast<unsigned long long>(min(n, 2 * L));
+        sevals += static_cast<unsigned long long>(min(n, 2 * L));
+      }
+    }
+    if (vA) es_e[hA * ld + s] = eA;
+    if (vB) es_e[hB * ld + s] = eB;
+  }
+  __syncthreads();
+  if (threadIdx.x < n && threadIdx.x < 2 * L) {
+    const int h = threadIdx.x;
+    float E = 0.0f;
+    for (int q = 0; q < eta; ++q) E = __fadd_rn(E, es_e[h * ld + q]);
+    const size_t idx = static_cast<size_t>(a) * ea.stride + h;
+    if (ea.kb == 0) ea.out[idx] = E;
+    else ea.out[idx * ea.kb + b] = E;
+  }
+  if (work && sevals) {
+    atomicAdd(&work[W_MODE_EVALS], evals);
+    atomicAdd(&work[W_SAMPLE_EVALS], sevals);
+  }
+}
+
 // E(I_k) = base + E_b0 + ... + E_b1 in batch order (base = E(I_{k-1}) when poses did not move).
 __global__ void k_energy_sum(const int* __restrict__ ncand, int n_out, int stride, int kb, int b0, int b1,
                              const float* __restrict__ base, const float* __restrict__ part, float* __restrict__ out) {
@@ -1609,9 +1704,26 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
       const int b0 = p.pose_update ? 0 : k;
       EnergyArgs ea{w.cand, nullptr, w.ncull_cap, w.ncand, p.n_out, w.samples, w.samples_cap, p.eta, b0, w.epart,
                     kEnergyBatches};
-      const size_t smem_small = static_cast<size_t>(kSmallHyps) * (p.eta + 1) * sizeof(float);
-      SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<dim3(1, k - b0 + 1, nA), 256, smem_small, s->stream>>>(ea, fr, pv,
-                                                                                                        wk)));
+      // at most ceil(n_cull / 2^(k-1)) candidates take part in step k
+      const int nb = (p.n_cull + (1 << (k - 1)) - 1) >> (k - 1);
+      int L = 1;
+      while (2 * L < nb) L <<= 1;
+      const dim3 grid(1, k - b0 + 1, nA);
+      const size_t smem_g = static_cast<size_t>(2 * L) * (p.eta + 1) * sizeof(float);
+      if (L >= 32) {
+        const size_t smem_small = static_cast<size_t>(kSmallHyps) * (p.eta + 1) * sizeof(float);
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<grid, 256, smem_small, s->stream>>>(ea, fr, pv, wk)));
+      } else if (L == 16) {
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<16><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+      } else if (L == 8) {
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<8><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+      } else if (L == 4) {
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<4><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+      } else if (L == 2) {
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<2><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+      } else {
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<1><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+      }
       SCR_LAUNCH(s, K_ENERGY, (k_energy_sum<<<nA, 64, 0, s->stream>>>(w.ncand, p.n_out, w.ncull_cap, kEnergyBatches,
                                                                       b0, k, p.pose_update ? nullptr : w.cenergy,
                                                                       w.epart, w.henergy)));
@@ -1647,6 +1759,8 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
 scr_status reloc_init() {
   SCR_CUDA(cudaFuncSetAttribute(k_energy_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kSmallHyps * (kEnergySampleCap + 1) * sizeof(float))));
+  SCR_CUDA(cudaFuncSetAttribute(k_energy_grouped<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(32 * (kEnergySampleCap + 1) * sizeof(float))));
   return SCR_OK;
 }
 

@@ -11,7 +11,7 @@ case "${1:-plain}" in
   plain) $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err; tail -c 600 gpurun_out/prof_plain.json ;;
   launches)
     $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || { echo "plain run failed"; exit 1; }
-    ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv \
         --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
     tail -3 gpurun_out/ncu_launch.log ;;
   full)
