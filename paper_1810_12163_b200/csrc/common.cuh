@@ -613,40 +613,44 @@ SCR_DEV Hit raycast_mask(const Prim* prims, const unsigned char* list, uint32_t 
   return h;
 }
 
-// Conservative frustum test of a primitive's bounding sphere against the rays of the pixel
-// rectangle [px0, px1] x [py0, py1] (pixel-centre coordinates, already widened by half a
-// pixel) for a camera (R cam->world, origin o): false only if no such ray can reach the
-// primitive in front of the camera.
+// Conservative frustum test of a primitive against the rays of the pixel rectangle
+// [px0, px1] x [py0, py1] (pixel-centre coordinates, already widened by half a pixel) for a
+// camera (R cam->world, origin o): false only if no such ray can reach the primitive in
+// front of the camera. Each side plane passes through the camera centre; a box is outside
+// a plane when its support along the plane normal (centre distance + sum |n_i| e_i) stays
+// below zero, a sphere when centre distance + r |n| does. Support terms carry a 1 % + 2 cm
+// margin, far above the float rounding of the test.
 SCR_DEV bool prim_in_frustum(const Prim& q, const float R[9], const float o[3], float fx, float fy, float cx,
                              float cy, float px0, float px1, float py0, float py1) {
-  float c[3], r;
-  if (q.type == 0) {
-    float e2 = 0.0f;
+  float c[3], e[3] = {0.0f, 0.0f, 0.0f}, r = 0.0f;
+  const bool box = q.type == 0;
+  if (box) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       c[i] = 0.5f * (q.a[i] + q.b[i]);
-      const float e = 0.5f * (q.b[i] - q.a[i]);
-      e2 += e * e;
+      e[i] = fabsf(0.5f * (q.b[i] - q.a[i]));
     }
-    r = sqrtf(e2);
   } else {
     c[0] = q.a[0];
     c[1] = q.a[1];
     c[2] = q.a[2];
     r = q.b[0];
   }
-  r = r * 1.01f + 0.02f;  // margin for rounding
   const float v[3] = {c[0] - o[0], c[1] - o[1], c[2] - o[2]};
-  const float px = R[0] * v[0] + R[3] * v[1] + R[6] * v[2];
-  const float py = R[1] * v[0] + R[4] * v[1] + R[7] * v[2];
-  const float pz = R[2] * v[0] + R[5] * v[1] + R[8] * v[2];
-  if (pz + r <= 0.0f) return false;
   const float xl = (px0 - cx) / fx, xh = (px1 - cx) / fx;
   const float yl = (py0 - cy) / fy, yh = (py1 - cy) / fy;
-  if ((px - xl * pz) < -r * sqrtf(1.0f + xl * xl)) return false;
-  if ((xh * pz - px) < -r * sqrtf(1.0f + xh * xh)) return false;
-  if ((py - yl * pz) < -r * sqrtf(1.0f + yl * yl)) return false;
-  if ((yh * pz - py) < -r * sqrtf(1.0f + yh * yh)) return false;
+  // camera-frame inward normals: near (0,0,1), left (1,0,-xl), right (-1,0,xh), top (0,1,-yl), bottom (0,-1,yh)
+  const float nc[5][3] = {{0.0f, 0.0f, 1.0f}, {1.0f, 0.0f, -xl}, {-1.0f, 0.0f, xh}, {0.0f, 1.0f, -yl}, {0.0f, -1.0f, yh}};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    float nw[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) nw[i] = R[3 * i + 0] * nc[k][0] + R[3 * i + 1] * nc[k][1] + R[3 * i + 2] * nc[k][2];
+    const float nlen = sqrtf(nc[k][0] * nc[k][0] + nc[k][1] * nc[k][1] + nc[k][2] * nc[k][2]);
+    const float dist = nw[0] * v[0] + nw[1] * v[1] + nw[2] * v[2];
+    const float sup = box ? (fabsf(nw[0]) * e[0] + fabsf(nw[1]) * e[1] + fabsf(nw[2]) * e[2]) : r * nlen;
+    if (dist + sup * 1.01f + 0.02f * nlen <= 0.0f) return false;
+  }
   return true;
 }
 SCR_DEV bool prim_in_view(const Prim& q, const float R[9], const float o[3], float fx, float fy, float cx, float cy,

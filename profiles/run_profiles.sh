@@ -17,7 +17,7 @@ case "${1:-plain}" in
   full)
     $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || { echo "plain run failed"; exit 1; }
     ncu --profile-from-start off --set full --clock-control none --import-source on \
-        -k regex:"k_hypgen|k_icp_score|k_energy_small|k_leaves" -c ${NCU_COUNT:-10} \
+        -k regex:"${NCU_REGEX:-k_hypgen|k_icp_score|k_energy_small|k_leaves}" -c ${NCU_COUNT:-10} \
         -o gpurun_out/full_top $CMD > gpurun_out/ncu_full.log 2>&1
     tail -3 gpurun_out/ncu_full.log ;;
 esac
