@@ -3,6 +3,8 @@
 // Build: g++ -std=c++17 -I include examples/cpp_drop_in.cpp -L paper_1810_12163_b200/lib \
 //          -lscreloc_gpu -Wl,-rpath,paper_1810_12163_b200/lib -o cpp_drop_in
 #include <cmath>
+#include <cstring>
+#include <thread>
 #include <cstdio>
 #include <vector>
 
@@ -58,6 +60,17 @@ int main() {
     return 2;
   } catch (const sg::UnreliablePose&) {
     std::printf("UnreliablePose raised as in the reference\n");
+  }
+  {  // a second relocalisation lane on another thread gives the same poses
+    sg::Relocaliser lane = reloc.fork_lane(n_test);
+    std::vector<sg::RelocalisationResult> lane_res;
+    std::thread th([&] { lane_res = lane.run_cascade_batch(sg::CascadeConfig::paper_three_stage(), frames, seeds); });
+    th.join();
+    for (int i = 0; i < n_test; ++i)
+      if (static_cast<bool>(lane_res[i].final_pose) != static_cast<bool>(res[i].final_pose) ||
+          (res[i].final_pose && std::memcmp(&*lane_res[i].final_pose, &*res[i].final_pose, sizeof(sg::RigidTransform))))
+        return 3;
+    std::printf("lane on a second thread: identical results\n");
   }
   return ok >= n_test / 2 ? 0 : 1;
 }

@@ -161,9 +161,21 @@ class Relocaliser {
     check(scr_scene_create(dev.handle(), forest_blob.data(), forest_blob.size(), &fp, &k, adapt_seed, max_batch, &s_),
           "deserialize_forest / scene create");
   }
-  ~Relocaliser() { scr_scene_destroy(s_); }
+  ~Relocaliser() {
+    if (s_) scr_scene_destroy(s_);
+  }
   Relocaliser(const Relocaliser&) = delete;
   Relocaliser& operator=(const Relocaliser&) = delete;
+  Relocaliser(Relocaliser&& o) noexcept : s_(o.s_) { o.s_ = nullptr; }
+
+  // A relocalisation lane (scr_scene_fork): shares this relocaliser's forest, adaptation
+  // state and model, with its own CUDA stream and workspace, so another host thread can
+  // relocalise concurrently. Lanes are read-only and must be destroyed before their root.
+  Relocaliser fork_lane(int max_batch = 64) {
+    scr_scene h = nullptr;
+    check(scr_scene_fork(s_, max_batch, &h), "fork_lane");
+    return Relocaliser(h);
+  }
 
   void set_scene_model(const std::vector<scr_prim>& prims) {
     check(scr_scene_set_analytic_model(s_, prims.data(), static_cast<int>(prims.size())), "set_scene_model");
@@ -222,6 +234,7 @@ class Relocaliser {
   scr_scene handle() const { return s_; }
 
  private:
+  explicit Relocaliser(scr_scene h) : s_(h) {}
   scr_scene s_ = nullptr;
 };
 

@@ -103,6 +103,12 @@ void scr_device_close(scr_device dev);
 scr_status scr_scene_create(scr_device dev, const uint8_t* forest_blob, size_t n, const scr_forest_params* fp,
                             const scr_intrinsics* k, uint64_t adapt_seed, int max_batch, scr_scene* out);
 void scr_scene_destroy(scr_scene s);
+/* Relocalisation lane: a second handle on the same forest, adaptation state and model with
+ * its own CUDA stream and batch workspace, so several host threads can relocalise
+ * concurrently (the reference facade is reentrant for distinct RNG streams).
+ * Lanes are read-only (train/update/reset/model/import return SCR_E_ARG) and always see
+ * the root scene's last completed update. Destroy lanes before the root. */
+scr_status scr_scene_fork(scr_scene root, int max_batch, scr_scene* out);
 int64_t scr_scene_total_leaves(scr_scene s);
 void* scr_scene_stream(scr_scene s); /* cudaStream_t all scene work runs on */
 /* SceneModel used by ICP + ranking: analytic synthetic scene */

@@ -145,6 +145,11 @@ struct scr_scene_s {
   scr::Prim* d_prims = nullptr;
   int n_prims = 0;
   scr::Workspace ws;
+  // relocalisation lanes (scr_scene_fork): a lane shares the parent's read-only device
+  // state (forest, predictions, model) and owns a stream + workspace of its own
+  scr_scene_s* parent = nullptr;
+  int lanes = 0;                      // live lanes forked from this scene
+  cudaEvent_t published = nullptr;    // recorded after every update of shared state
   int64_t launches = 0;
   scr::Profiler prof;
   scr::ForestView forest_view() const;
@@ -182,6 +187,8 @@ inline unsigned long long* work_ptr(scr_scene s) { return s->prof.on ? s->prof.d
   } while (0)
 
 // scene.cu
+scr_status refresh_lane(scr_scene s);
+scr_status publish(scr_scene s);
 scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_base, const int* d_idx, int n);
 scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int samples);
 scr_status ensure_icp_ws(scr_scene s, int jobs);

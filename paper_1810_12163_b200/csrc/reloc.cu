@@ -1894,11 +1894,12 @@ scr_status scr_cascade_batch(scr_scene s, const scr_frame* frames, int n, const 
   if (!s) return SCR_E_ARG;
   SCR_TRY(check_stage_args(n, stages, modes, nstages, seeds, out));
   if (nstages > 1 && !thr) return SCR_E_ARG;
-  if (!s->d_prims) {  // every mode scores its output against the model (A11)
+  if (!(s->parent ? s->parent->d_prims : s->d_prims)) {  // every mode scores against the model (A11)
     set_error("relocalise: no scene model set (scr_scene_set_analytic_model)");
     return SCR_E_ARG;
   }
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
   for (int b0 = 0; b0 < n; b0 += s->ws.cap) {
     const int nb = std::min(s->ws.cap, n - b0);
@@ -1926,11 +1927,12 @@ scr_status scr_cascade_frameset(scr_scene s, scr_frameset fs, const int32_t* idx
   if (!s || !fs || (!idx && n > 0)) return SCR_E_ARG;
   SCR_TRY(check_stage_args(n, stages, modes, nstages, seeds, out));
   if (nstages > 1 && !thr) return SCR_E_ARG;
-  if (!s->d_prims) {
+  if (!(s->parent ? s->parent->d_prims : s->d_prims)) {
     set_error("relocalise: no scene model set (scr_scene_set_analytic_model)");
     return SCR_E_ARG;
   }
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   for (int i = 0; i < n; ++i)
     if (idx[i] < 0 || idx[i] >= fs->cap) return SCR_E_ARG;
   for (int b0 = 0; b0 < n; b0 += s->ws.cap) {
@@ -1947,6 +1949,7 @@ scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_pa
                             scr_pose* surv_poses, float* surv_energy, int* n_surv) {
   if (!s || !f || !p || !n_gen || !n_surv) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
   SCR_CUDA(cudaMemcpyAsync(s->ws.depth, f->depth, WH * sizeof(float), cudaMemcpyHostToDevice, s->stream));
   SCR_CUDA(cudaMemcpyAsync(s->ws.rgb, f->rgb, WH * 3, cudaMemcpyHostToDevice, s->stream));
@@ -2003,6 +2006,7 @@ scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, 
                          double* rms, double* inlier_frac, double* score) {
   if (!s || !f || !init || !s->d_prims) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
   SCR_TRY(ensure_ransac_ws(s, 1, 1, 1));
   SCR_TRY(ensure_icp_ws(s, 1));

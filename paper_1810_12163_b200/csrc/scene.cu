@@ -604,6 +604,71 @@ scr_status dalloc(T** p, size_t count) {
   } while (0)
 }  // namespace
 
+namespace scr {
+// Per-lane batch workspace (frames addressed by workspace slot f in [0, max_batch)).
+scr_status alloc_workspace(scr_scene s, int max_batch) {
+  const scr_intrinsics* k = &s->k;
+  const int64_t L = s->L;
+  scr_status st;
+  Workspace& w = s->ws;
+  w.cap = max_batch;
+  w.gmax = ((k->width + 3) / 4) * ((k->height + 3) / 4);
+  const size_t WH = static_cast<size_t>(k->width) * k->height;
+  const size_t B = static_cast<size_t>(max_batch);
+  if ((st = dalloc(&w.depth, B * WH)) != SCR_OK) return st;
+  if ((st = dalloc(&w.rgb, B * WH * 3)) != SCR_OK) return st;
+  if ((st = dalloc(&w.tex, B * WH)) != SCR_OK) return st;
+  if ((st = dalloc(&w.gcount, B)) != SCR_OK) return st;
+  if ((st = dalloc(&w.gpx, B * w.gmax)) != SCR_OK) return st;
+  if ((st = dalloc(&w.gcam, B * w.gmax)) != SCR_OK) return st;
+  if ((st = dalloc(&w.gslot, B * w.gmax * s->T)) != SCR_OK) return st;
+  if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return st;
+  if ((st = dalloc(&w.grec, B * w.gmax)) != SCR_OK) return st;
+  if ((st = dalloc(&w.gleaf, B * w.gmax)) != SCR_OK) return st;
+  if ((st = dalloc(&w.gcamd, B * w.gmax)) != SCR_OK) return st;
+  if ((st = dalloc(&w.fidx, B)) != SCR_OK) return st;
+  if ((st = dalloc(&w.seeds, B)) != SCR_OK) return st;
+  if ((st = dalloc(&w.status, B)) != SCR_OK) return st;
+  if ((st = dalloc(&w.hctr, B)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_cnt, L)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_off, L + 1)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_cur, L)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_item, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_tgt, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_rank, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_total, 1)) != SCR_OK) return st;
+  return SCR_OK;
+}
+
+// A lane reads the parent's current shared pointers and orders its stream after the
+// parent's last published update (readers never see a half-published state).
+scr_status refresh_lane(scr_scene s) {
+  scr_scene p = s->parent;
+  if (!p) return SCR_OK;
+  s->d_nodes = p->d_nodes;
+  s->d_specs = p->d_specs;
+  s->d_entries = p->d_entries;
+  s->d_seen = p->d_seen;
+  s->d_count = p->d_count;
+  s->d_geom = p->d_geom;
+  s->d_col = p->d_col;
+  s->d_cov = p->d_cov;
+  s->d_prims = p->d_prims;
+  s->n_prims = p->n_prims;
+  s->cursor = p->cursor;
+  if (p->published && s->stream) SCR_CUDA(cudaStreamWaitEvent(s->stream, p->published, 0));
+  return SCR_OK;
+}
+
+// Marks the end of an update of shared state on the scene's stream (lanes wait on it).
+scr_status publish(scr_scene s) {
+  if (!s->published) SCR_CUDA(cudaEventCreateWithFlags(&s->published, cudaEventDisableTiming));
+  SCR_CUDA(cudaEventRecord(s->published, s->stream));
+  return SCR_OK;
+}
+
+}  // namespace scr
+
 extern "C" {
 
 const char* scr_last_error(void) { return g_err.c_str(); }
@@ -741,34 +806,7 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   if (e != cudaSuccess) return fail(cuda_fail(e, "upload nodes"));
   e = cudaMemcpy(s->d_specs, specs.data(), kFeatures * sizeof(short4), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return fail(cuda_fail(e, "upload specs"));
-  // workspace
-  Workspace& w = s->ws;
-  w.cap = max_batch;
-  w.gmax = ((k->width + 3) / 4) * ((k->height + 3) / 4);
-  const size_t WH = static_cast<size_t>(k->width) * k->height;
-  const size_t B = static_cast<size_t>(max_batch);
-  if ((st = dalloc(&w.depth, B * WH)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.rgb, B * WH * 3)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.tex, B * WH)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.gcount, B)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.gpx, B * w.gmax)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.gcam, B * w.gmax)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.gslot, B * w.gmax * s->T)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.grec, B * w.gmax)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.gleaf, B * w.gmax)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.gcamd, B * w.gmax)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.fidx, B)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.seeds, B)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.status, B)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.hctr, B)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.ins_cnt, L)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.ins_off, L + 1)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.ins_cur, L)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.ins_item, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.ins_tgt, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.ins_rank, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return fail(st);
-  if ((st = dalloc(&w.ins_total, 1)) != SCR_OK) return fail(st);
+  if ((st = alloc_workspace(s, max_batch)) != SCR_OK) return fail(st);
   if ((st = scr_reset(s)) != SCR_OK) return fail(st);
   e = cudaFuncSetAttribute(k_rqs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return fail(cuda_fail(e, "cudaFuncSetAttribute(k_rqs)"));
@@ -779,10 +817,52 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   return SCR_OK;
 }
 
+scr_status scr_scene_fork(scr_scene parent, int max_batch, scr_scene* out) {
+  if (!parent || !out || max_batch <= 0 || max_batch > 4096) {
+    set_error("scr_scene_fork: bad arguments (max_batch 1..4096)");
+    return SCR_E_ARG;
+  }
+  if (parent->parent) {
+    set_error("scr_scene_fork: fork the root scene, not a lane");
+    return SCR_E_ARG;
+  }
+  SCR_CUDA(cudaSetDevice(parent->dev->ordinal));
+  scr_scene s = new scr_scene_s();
+  s->parent = parent;
+  s->dev = parent->dev;
+  s->k = parent->k;
+  s->geom = parent->geom;
+  s->fp = parent->fp;
+  s->adapt_seed = parent->adapt_seed;
+  s->T = parent->T;
+  s->L = parent->L;
+  s->cursor = parent->cursor;
+  s->node_base = parent->node_base;
+  s->leaf_base = parent->leaf_base;
+  s->leaves16 = parent->leaves16;
+  parent->lanes++;
+  scr_status st = refresh_lane(s);
+  cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) st = cuda_fail(e, "cudaStreamCreate");
+  if (st == SCR_OK) st = alloc_workspace(s, max_batch);
+  if (st != SCR_OK) {
+    scr_scene_destroy(s);
+    return st;
+  }
+  *out = s;
+  return SCR_OK;
+}
+
 void scr_scene_destroy(scr_scene s) {
   if (!s) return;
   cudaSetDevice(s->dev->ordinal);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  if (s->parent) {  // a lane: the shared state belongs to the parent
+    s->parent->lanes--;
+    s->d_nodes = nullptr; s->d_specs = nullptr; s->d_entries = nullptr; s->d_seen = nullptr;
+    s->d_count = nullptr; s->d_geom = nullptr; s->d_col = nullptr; s->d_cov = nullptr; s->d_prims = nullptr;
+  }
+  if (s->published) cudaEventDestroy(s->published);
   void* ptrs[] = {s->d_nodes, s->d_specs, s->d_entries, s->d_seen, s->d_count, s->d_geom, s->d_col, s->d_cov,
                   s->d_prims, s->ws.depth, s->ws.rgb, s->ws.tex, s->ws.gcount, s->ws.gpx, s->ws.gcam, s->ws.gslot,
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
@@ -830,7 +910,7 @@ void* scr_scene_stream(scr_scene s) { return s ? static_cast<void*>(s->stream) :
 int64_t scr_kernel_launches(scr_scene s) { return s ? s->launches : 0; }
 int64_t scr_update_cursor(scr_scene s) { return s ? s->cursor : 0; }
 
-scr_status scr_scene_set_analytic_model(scr_scene s, const scr_prim* prims, int n) {
+static scr_status scr_scene_set_analytic_model_impl(scr_scene s, const scr_prim* prims, int n) {
   if (!s || (!prims && n > 0) || n < 0 || n > 256) {
     set_error("scr_scene_set_analytic_model: 0..256 primitives");
     return SCR_E_ARG;
@@ -862,7 +942,7 @@ scr_status scr_scene_set_analytic_model(scr_scene s, const scr_prim* prims, int 
   return SCR_OK;
 }
 
-scr_status scr_reset(scr_scene s) {
+static scr_status scr_reset_impl(scr_scene s) {
   if (!s) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_CUDA(cudaMemsetAsync(s->d_entries, 0, static_cast<size_t>(s->L) * s->fp.capacity * sizeof(scr_entry), s->stream));
@@ -951,7 +1031,7 @@ extern "C" {
 
 scr_status scr_train(scr_scene s, const scr_frame* frame, const scr_pose* pose) { return scr_train_batch(s, frame, pose, 1); }
 
-scr_status scr_train_batch(scr_scene s, const scr_frame* frames, const scr_pose* poses, int n) {
+static scr_status scr_train_batch_impl(scr_scene s, const scr_frame* frames, const scr_pose* poses, int n) {
   if (!s || (!frames && n > 0) || (!poses && n > 0) || n < 0) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   for (int i = 0; i < n; ++i) {
@@ -967,7 +1047,7 @@ scr_status scr_train_batch(scr_scene s, const scr_frame* frames, const scr_pose*
   return SCR_OK;
 }
 
-scr_status scr_train_frameset(scr_scene s, scr_frameset fs, const int32_t* idx, const scr_pose* poses, int n) {
+static scr_status scr_train_frameset_impl(scr_scene s, scr_frameset fs, const int32_t* idx, const scr_pose* poses, int n) {
   if (!s || !fs || (!idx && n > 0) || (!poses && n > 0)) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
@@ -980,7 +1060,7 @@ scr_status scr_train_frameset(scr_scene s, scr_frameset fs, const int32_t* idx, 
   return SCR_OK;
 }
 
-scr_status scr_update(scr_scene s, int64_t leaves_per_call) {
+static scr_status scr_update_impl(scr_scene s, int64_t leaves_per_call) {
   if (!s || leaves_per_call < 0) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   const int64_t n = std::min<int64_t>(leaves_per_call, s->L);
@@ -1060,6 +1140,7 @@ scr_status scr_debug_cluster(scr_scene s, const scr_entry* e, int n, scr_mode* o
 scr_status scr_dump_seen(scr_scene s, uint32_t* out) {
   if (!s || !out) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   SCR_CUDA(cudaStreamSynchronize(s->stream));
   SCR_CUDA(cudaMemcpy(out, s->d_seen, s->L * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   return SCR_OK;
@@ -1068,6 +1149,7 @@ scr_status scr_dump_seen(scr_scene s, uint32_t* out) {
 scr_status scr_dump_entries(scr_scene s, int64_t slot0, int64_t nslots, scr_entry* out) {
   if (!s || !out || slot0 < 0 || nslots < 0 || slot0 + nslots > s->L) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   SCR_CUDA(cudaStreamSynchronize(s->stream));
   SCR_CUDA(cudaMemcpy(out, s->d_entries + slot0 * s->fp.capacity,
                       static_cast<size_t>(nslots) * s->fp.capacity * sizeof(scr_entry), cudaMemcpyDeviceToHost));
@@ -1077,6 +1159,7 @@ scr_status scr_dump_entries(scr_scene s, int64_t slot0, int64_t nslots, scr_entr
 scr_status scr_dump_predictions(scr_scene s, int32_t* counts, scr_mode* modes) {
   if (!s || !counts) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   SCR_CUDA(cudaStreamSynchronize(s->stream));
   SCR_CUDA(cudaMemcpy(counts, s->d_count, s->L * sizeof(int), cudaMemcpyDeviceToHost));
   if (!modes) return SCR_OK;
@@ -1101,7 +1184,7 @@ scr_status scr_dump_predictions(scr_scene s, int32_t* counts, scr_mode* modes) {
   return SCR_OK;
 }
 
-scr_status scr_load_predictions(scr_scene s, const int32_t* counts, const scr_mode* modes) {
+static scr_status scr_load_predictions_impl(scr_scene s, const int32_t* counts, const scr_mode* modes) {
   if (!s || !counts || !modes) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   const size_t M = static_cast<size_t>(s->L) * kMaxModes;
@@ -1136,6 +1219,7 @@ size_t scr_predictions_bytes(scr_scene s) {
 scr_status scr_predictions_export(scr_scene s, void* dst) {
   if (!s || !dst) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   const size_t M = static_cast<size_t>(s->L) * kMaxModes;
   char* p = static_cast<char*>(dst);
   SCR_CUDA(cudaMemcpyAsync(p, s->d_count, s->L * sizeof(int), cudaMemcpyDeviceToDevice, s->stream));
@@ -1149,7 +1233,7 @@ scr_status scr_predictions_export(scr_scene s, void* dst) {
   return SCR_OK;
 }
 
-scr_status scr_predictions_import(scr_scene s, const void* src) {
+static scr_status scr_predictions_import_impl(scr_scene s, const void* src) {
   if (!s || !src) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   const size_t M = static_cast<size_t>(s->L) * kMaxModes;
@@ -1168,6 +1252,7 @@ scr_status scr_predictions_import(scr_scene s, const void* src) {
 scr_status scr_debug_leaves(scr_scene s, const scr_frame* f, int32_t* grid_px, int32_t* leaves, int* n_grid) {
   if (!s || !f || !n_grid) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   SCR_TRY(upload_frames(s, f, 1));
   SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
   int G = 0;
@@ -1187,6 +1272,7 @@ scr_status scr_debug_leaves(scr_scene s, const scr_frame* f, int32_t* grid_px, i
 scr_status scr_debug_features(scr_scene s, const scr_frame* f, const int32_t* px, int n, float* out) {
   if (!s || !f || !px || !out || n < 0) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   SCR_TRY(upload_frames(s, f, 1));
   SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
   int* d_px = nullptr;
@@ -1259,11 +1345,12 @@ scr_status scr_frameset_upload(scr_frameset fs, int first, const scr_frame* fram
 scr_status scr_frameset_render(scr_frameset fs, int first, const scr_pose* poses, int n) {
   if (!fs || first < 0 || n < 0 || first + n > fs->cap || !poses) return SCR_E_ARG;
   scr_scene s = fs->scene;
-  if (!s->d_prims) {
+  if (!(s->parent ? s->parent->d_prims : s->d_prims)) {
     set_error("scr_frameset_render: no analytic model set");
     return SCR_E_ARG;
   }
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
   Pose* d_p = nullptr;
   SCR_CUDA(cudaMalloc(&d_p, std::max(1, n) * sizeof(Pose)));
@@ -1290,6 +1377,77 @@ scr_status scr_frameset_download(scr_frameset fs, int first, int n, float* depth
   if (depth) SCR_CUDA(cudaMemcpy(depth, fs->depth + first * WH, n * WH * sizeof(float), cudaMemcpyDeviceToHost));
   if (rgb) SCR_CUDA(cudaMemcpy(rgb, fs->rgb + first * WH * 3, n * WH * 3, cudaMemcpyDeviceToHost));
   return SCR_OK;
+}
+
+// Updates of shared scene state: refused on lanes, published to lanes when done.
+scr_status scr_scene_set_analytic_model(scr_scene s, const scr_prim* prims, int n) {
+  if (s && s->parent) {
+    set_error("scr_scene_set_analytic_model: a relocalisation lane is read-only; update the scene it was forked from");
+    return SCR_E_ARG;
+  }
+  scr_status st = scr_scene_set_analytic_model_impl(s, prims, n);
+  if (st == SCR_OK && s) st = publish(s);
+  return st;
+}
+
+scr_status scr_reset(scr_scene s) {
+  if (s && s->parent) {
+    set_error("scr_reset: a relocalisation lane is read-only; update the scene it was forked from");
+    return SCR_E_ARG;
+  }
+  scr_status st = scr_reset_impl(s);
+  if (st == SCR_OK && s) st = publish(s);
+  return st;
+}
+
+scr_status scr_train_batch(scr_scene s, const scr_frame* frames, const scr_pose* poses, int n) {
+  if (s && s->parent) {
+    set_error("scr_train_batch: a relocalisation lane is read-only; update the scene it was forked from");
+    return SCR_E_ARG;
+  }
+  scr_status st = scr_train_batch_impl(s, frames, poses, n);
+  if (st == SCR_OK && s) st = publish(s);
+  return st;
+}
+
+scr_status scr_train_frameset(scr_scene s, scr_frameset fs, const int32_t* idx, const scr_pose* poses, int n) {
+  if (s && s->parent) {
+    set_error("scr_train_frameset: a relocalisation lane is read-only; update the scene it was forked from");
+    return SCR_E_ARG;
+  }
+  scr_status st = scr_train_frameset_impl(s, fs, idx, poses, n);
+  if (st == SCR_OK && s) st = publish(s);
+  return st;
+}
+
+scr_status scr_update(scr_scene s, int64_t leaves_per_call) {
+  if (s && s->parent) {
+    set_error("scr_update: a relocalisation lane is read-only; update the scene it was forked from");
+    return SCR_E_ARG;
+  }
+  scr_status st = scr_update_impl(s, leaves_per_call);
+  if (st == SCR_OK && s) st = publish(s);
+  return st;
+}
+
+scr_status scr_load_predictions(scr_scene s, const int32_t* counts, const scr_mode* modes) {
+  if (s && s->parent) {
+    set_error("scr_load_predictions: a relocalisation lane is read-only; update the scene it was forked from");
+    return SCR_E_ARG;
+  }
+  scr_status st = scr_load_predictions_impl(s, counts, modes);
+  if (st == SCR_OK && s) st = publish(s);
+  return st;
+}
+
+scr_status scr_predictions_import(scr_scene s, const void* src) {
+  if (s && s->parent) {
+    set_error("scr_predictions_import: a relocalisation lane is read-only; update the scene it was forked from");
+    return SCR_E_ARG;
+  }
+  scr_status st = scr_predictions_import_impl(s, src);
+  if (st == SCR_OK && s) st = publish(s);
+  return st;
 }
 
 }  // extern "C"

@@ -108,6 +108,7 @@ SIGNATURES = {
     "scr_scene_create": (C.c_int, [_vp, _P(C.c_uint8), _sz, _P(ForestParams), _P(Intrinsics), _u64, C.c_int,
                                    _P(_vp)]),
     "scr_scene_destroy": (None, [_vp]),
+    "scr_scene_fork": (C.c_int, [_vp, C.c_int, _P(_vp)]),
     "scr_scene_total_leaves": (_i64, [_vp]),
     "scr_scene_stream": (_vp, [_vp]),
     "scr_scene_set_analytic_model": (C.c_int, [_vp, _vp, C.c_int]),

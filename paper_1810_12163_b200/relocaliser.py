@@ -150,8 +150,25 @@ class Scene:
         self.handle = h
         self.total_leaves = int(self.lib.scr_scene_total_leaves(h))
         self.trees = int(np.frombuffer(forest_blob[8:12], "<u4")[0])
+        self.max_batch = max_batch
+        self._lanes = []
+
+    def fork(self, max_batch: int | None = None) -> "Scene":
+        """A relocalisation lane: same forest / predictions / model, own stream + workspace
+        (scr_scene_fork). Lanes let several host threads relocalise concurrently."""
+        lane = Scene.__new__(Scene)
+        lane.lib, lane.device, lane.k, lane.fparams = self.lib, self.device, self.k, self.fparams
+        h = C.c_void_p()
+        N.check(self.lib.scr_scene_fork(self.handle, max_batch or self.max_batch, C.byref(h)), "scr_scene_fork")
+        lane.handle = h
+        lane.total_leaves, lane.trees, lane.max_batch = self.total_leaves, self.trees, max_batch or self.max_batch
+        lane.root = self  # the root must outlive its lanes
+        self._lanes.append(lane)
+        return lane
 
     def close(self):
+        for lane in getattr(self, "_lanes", []):
+            lane.close()
         if self.handle:
             self.lib.scr_scene_destroy(self.handle)
             self.handle = None
@@ -391,7 +408,8 @@ class FrameSet:
         N.check(self.lib.scr_train_frameset(self.scene.handle, self.handle, N.ptr(idx, C.c_int32), ps, idx.size),
                 "integrate_frame")
 
-    def cascade(self, idx, config: CascadeConfig, seeds) -> list[N.Result]:
+    def cascade(self, idx, config: CascadeConfig, seeds, scene: "Scene | None" = None) -> list[N.Result]:
+        """run_cascade over resident frames idx; `scene` may be a lane of the owning scene."""
         idx = np.ascontiguousarray(list(idx), np.int32)
         n = idx.size
         st = (N.RansacParams * len(config.stages))(*config.stages)
@@ -399,7 +417,7 @@ class FrameSet:
         th = np.asarray(list(config.thresholds) + [0.0], np.float64)
         sd = np.ascontiguousarray(seeds, np.uint64)
         out = (N.Result * n)()
-        N.check(self.lib.scr_cascade_frameset(self.scene.handle, self.handle, N.ptr(idx, C.c_int32), n, st,
+        N.check(self.lib.scr_cascade_frameset((scene or self.scene).handle, self.handle, N.ptr(idx, C.c_int32), n, st,
                                               N.ptr(md, C.c_int32), N.ptr(th, C.c_double), len(config.stages),
                                               N.ptr(sd, C.c_uint64), out), "run_cascade")
         return list(out)

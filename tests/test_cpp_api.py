@@ -14,7 +14,7 @@ def build_example():
 
     build.build()
     lib = os.path.join(ROOT, "paper_1810_12163_b200", "lib")
-    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-pthread", "-I", os.path.join(ROOT, "include"),
                     os.path.join(ROOT, "examples", "cpp_drop_in.cpp"), "-L", lib, "-lscreloc_gpu",
                     f"-Wl,-rpath,{lib}", "-o", EXE], check=True)
     return EXE

@@ -1,0 +1,91 @@
+"""Relocalisation lanes (scr_scene_fork): concurrent relocalisation on one GPU.
+
+A lane shares the root scene's forest, adaptation state and model and owns a stream and a
+workspace; results must be bit-identical to the root's, from any thread, and a lane must
+see the root's updates and refuse to make its own."""
+import threading
+
+import numpy as np
+import pytest
+
+from world import OracleWorld, gpu_scene
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def adapted(oracle, gpu_device):
+    w = OracleWorld(oracle, scene_seed=3, n_adapt=20, n_test=8)
+    s = gpu_scene(gpu_device, w)
+    s.integrate_frames(list(w.D), list(w.RGB), w.adapt_poses)
+    s.update_leaves_round_robin(s.total_leaves)
+    return w, s
+
+
+def test_lane_matches_root(adapted):
+    import paper_1810_12163_b200 as P
+
+    w, s = adapted
+    lane = s.fork(8)
+    cfg = P.CascadeConfig.paper_three_stage()
+    seeds = [900 + i for i in range(len(w.test_poses))]
+    a = s.run_cascade_batch(w.Dt, w.RGBt, cfg, seeds)
+    b = lane.run_cascade_batch(w.Dt, w.RGBt, cfg, seeds)
+    for x, y in zip(a, b):
+        assert x.stage_used == y.stage_used and x.has_pose == y.has_pose
+        if x.has_pose:
+            assert bytes(x.pose) == bytes(y.pose) and x.score == y.score
+    lane.close()
+
+
+def test_lanes_concurrent_threads(adapted):
+    import paper_1810_12163_b200 as P
+
+    w, s = adapted
+    lanes = [s.fork(8) for _ in range(3)]
+    cfg = P.CascadeConfig.paper_three_stage()
+    seeds = [40 + i for i in range(len(w.test_poses))]
+    ref = s.run_cascade_batch(w.Dt, w.RGBt, cfg, seeds)
+    out = [None] * len(lanes)
+
+    def run(i):
+        for _ in range(3):
+            out[i] = lanes[i].run_cascade_batch(w.Dt, w.RGBt, cfg, seeds)
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(len(lanes))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for res in out:
+        for x, y in zip(ref, res):
+            assert bytes(x.pose) == bytes(y.pose) and x.stage_used == y.stage_used
+    for lane in lanes:
+        lane.close()
+
+
+def test_lane_is_read_only_and_sees_updates(adapted):
+    import paper_1810_12163_b200 as P
+    import paper_1810_12163_b200.native as N
+
+    w, s = adapted
+    lane = s.fork(4)
+    with pytest.raises(N.ScrelocError):
+        lane.update_leaves_round_robin(16)
+    with pytest.raises(N.ScrelocError):
+        lane.integrate_frame(w.D[0], w.RGB[0], w.adapt_poses[0])
+    p = P.ransac_params("fast")
+    before = lane.relocalise_batch(w.Dt[:2], w.RGBt[:2], p, 1, [5, 6])
+    # the root clears its adaptation: the lane must observe it (no predictions -> no pose)
+    s.clear_adaptation()
+    after = lane.relocalise_batch(w.Dt[:2], w.RGBt[:2], p, 1, [5, 6])
+    assert any(r.has_pose for r in before)
+    assert not any(r.has_pose for r in after)
+    # re-adapt on the root: the lane reproduces the root's results again
+    s.integrate_frames(list(w.D), list(w.RGB), w.adapt_poses)
+    s.update_leaves_round_robin(s.total_leaves)
+    again = lane.relocalise_batch(w.Dt[:2], w.RGBt[:2], p, 1, [5, 6])
+    root = s.relocalise_batch(w.Dt[:2], w.RGBt[:2], p, 1, [5, 6])
+    for x, y in zip(again, root):
+        assert bytes(x.pose) == bytes(y.pose)
+    lane.close()
