@@ -49,7 +49,9 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 
 
 def kernel_short(name: str) -> str:
-    n = name.split("(")[0]
+    n = name.split("(")[0].strip()
+    if n.startswith("void "):
+        n = n[5:]
     return n.split("::")[-1].strip()
 
 
@@ -125,7 +127,7 @@ def full(reps: list[str], tag: str) -> str:
             if name not in picked or dur > picked[name][0]:
                 picked[name] = (dur, d, rep)
     for name, (_, d, rep) in sorted(picked.items(), key=lambda x: -x[1][0]):
-        if True:
+        if name:
             md.append(f"## {name}  ({os.path.basename(rep)})")
             md.append("| metric | value |")
             md.append("|---|---|")
