@@ -131,9 +131,9 @@ SCR_DEV bool colour_ok(uint32_t col, float4 mc, float thresh) {
   return !(linf > thresh);
 }
 
-// Kabsch (f64 SVD) runs only for triplets that passed every check; out of line so it does
-// not set the register budget of the retry loop.
-__device__ __noinline__ bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return kabsch3(cm, w, *T); }
+// Kabsch for a triplet that passed every check. Inlined: an out-of-line call inside the
+// attempt loop costs more (caller-saved registers around the call) than the extra code.
+SCR_DEV bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return kabsch3(cm, w, *T); }
 
 // Checks 2-3 (distances in f64) and Kabsch for a triplet whose colour
 // check passed. Camera points come precomputed (f64 backprojection, K1).
@@ -1185,7 +1185,12 @@ __device__ __forceinline__ int cta_isum(int v, int* ired) {
 // Gauss-Newton step of ICP on the reduced normal equations (one thread): damped 6x6
 // Cholesky solve, T <- exp(delta) T. Kept out of line (and un-unrolled) so its f64
 // temporaries do not set the register budget of the pixel loops.
-__device__ __noinline__ bool icp_step(const double* tot, Pose* T) {
+#ifdef SCR_ICP_STEP_INLINE
+SCR_DEV
+#else
+__device__ __noinline__
+#endif
+bool icp_step(const double* tot, Pose* T) {
   double M[36], rhs[6], delta[6];
   int k = 0;
 #pragma unroll 1
