@@ -12,8 +12,9 @@ class OracleWorld:
     """Scene + random forest + adapted state on the CPU oracle."""
 
     def __init__(self, oracle, scene_seed=1, n_adapt=30, n_test=6, forest=of.FOREST_DEFAULT, cluster=True,
-                 adapt_seed=7, forest_seed=42):
+                 adapt_seed=7, forest_seed=42, k=None):
         self.O = O = oracle
+        self.k = k = K if k is None else k
         L = O.lib
         self.scene_seed = scene_seed
         self.fp = dict(forest)
@@ -21,14 +22,14 @@ class OracleWorld:
         self.prims = O.scene_prims(self.scene)
         self.adapt_poses = O.trajectory(scene_seed, n_adapt, 0)
         self.test_poses = O.trajectory(scene_seed, n_test, 1)
-        self.D, self.RGB = O.render(self.scene, self.adapt_poses, K)
-        self.Dt, self.RGBt = O.render(self.scene, self.test_poses, K)
+        self.D, self.RGB = O.render(self.scene, self.adapt_poses, k)
+        self.Dt, self.RGBt = O.render(self.scene, self.test_poses, k)
         self.forest = L.or_forest_random(forest_seed, 14, 0.4, 5, 130)
         self.blob = O.serialize(self.forest)
         self.total_leaves = L.or_forest_total_leaves(self.forest)
         self.state = O.state_create(self.forest, self.fp, adapt_seed)
         for i in range(n_adapt):
-            assert O.integrate(self.state, self.forest, self.D[i], self.RGB[i], K, self.adapt_poses[i]) == 0
+            assert O.integrate(self.state, self.forest, self.D[i], self.RGB[i], k, self.adapt_poses[i]) == 0
         if cluster:
             L.or_update_all_parallel(self.state, 8)
 
@@ -39,8 +40,9 @@ class OracleWorld:
 def gpu_scene(device, world: OracleWorld, max_batch=8, adapt_seed=7):
     import paper_1810_12163_b200 as P
 
-    s = P.Scene(device, world.blob, P.forest_params(world.fp), P.intrinsics(), adapt_seed=adapt_seed,
-                max_batch=max_batch)
+    k = world.k
+    s = P.Scene(device, world.blob, P.forest_params(world.fp),
+                P.intrinsics(k.width, k.height, k.fx, k.fy, k.cx, k.cy), adapt_seed=adapt_seed, max_batch=max_batch)
     s.set_model(world.prims)
     return s
 
