@@ -144,10 +144,27 @@ __device__ __noinline__
 #else
 SCR_DEV
 #endif
-bool geometry_checks(double min_sq_dist, double rigidity_tol, const double4* gcamd,
+bool geometry_checks(double min_sq_dist, double rigidity_tol, const double4* gcamd, const float4* gcam,
                                              const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1, int m2,
                                              Pose* T) {
   const float4 w0 = geom[m0].q0, w1 = geom[m1].q0, w2 = geom[m2].q0;
+  {  // f32 pre-filter: rejects only triplets the exact f64 checks reject too. World points are
+     // the same f32 values; camera points are the f64 ones rounded to f32 (<= 4e-7 m at 6 m);
+     // the f32 distances are within 1e-5 m, far inside the 1e-3 m / 1e-3 m^2 margins.
+    const float4 f0 = gcam[g0], f1 = gcam[g1], f2 = gcam[g2];
+    const float4 wf[3] = {w0, w1, w2}, cf[3] = {f0, f1, f2};
+    const float tolf = static_cast<float>(rigidity_tol) + 1e-3f;
+    const float closef = static_cast<float>(min_sq_dist) - 1e-3f;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
+      const float ax = wf[pa].x - wf[pb].x, ay = wf[pa].y - wf[pb].y, az = wf[pa].z - wf[pb].z;
+      const float bx = cf[pa].x - cf[pb].x, by = cf[pa].y - cf[pb].y, bz = cf[pa].z - cf[pb].z;
+      const float dw2f = ax * ax + ay * ay + az * az, dc2f = bx * bx + by * by + bz * bz;
+      if (dw2f < closef) return false;
+      if (fabsf(sqrtf(dw2f) - sqrtf(dc2f)) > tolf) return false;
+    }
+  }
   const double4 c0 = gcamd[g0], c1 = gcamd[g1], c2 = gcamd[g2];
   double w[9] = {w0.x, w0.y, w0.z, w1.x, w1.y, w1.z, w2.x, w2.y, w2.z};
   double cm[9] = {c0.x, c0.y, c0.z, c1.x, c1.y, c1.z, c2.x, c2.y, c2.z};
@@ -369,7 +386,7 @@ __global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, F
         att = e.owner_att >> 5;
         eslot = e.slot;
         if (s_cur[wid][owner] == eslot) {  // stale if the owner's slot was already resolved
-          pass = geometry_checks(gp.min_sq_dist, gp.rigidity_tol, fr.gcamd + fbase, pv.geom, e.g0, e.g1, e.g2, e.m0, e.m1, e.m2, &T);
+          pass = geometry_checks(gp.min_sq_dist, gp.rigidity_tol, fr.gcamd + fbase, fr.gcam + fbase, pv.geom, e.g0, e.g1, e.g2, e.m0, e.m1, e.m2, &T);
           atomicSub(&s_pend[wid][owner], 1);
           if (pass) atomicMin(&s_best[wid][owner], att);
         }
