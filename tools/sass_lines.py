@@ -66,6 +66,7 @@ def line_map(kernel_mangled_sub: str):
 def main():
     rep, kernel = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+    by_exec = len(sys.argv) > 4 and sys.argv[4] == "exec"
     name, rows = sass_rows(rep, kernel)
     base = int(rows[0]["Address"], 16)
     lm = line_map(kernel)
@@ -85,10 +86,14 @@ def main():
         if os.path.exists(p):
             src[f] = open(p).read().splitlines()
     print(f"{name[:100]}\n{tot} samples, {len(rows)} SASS instructions, {len(lm)} mapped")
-    for key, s in samples.most_common(top):
+    order = execd.most_common(top) if by_exec else samples.most_common(top)
+    tot_exec = max(1, sum(execd.values()))
+    print(f"{sum(execd.values())} warp instructions executed")
+    for key, _ in order:
+        s = samples[key]
         f, l = key
         text = src.get(f, [])[l - 1].strip() if f in src and 0 < l <= len(src[f]) else ""
-        print(f"{100 * s / tot:5.1f}%  {execd[key]:>12d}  {f}:{l:<5d} {text[:90]}")
+        print(f"{100 * s / tot:5.1f}%  {execd[key]:>12d} ({100 * execd[key] / tot_exec:4.1f}%)  {f}:{l:<5d} {text[:80]}")
 
 
 def dump_line(rep: str, kernel: str, fname: str, line: int):
