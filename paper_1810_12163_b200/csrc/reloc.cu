@@ -1253,7 +1253,7 @@ SCR_DEV void divmod_w(int p, int W, float invW, int& x, int& y) {
 }
 
 #ifndef SCR_ICP_MINB
-#define SCR_ICP_MINB 3
+#define SCR_ICP_MINB 4
 #endif
 __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, SCR_ICP_MINB)
     k_icp_score(IcpArgs ia, FrameGeom g, FrameRefs fr, const Prim* __restrict__ prims, int nprims,
