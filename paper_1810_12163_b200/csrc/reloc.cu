@@ -1231,6 +1231,10 @@ bool icp_step(const double* tot, Pose* T) {
   return true;
 }
 
+#ifndef SCR_ICP_PIX
+#define SCR_ICP_PIX 3
+#endif
+constexpr int kIcpPix = SCR_ICP_PIX;  // live pixels per lane in flight in the association loop
 struct IcpPix {  // one live pixel of the association loop in flight
   int x, y, q, ui, vi;
   float dl, pw[3];
@@ -1357,16 +1361,16 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
         // lane (p, p + kIcpLanes) are in flight at once: both depth loads, then both model-map
         // loads, then both accumulated in pixel order (same per-lane order as one at a time).
         const int npx = Wl * Hl;
-        for (int p = lane_id; p < npx; p += 2 * kIcpLanes) {
-          IcpPix px[2];
+        for (int p = lane_id; p < npx; p += kIcpPix * kIcpLanes) {
+          IcpPix px[kIcpPix];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < kIcpPix; ++u) {
             const int pp = p + u * kIcpLanes;
             divmod_w(pp, Wl, invWl, px[u].x, px[u].y);
             px[u].dl = pp < npx ? __uint_as_float(tex[(px[u].y * fs) * g.W + px[u].x * fs].x) : 0.0f;
           }
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < kIcpPix; ++u) {
             px[u].q = -1;
             if (!depth_valid(px[u].dl)) continue;
             ++valid;
@@ -1392,11 +1396,11 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
             px[u].ui = ui;
             px[u].vi = vi;
           }
-          uint2 mv[2];
+          uint2 mv[kIcpPix];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) mv[u] = px[u].q >= 0 ? map[px[u].q] : make_uint2(0u, 0xffffffffu);
+          for (int u = 0; u < kIcpPix; ++u) mv[u] = px[u].q >= 0 ? map[px[u].q] : make_uint2(0u, 0xffffffffu);
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < kIcpPix; ++u) {
             if (mv[u].y == 0xffffffffu) continue;
             const float th = __uint_as_float(mv[u].x);
             const int ui = px[u].ui, vi = px[u].vi;
