@@ -41,8 +41,8 @@ struct FrameRefs {  // per-batch views of the packed frames
   const float4* gcam;
   const int* gslot;
   const int* gnm;
-  const int4* grec;
-  const uint4* gleaf;
+  const int4* grec;    // interleaved 32-B pixel records: grec[2 i] = {x|y<<16, depth, rgb|nm<<24, counts},
+  const uint4* gleaf;  // gleaf[2 i + 1] = 16-bit leaf ids (one sector per pixel)
   const double4* gcamd;
   const uint2* tex;
   int gmax, T;
@@ -271,8 +271,8 @@ __global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, F
         const int cc = static_cast<int>(mod_barrett32(buf.b6, 3u, m3));
         const uint64_t r0 = buf.b1, r1 = buf.b3, r2 = buf.b5;
         const int gc = cc == 0 ? g0 : (cc == 1 ? g1 : g2);
-        const int4 A0 = fr.grec[fbase + g0], A1 = fr.grec[fbase + g1], A2 = fr.grec[fbase + g2];
-        const uint4 Lc = fr.gleaf[fbase + gc];  // issued together with the records
+        const int4 A0 = fr.grec[2 * (fbase + g0)], A1 = fr.grec[2 * (fbase + g1)], A2 = fr.grec[2 * (fbase + g2)];
+        const uint4 Lc = fr.gleaf[2 * (fbase + gc) + 1];  // issued together with the records
         const uint32_t nm0 = static_cast<uint32_t>(A0.z) >> 24, nm1 = static_cast<uint32_t>(A1.z) >> 24,
                        nm2 = static_cast<uint32_t>(A2.z) >> 24;
         const bool full = nm0 != 0 && nm1 != 0 && nm2 != 0;  // all 7 raw values consumed
@@ -303,9 +303,9 @@ __global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, F
           c.slot = slot;
           c.owner_att = lane | (it << 5);
           c.g0 = g0; c.g1 = g1; c.g2 = g2;
-          c.m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), fr.gleaf[fbase + g0], p0);
-          c.m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), fr.gleaf[fbase + g1], p1);
-          c.m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), fr.gleaf[fbase + g2], p2);
+          c.m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), fr.gleaf[2 * (fbase + g0) + 1], p0);
+          c.m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), fr.gleaf[2 * (fbase + g1) + 1], p1);
+          c.m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), fr.gleaf[2 * (fbase + g2) + 1], p2);
         }
       } else {  // exact sequential replay of the attempt from the buffered stream
         int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0;
@@ -313,20 +313,20 @@ __global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, F
         uint4 L0, L1, L2;
         bool proceed = false;
         g0 = static_cast<int>(buf.draw(rng, G, mG, tG));
-        A0 = fr.grec[fbase + g0];
-        L0 = fr.gleaf[fbase + g0];
+        A0 = fr.grec[2 * (fbase + g0)];
+        L0 = fr.gleaf[2 * (fbase + g0) + 1];
         const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
         if (nm0 > 0) {
           p0 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
           g1 = static_cast<int>(buf.draw(rng, G, mG, tG));
-          A1 = fr.grec[fbase + g1];
-          L1 = fr.gleaf[fbase + g1];
+          A1 = fr.grec[2 * (fbase + g1)];
+          L1 = fr.gleaf[2 * (fbase + g1) + 1];
           const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
           if (nm1 > 0) {
             p1 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
             g2 = static_cast<int>(buf.draw(rng, G, mG, tG));
-            A2 = fr.grec[fbase + g2];
-            L2 = fr.gleaf[fbase + g2];
+            A2 = fr.grec[2 * (fbase + g2)];
+            L2 = fr.gleaf[2 * (fbase + g2) + 1];
             const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
             if (nm2 > 0) {
               p2 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
@@ -1629,7 +1629,7 @@ FrameRefs frame_refs(scr_scene s) {
   fr.gslot = s->ws.gslot;
   fr.gnm = s->ws.gnm;
   fr.grec = s->ws.grec;
-  fr.gleaf = s->ws.gleaf;
+  fr.gleaf = reinterpret_cast<const uint4*>(s->ws.grec);
   fr.gcamd = s->ws.gcamd;
   fr.tex = s->ws.tex;
   fr.gmax = s->ws.gmax;

@@ -187,9 +187,9 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
   gnm[gidx] = nm;
   // packed per-pixel record for hypothesis generation: pixel, depth, colour + |M(u)|,
   // per-tree mode counts (6 bits each, trees 0..4)
-  grec[gidx] = make_int4(px, static_cast<int>(c.x), static_cast<int>((c.y & 0xffffffu) | (min(nm, 255) << 24)),
+  grec[2 * gidx] = make_int4(px, static_cast<int>(c.x), static_cast<int>((c.y & 0xffffffu) | (min(nm, 255) << 24)),
                          static_cast<int>(counts));
-  gleaf[gidx] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+  reinterpret_cast<uint4*>(grec)[2 * gidx + 1] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   if (work) atomicAdd(&work[W_NODE_VISITS], static_cast<unsigned long long>(visits));
   const double dd = static_cast<double>(d);
   const double X = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
@@ -623,8 +623,7 @@ scr_status alloc_workspace(scr_scene s, int max_batch) {
   if ((st = dalloc(&w.gcam, B * w.gmax)) != SCR_OK) return st;
   if ((st = dalloc(&w.gslot, B * w.gmax * s->T)) != SCR_OK) return st;
   if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return st;
-  if ((st = dalloc(&w.grec, B * w.gmax)) != SCR_OK) return st;
-  if ((st = dalloc(&w.gleaf, B * w.gmax)) != SCR_OK) return st;
+  if ((st = dalloc(&w.grec, 2 * B * w.gmax)) != SCR_OK) return st;  // interleaved with the leaf ids
   if ((st = dalloc(&w.gcamd, B * w.gmax)) != SCR_OK) return st;
   if ((st = dalloc(&w.fidx, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return st;
