@@ -188,16 +188,19 @@ bool geometry_checks(double min_sq_dist, double rigidity_tol, const double4* gca
 
 // Per-warp queue of colour-check survivors, evaluated 32 at a time at full SIMD width.
 #ifndef SCR_HYPGEN_MINB
-#define SCR_HYPGEN_MINB 4  // resident CTAs per SM the register budget is sized for
+#define SCR_HYPGEN_MINB 2  // resident CTAs per SM the register budget is sized for (16 warps)
 #endif
-constexpr int kGenWarps = 4;
+#ifndef SCR_GEN_WARPS
+#define SCR_GEN_WARPS 8
+#endif
+constexpr int kGenWarps = SCR_GEN_WARPS;  // warps per generation CTA
 constexpr int kGenQ = 64;
 struct GenCand {
   int slot, owner_att;  // owner lane | attempt << 5
   int g0, g1, g2, m0, m1, m2;
 };
 
-__global__ void __launch_bounds__(128, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
+__global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
                                                    const uint64_t* __restrict__ seeds, int* __restrict__ slot_ctr,
                                                    Pose* __restrict__ hyp, int* __restrict__ hok,
                                                    int* __restrict__ hiters, unsigned long long* __restrict__ work) {
@@ -1687,7 +1690,7 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   SCR_CUDA(cudaMemsetAsync(w.hctr, 0, nA * sizeof(int), s->stream));  // per-frame slot counters
   const int gen_threads = std::min(p.n_max, kGenThreadsPerFrame);
   SCR_LAUNCH(s, K_HYPGEN,
-             (k_hypgen<<<dim3((gen_threads + 127) / 128, nA), 128, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds,
+             (k_hypgen<<<dim3((gen_threads + kGenWarps * 32 - 1) / (kGenWarps * 32), nA), kGenWarps * 32, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds,
                                                                                   w.hctr, w.hyp, w.hok, w.hiters,
                                                                                   wk)));
   SCR_LAUNCH(s, K_SAMPLES,
