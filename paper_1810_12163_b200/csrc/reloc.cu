@@ -105,6 +105,14 @@ struct RawBuf {  // next 7 raw outputs of the slot's stream
   }
 };
 
+// uniform_int by rejection (rng.hpp:50-56) with a precomputed Barrett reciprocal/threshold.
+SCR_DEV uint64_t draw_exact(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
+  for (;;) {
+    const uint64_t v = rng_next(r);
+    if (v >= thr) return mod_barrett(v, n, m);
+  }
+}
+
 // Mode index of the pick-th predicted mode of a pixel (union over trees in tree order),
 // branch-free from the record: 6-bit per-tree counts and 16-bit leaf ids (trees 0..4).
 SCR_DEV int mode_from_record(const int* lbase, uint32_t counts, uint4 lv, int pick) {
@@ -237,7 +245,6 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
   int slot = -1, it = 0;
   bool exhausted = false;
   Rng rng;
-  RawBuf buf;
   for (;;) {
     if (slot < 0 && !exhausted) {
       slot = atomicAdd(&slot_ctr[a], 1);
@@ -251,7 +258,6 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
         slot = -1;
       } else {
         rng = rng_stream(seeds[a], static_cast<uint64_t>(slot));
-        buf.fill(rng);
         it = 0;
         s_cur[wid][lane] = slot;
       }
@@ -261,10 +267,16 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
     bool push = false;
     GenCand c;
     if (slot >= 0 && it < gp.max_iters) {
-      // Fast path: none of the 7 buffered raw values can be rejected (every rejection
-      // threshold is < 2^32, so a non-zero high word always passes; otherwise replay the
-      // attempt exactly below). Pixel indices and the colour-check index are then known up
-      // front; only the mode the colour check needs is resolved before the check.
+      // The 7 raw values an attempt can consume are generated up front; the stream state
+      // before them is kept, so an attempt that consumes fewer (a pixel without modes) or
+      // must be replayed exactly rewinds instead of carrying values between attempts.
+      const Rng saved = rng;
+      RawBuf buf;
+      buf.fill(rng);
+      // Fast path: none of the 7 raw values can be rejected (every rejection threshold is
+      // < 2^32, so a non-zero high word always passes; otherwise replay the attempt exactly
+      // below). Pixel indices and the colour-check index are then known up front; only the
+      // mode the colour check needs is resolved before the check.
       const bool spec = fast && (buf.b0 >> 32) != 0 && (buf.b1 >> 32) != 0 && (buf.b2 >> 32) != 0 &&
                         (buf.b3 >> 32) != 0 && (buf.b4 >> 32) != 0 && (buf.b5 >> 32) != 0 && (buf.b6 >> 32) != 0;
       if (spec) {
@@ -289,14 +301,11 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
           const int pc = static_cast<int>(mod_barrett32(rc, nmc, s_m[nmc]));
           mcol = pv.col[mode_from_record(s_lbase, static_cast<uint32_t>(Ac.w), Lc, pc)];
         }
-        if (full) {
-          buf.fill(rng);
-        } else if (nm0 == 0) {
-          buf.pop(rng);
-        } else if (nm1 == 0) {
-          buf.pop(rng); buf.pop(rng); buf.pop(rng);
-        } else {
-          buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng); buf.pop(rng);
+        if (!full) {  // consumed 1, 3 or 5 raw values: rewind and advance by that many
+          rng = saved;
+          const int k = nm0 == 0 ? 1 : (nm1 == 0 ? 3 : 5);
+#pragma unroll 1
+          for (int j = 0; j < k; ++j) rng_next(rng);
         }
         if (full && colour_ok(static_cast<uint32_t>(Ac.z), mcol, gp.colour_thresh)) {
           const int p0 = static_cast<int>(mod_barrett32(r0, nm0, s_m[nm0]));
@@ -310,30 +319,31 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
           c.m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), fr.gleaf[2 * (fbase + g1) + 1], p1);
           c.m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), fr.gleaf[2 * (fbase + g2) + 1], p2);
         }
-      } else {  // exact sequential replay of the attempt from the buffered stream
+      } else {  // exact sequential replay of the attempt from the saved stream state
+        rng = saved;
         int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0;
         int4 A0, A1, A2;
         uint4 L0, L1, L2;
         bool proceed = false;
-        g0 = static_cast<int>(buf.draw(rng, G, mG, tG));
+        g0 = static_cast<int>(draw_exact(rng, G, mG, tG));
         A0 = fr.grec[2 * (fbase + g0)];
         L0 = fr.gleaf[2 * (fbase + g0) + 1];
         const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
         if (nm0 > 0) {
-          p0 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
-          g1 = static_cast<int>(buf.draw(rng, G, mG, tG));
+          p0 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
+          g1 = static_cast<int>(draw_exact(rng, G, mG, tG));
           A1 = fr.grec[2 * (fbase + g1)];
           L1 = fr.gleaf[2 * (fbase + g1) + 1];
           const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
           if (nm1 > 0) {
-            p1 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
-            g2 = static_cast<int>(buf.draw(rng, G, mG, tG));
+            p1 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
+            g2 = static_cast<int>(draw_exact(rng, G, mG, tG));
             A2 = fr.grec[2 * (fbase + g2)];
             L2 = fr.gleaf[2 * (fbase + g2) + 1];
             const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
             if (nm2 > 0) {
-              p2 = static_cast<int>(buf.draw(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
-              cc = static_cast<int>(buf.draw(rng, 3, m3, t3));
+              p2 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
+              cc = static_cast<int>(draw_exact(rng, 3, m3, t3));
               proceed = true;
             }
           }

@@ -8,6 +8,8 @@ import threading
 import numpy as np
 import pytest
 
+import oracle_ffi as of
+
 from world import OracleWorld, gpu_scene
 
 pytestmark = pytest.mark.gpu
@@ -89,3 +91,28 @@ def test_lane_is_read_only_and_sees_updates(adapted):
     for x, y in zip(again, root):
         assert bytes(x.pose) == bytes(y.pose)
     lane.close()
+
+
+def test_scenes_are_isolated(oracle, gpu_device, adapted):
+    """SURVEY.md §8(d) config 4 places several scenes on one GPU: each scene's state is its own,
+    so relocalising in one never changes another's results (interleaved calls)."""
+    import paper_1810_12163_b200 as P
+
+    w, s = adapted
+    w2 = OracleWorld(oracle, scene_seed=5, n_adapt=12, n_test=2)
+    s2 = gpu_scene(gpu_device, w2)
+    s2.integrate_frames(list(w2.D), list(w2.RGB), w2.adapt_poses)
+    s2.update_leaves_round_robin(s2.total_leaves)
+    p = P.ransac_params("fast")
+    a1 = s.relocalise_batch(w.Dt[:2], w.RGBt[:2], p, 1, [11, 12])
+    b1 = s2.relocalise_batch(w2.Dt, w2.RGBt, p, 1, [13, 14])
+    a2 = s.relocalise_batch(w.Dt[:2], w.RGBt[:2], p, 1, [11, 12])
+    for x, y in zip(a1, a2):
+        assert bytes(x.pose) == bytes(y.pose)
+    for i, r in enumerate(b1):
+        ref = oracle.relocalise(w2.forest, w2.state, w2.scene, w2.Dt[i], w2.RGBt[i], w2.k, of.ransac_params("fast"), 1,
+                                13 + i)
+        assert r.has_pose == ref.has_pose
+        if r.has_pose:
+            assert bytes(r.pose) == bytes(ref.pose)
+    s2.close()
