@@ -75,8 +75,6 @@ struct Workspace {
   int* gnm = nullptr;         // [cap * gmax] number of modes (union over trees)
   int4* grec = nullptr;       // [cap * gmax * 2] 32-B pixel records: {x|y<<16, depth bits, rgb | nm<<24,
                               // 6-bit counts of trees 0..4} then the 16-bit leaf ids of trees 0..7
-  uint4* gleaf = nullptr;     // unused (leaf ids live in the interleaved records)
-  double4* gcamd = nullptr;   // [cap * gmax] f64 camera point (backproject)
   // RANSAC (grown on demand)
   int nmax_cap = 0, ncull_cap = 0, samples_cap = 0;
   Pose* hyp = nullptr;        // [cap * nmax]

@@ -43,7 +43,6 @@ struct FrameRefs {  // per-batch views of the packed frames
   const int* gnm;
   const int4* grec;    // interleaved 32-B pixel records: grec[2 i] = {x|y<<16, depth, rgb|nm<<24, counts},
   const uint4* gleaf;  // gleaf[2 i + 1] = 16-bit leaf ids (one sector per pixel)
-  const double4* gcamd;
   const uint2* tex;
   int gmax, T;
 };
@@ -85,23 +84,11 @@ SCR_DEV uint64_t draw(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
   }
 }
 
-struct RawBuf {  // next 7 raw outputs of the slot's stream
+struct RawBuf {  // the 7 raw outputs one generation attempt can consume
   uint64_t b0, b1, b2, b3, b4, b5, b6;
   SCR_DEV void fill(Rng& r) {
     b0 = rng_next(r); b1 = rng_next(r); b2 = rng_next(r); b3 = rng_next(r);
     b4 = rng_next(r); b5 = rng_next(r); b6 = rng_next(r);
-  }
-  SCR_DEV uint64_t pop(Rng& r) {
-    const uint64_t v = b0;
-    b0 = b1; b1 = b2; b2 = b3; b3 = b4; b4 = b5; b5 = b6;
-    b6 = rng_next(r);
-    return v;
-  }
-  SCR_DEV uint64_t draw(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
-    for (;;) {
-      const uint64_t v = pop(r);
-      if (v >= thr) return mod_barrett(v, n, m);
-    }
   }
 };
 
@@ -147,35 +134,53 @@ SCR_DEV bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return k
 // check passed. Camera points come precomputed (f64 backprojection, K1).
 // Scalars and pointers only: passing the kernel-parameter structs by reference would force
 // copies of them into local memory.
-#ifdef SCR_GEOM_NOINLINE
-__device__ __noinline__
-#else
-SCR_DEV
-#endif
-bool geometry_checks(double min_sq_dist, double rigidity_tol, const double4* gcamd, const float4* gcam,
-                                             const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1, int m2,
-                                             Pose* T) {
+// Checks 2-3 (distances in f64) and Kabsch for a triplet whose colour
+// check passed. Camera points come from the pixel records (x, y, depth): an f32 estimate
+// for a conservative pre-filter, then the exact f64 backprojection (geometry.hpp:194-199,
+// the same operations as K1) only for triplets the pre-filter keeps.
+SCR_DEV void cam_point_f64(int4 rec, const FrameGeom& g, double out[3]) {
+  const int x = rec.x & 0xffff, y = rec.x >> 16;
+  const double dd = static_cast<double>(__int_as_float(rec.y));
+  out[0] = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
+  out[1] = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
+  out[2] = dd;
+}
+
+SCR_DEV bool geometry_checks(double min_sq_dist, double rigidity_tol, const int4* grec, const FrameGeom& g,
+                             float ifx, float ify, const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1,
+                             int m2, Pose* T) {
   const float4 w0 = geom[m0].q0, w1 = geom[m1].q0, w2 = geom[m2].q0;
-  {  // f32 pre-filter: rejects only triplets the exact f64 checks reject too. World points are
-     // the same f32 values; camera points are the f64 ones rounded to f32 (<= 4e-7 m at 6 m);
-     // the f32 distances are within 1e-5 m, far inside the 1e-3 m / 1e-3 m^2 margins.
-    const float4 f0 = gcam[g0], f1 = gcam[g1], f2 = gcam[g2];
-    const float4 wf[3] = {w0, w1, w2}, cf[3] = {f0, f1, f2};
+  const int4 r0 = grec[2 * g0], r1 = grec[2 * g1], r2 = grec[2 * g2];
+  {  // f32 pre-filter: rejects only triplets the exact f64 checks reject too (world points are
+     // the same f32 values; the f32 camera points are within 1e-5 m of the f64 ones, far
+     // inside the 1e-3 m / 1e-3 m^2 margins)
+    const int4 rr[3] = {r0, r1, r2};
+    float cf[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float d = __int_as_float(rr[k].y);
+      cf[k][0] = (static_cast<float>(rr[k].x & 0xffff) - g.cx) * d * ifx;
+      cf[k][1] = (static_cast<float>(rr[k].x >> 16) - g.cy) * d * ify;
+      cf[k][2] = d;
+    }
+    const float4 wf[3] = {w0, w1, w2};
     const float tolf = static_cast<float>(rigidity_tol) + 1e-3f;
     const float closef = static_cast<float>(min_sq_dist) - 1e-3f;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
       const float ax = wf[pa].x - wf[pb].x, ay = wf[pa].y - wf[pb].y, az = wf[pa].z - wf[pb].z;
-      const float bx = cf[pa].x - cf[pb].x, by = cf[pa].y - cf[pb].y, bz = cf[pa].z - cf[pb].z;
+      const float bx = cf[pa][0] - cf[pb][0], by = cf[pa][1] - cf[pb][1], bz = cf[pa][2] - cf[pb][2];
       const float dw2f = ax * ax + ay * ay + az * az, dc2f = bx * bx + by * by + bz * bz;
       if (dw2f < closef) return false;
       if (fabsf(sqrtf(dw2f) - sqrtf(dc2f)) > tolf) return false;
     }
   }
-  const double4 c0 = gcamd[g0], c1 = gcamd[g1], c2 = gcamd[g2];
   double w[9] = {w0.x, w0.y, w0.z, w1.x, w1.y, w1.z, w2.x, w2.y, w2.z};
-  double cm[9] = {c0.x, c0.y, c0.z, c1.x, c1.y, c1.z, c2.x, c2.y, c2.z};
+  double cm[9];
+  cam_point_f64(r0, g, cm);
+  cam_point_f64(r1, g, cm + 3);
+  cam_point_f64(r2, g, cm + 6);
   double dw2[3], dc2[3];
   bool close = false;
 #pragma unroll
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
   const uint64_t m3 = 0x5555555555555555ull, t3 = 1;  // floor((2^64-1)/3), 2^64 mod 3
   const bool fast = gp.fast != 0;
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  const float ifx = 1.0f / g.fx, ify = 1.0f / g.fy;  // f32 pre-filter only
   GenCand* q = s_q[wid];
   int qn = 0;  // warp-uniform queue length
   unsigned long long attempts_total = 0;
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
         att = e.owner_att >> 5;
         eslot = e.slot;
         if (s_cur[wid][owner] == eslot) {  // stale if the owner's slot was already resolved
-          pass = geometry_checks(gp.min_sq_dist, gp.rigidity_tol, fr.gcamd + fbase, fr.gcam + fbase, pv.geom, e.g0, e.g1, e.g2, e.m0, e.m1, e.m2, &T);
+          pass = geometry_checks(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, ifx, ify, pv.geom, e.g0, e.g1, e.g2, e.m0, e.m1, e.m2, &T);
           atomicSub(&s_pend[wid][owner], 1);
           if (pass) atomicMin(&s_best[wid][owner], att);
         }
@@ -1643,7 +1649,6 @@ FrameRefs frame_refs(scr_scene s) {
   fr.gnm = s->ws.gnm;
   fr.grec = s->ws.grec;
   fr.gleaf = reinterpret_cast<const uint4*>(s->ws.grec);
-  fr.gcamd = s->ws.gcamd;
   fr.tex = s->ws.tex;
   fr.gmax = s->ws.gmax;
   fr.T = s->T;

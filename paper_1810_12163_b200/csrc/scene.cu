@@ -134,7 +134,6 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
                                                 const int* __restrict__ gcount, const int* __restrict__ gpx,
                                                 int gmax, int* __restrict__ gslot, int* __restrict__ gnm,
                                                 float4* __restrict__ gcam, int4* __restrict__ grec,
-                                                uint4* __restrict__ gleaf, double4* __restrict__ gcamd,
                                                 const int* __restrict__ pcount, unsigned long long* __restrict__ work) {
   __shared__ short4 sspec[kFeatures];
   for (int i = threadIdx.x; i < kFeatures; i += blockDim.x) sspec[i] = fv.specs[i];
@@ -195,7 +194,6 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
   const double X = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
   const double Y = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
   gcam[gidx] = make_float4(static_cast<float>(X), static_cast<float>(Y), static_cast<float>(dd), 0.0f);
-  gcamd[gidx] = make_double4(X, Y, dd, 0.0);  // backproject (geometry.hpp:198) in f64 for the generation checks
 }
 
 // Debug: full 256-D feature vectors at given pixels (features.cpp:60-65).
@@ -624,7 +622,6 @@ scr_status alloc_workspace(scr_scene s, int max_batch) {
   if ((st = dalloc(&w.gslot, B * w.gmax * s->T)) != SCR_OK) return st;
   if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return st;
   if ((st = dalloc(&w.grec, 2 * B * w.gmax)) != SCR_OK) return st;  // interleaved with the leaf ids
-  if ((st = dalloc(&w.gcamd, B * w.gmax)) != SCR_OK) return st;
   if ((st = dalloc(&w.fidx, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.status, B)) != SCR_OK) return st;
@@ -867,7 +864,7 @@ void scr_scene_destroy(scr_scene s) {
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
-                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.gleaf, s->ws.gcamd, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
+                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
                   s->ws.ins_rank, s->ws.ins_total};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -970,7 +967,7 @@ scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_
   SCR_LAUNCH(s, K_LEAVES,
              (k_leaves<<<dim3((w.gmax + 127) / 128, n), 128, 0, s->stream>>>(
                  s->forest_view(), s->geom, w.tex, w.gcount, w.gpx, w.gmax, w.gslot, w.gnm, w.gcam, w.grec,
-                 w.gleaf, w.gcamd, s->d_count, work_ptr(s))));
+                 s->d_count, work_ptr(s))));
   SCR_CUDA(cudaGetLastError());
   return SCR_OK;
 }
