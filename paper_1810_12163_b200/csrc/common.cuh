@@ -24,6 +24,14 @@ constexpr int kLanes = 256;  // canonical ICP / score reduction width
 
 SCR_DEV bool depth_valid(float d) { return d > 0.0f && d <= kMaxValidDepth; }
 
+// std::lround for finite |x| < 2^23 (feature probe offsets, features.cpp:38-40): the
+// fractional part x - trunc(x) is exact in f32, so halves round away from zero exactly.
+SCR_DEV int lround_small(float x) {
+  float t = truncf(x);
+  if (fabsf(__fsub_rn(x, t)) >= 0.5f) t = __fadd_rn(t, copysignf(1.0f, x));
+  return static_cast<int>(t);
+}
+
 // ---- RNG: xoshiro256** / splitmix64 (reference rng.hpp:14-88) ----------------------
 struct Rng {
   uint64_t s0, s1, s2, s3;

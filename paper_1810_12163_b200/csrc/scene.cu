@@ -163,8 +163,8 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
       }
       ++visits;
       const short4 sp = sspec[nd.z];
-      const int qx = x + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.x), d)));
-      const int qy = y + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.y), d)));
+      const int qx = x + lround_small(__fdiv_rn(static_cast<float>(sp.x), d));
+      const int qy = y + lround_small(__fdiv_rn(static_cast<float>(sp.y), d));
       uint2 pt = make_uint2(0u, 0u);
       if (qx >= 0 && qx < W && qy >= 0 && qy < H) pt = T[qy * W + qx];
       float v;
@@ -211,8 +211,8 @@ __global__ void k_features(ForestView fv, FrameGeom g, const uint2* __restrict__
     out[static_cast<size_t>(i) * kFeatures + k] = __int_as_float(0x7fc00000);
     return;
   }
-  const int qx = x + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.x), d)));
-  const int qy = y + static_cast<int>(lroundf(__fdiv_rn(static_cast<float>(sp.y), d)));
+  const int qx = x + lround_small(__fdiv_rn(static_cast<float>(sp.x), d));
+  const int qy = y + lround_small(__fdiv_rn(static_cast<float>(sp.y), d));
   uint2 pt = make_uint2(0u, 0u);
   if (qx >= 0 && qx < W && qy >= 0 && qy < H) pt = tex[qy * W + qx];
   float v;
