@@ -69,7 +69,27 @@ __global__ void k_pack(const float* __restrict__ depth_base, const uint8_t* __re
   const float* dp = depth_base + src * WH;
   const uint8_t* cp = rgb_base + src * WH * 3;
   uint2* out = tex + static_cast<size_t>(f) * WH;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < WH; p += gridDim.x * blockDim.x) {
+  const int stride = gridDim.x * blockDim.x;
+  if ((WH & 3) == 0) {  // 4 pixels per thread: 16-B depth, 12-B colour, 32-B texel stores
+    const float4* d4 = reinterpret_cast<const float4*>(dp);
+    const uint3* c3 = reinterpret_cast<const uint3*>(cp);
+    uint4* o4 = reinterpret_cast<uint4*>(out);
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (WH >> 2); q += stride) {
+      const float4 d = d4[q];
+      const uint3 c = c3[q];  // bytes r0 g0 b0 r1 | g1 b1 r2 g2 | b2 r3 g3 b3
+      const uint32_t rgb0 = c.x & 0xffffffu;
+      const uint32_t rgb1 = (c.x >> 24) | ((c.y & 0xffffu) << 8);
+      const uint32_t rgb2 = (c.y >> 16) | ((c.z & 0xffu) << 16);
+      const uint32_t rgb3 = c.z >> 8;
+      const bool v0 = depth_valid(d.x), v1 = depth_valid(d.y), v2 = depth_valid(d.z), v3 = depth_valid(d.w);
+      o4[2 * q] = make_uint4(v0 ? __float_as_uint(d.x) : 0u, v0 ? (rgb0 | (1u << 24)) : 0u,
+                             v1 ? __float_as_uint(d.y) : 0u, v1 ? (rgb1 | (1u << 24)) : 0u);
+      o4[2 * q + 1] = make_uint4(v2 ? __float_as_uint(d.z) : 0u, v2 ? (rgb2 | (1u << 24)) : 0u,
+                                 v3 ? __float_as_uint(d.w) : 0u, v3 ? (rgb3 | (1u << 24)) : 0u);
+    }
+    return;
+  }
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < WH; p += stride) {
     const float d = dp[p];
     uint2 t = make_uint2(0u, 0u);
     if (depth_valid(d)) {
