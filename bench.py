@@ -375,7 +375,7 @@ def run_ours(args):
         lane.run_cascade_batch([dnp[j] for j in e2e_idx], [cnp[j] for j in e2e_idx], cfg, e2e_seeds)
     if dist is not None:
         dist.barrier()
-    e2e_steps = max(len(lanes), args.steps // 2)
+    e2e_steps = max(len(lanes), args.steps)
     e2e_ms = max_over_ranks(
         run_lanes(lambda lane, st: lane.run_cascade_batch([dnp[j] for j in e2e_idx], [cnp[j] for j in e2e_idx], cfg,
                                                           e2e_seeds), e2e_steps), dist, dev_t)
@@ -581,13 +581,13 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=256, help="frames per step per GPU")
+    ap.add_argument("--batch", type=int, default=128, help="frames per step per GPU")
     ap.add_argument("--test-frames", type=int, default=1024, help="resident test frames per GPU")
     ap.add_argument("--adapt-frames", type=int, default=1000)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-batch", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--lanes", type=int, default=2, help="relocalisation lanes (streams + host threads) per GPU")
+    ap.add_argument("--lanes", type=int, default=4, help="relocalisation lanes (streams + host threads) per GPU")
     ap.add_argument("--profile-window", action="store_true",
                     help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
     args = ap.parse_args(argv)

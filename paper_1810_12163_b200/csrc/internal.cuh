@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -64,6 +65,14 @@ struct PredView {
 // Per-batch device workspace (frames are addressed by workspace slot f in [0, cap)).
 struct Workspace {
   int cap = 0;    // frames
+  // per-call staging, allocated once: device results, pinned host mirrors, stage events
+  scr_result* d_res = nullptr;  // [cap]
+  scr_result* h_res = nullptr;  // pinned [cap]
+  int* h_idx = nullptr;         // pinned [cap] stage frame list
+  int* h_fsidx = nullptr;       // pinned [cap] frameset indices of a call
+  uint64_t* h_seeds = nullptr;  // pinned [cap]
+  cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev_upload = nullptr;
   int gmax = 0;   // grid pixels per frame
   float* depth = nullptr;     // staging for host uploads [cap * WH]
   uint8_t* rgb = nullptr;     // [cap * WH * 3]
@@ -119,6 +128,10 @@ struct Workspace {
 struct scr_device_s {
   int ordinal = 0;
   int sm_count = 148;
+  // host->device frame uploads of every scene/lane on this GPU go through one copy stream,
+  // each call's frames enqueued contiguously: one lane's upload overlaps the others' kernels
+  cudaStream_t copy = nullptr;
+  std::mutex copy_mu;
 };
 
 struct scr_scene_s {

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -1860,52 +1861,42 @@ uint64_t stage_seed(uint64_t seed, int stage) { return seed + static_cast<uint64
 // run_cascade for frames packed in workspace slots 0..n-1.
 scr_status run_cascade(scr_scene s, int n, const scr_ransac_params* stages, const int32_t* modes, const double* thr,
                        int nstages, const uint64_t* seeds, scr_result* out) {
+  // Host control between stages only: stage i+1 takes the frames whose stage-i score exceeds
+  // the threshold. Staging buffers are pinned and allocated once per
+  // workspace, so a call makes no allocation and no implicit device synchronisation.
   Workspace& w = s->ws;
   std::vector<int> active(n);
   for (int i = 0; i < n; ++i) active[i] = i;
-  std::vector<int> act_idx;
-  std::vector<uint64_t> act_seed;
   std::vector<scr_result> res(n);
-  scr_result* d_res = nullptr;
-  SCR_CUDA(cudaMalloc(&d_res, std::max(1, n) * sizeof(scr_result)));
-  cudaEvent_t ev0, ev1;
-  cudaEventCreate(&ev0);
-  cudaEventCreate(&ev1);
   for (int st = 0; st < nstages && !active.empty(); ++st) {
     const int nA = static_cast<int>(active.size());
-    act_seed.resize(nA);
-    for (int i = 0; i < nA; ++i) act_seed[i] = stage_seed(seeds[active[i]], st);
-    SCR_CUDA(cudaMemcpyAsync(w.fidx, active.data(), nA * sizeof(int), cudaMemcpyHostToDevice, s->stream));
-    SCR_CUDA(cudaMemcpyAsync(w.seeds, act_seed.data(), nA * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream));
-    cudaEventRecord(ev0, s->stream);
-    scr_status rs = run_stage(s, nA, stages[st], modes[st], d_res);
-    if (rs != SCR_OK) {
-      cudaFree(d_res);
-      return rs;
+    for (int i = 0; i < nA; ++i) {
+      w.h_idx[i] = active[i];
+      w.h_seeds[i] = stage_seed(seeds[active[i]], st);
     }
-    cudaEventRecord(ev1, s->stream);
-    std::vector<scr_result> sr(nA);
-    SCR_CUDA(cudaMemcpyAsync(sr.data(), d_res, nA * sizeof(scr_result), cudaMemcpyDeviceToHost, s->stream));
+    SCR_CUDA(cudaMemcpyAsync(w.fidx, w.h_idx, nA * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    SCR_CUDA(cudaMemcpyAsync(w.seeds, w.h_seeds, nA * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream));
+    cudaEventRecord(w.ev_stage[0], s->stream);
+    SCR_TRY(run_stage(s, nA, stages[st], modes[st], w.d_res));
+    cudaEventRecord(w.ev_stage[1], s->stream);
+    SCR_CUDA(cudaMemcpyAsync(w.h_res, w.d_res, nA * sizeof(scr_result), cudaMemcpyDeviceToHost, s->stream));
     SCR_CUDA(cudaStreamSynchronize(s->stream));
     prof_flush(s);
     float ms = 0.0f;
-    cudaEventElapsedTime(&ms, ev0, ev1);
+    cudaEventElapsedTime(&ms, w.ev_stage[0], w.ev_stage[1]);
     std::vector<int> next;
     for (int i = 0; i < nA; ++i) {
       const int f = active[i];
       float keep[4];
       std::memcpy(keep, res[f].stage_ms, sizeof(keep));
-      res[f] = sr[i];
+      res[f] = w.h_res[i];
       std::memcpy(res[f].stage_ms, keep, sizeof(keep));
       if (st < 4) res[f].stage_ms[st] = ms / nA;
       res[f].stage_used = st;
-      if (st < nstages - 1 && !(sr[i].score <= thr[st])) next.push_back(f);
+      if (st < nstages - 1 && !(w.h_res[i].score <= thr[st])) next.push_back(f);
     }
     active.swap(next);
   }
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
-  cudaFree(d_res);
   std::memcpy(out, res.data(), n * sizeof(scr_result));
   return SCR_OK;
 }
@@ -1947,12 +1938,20 @@ scr_status scr_cascade_batch(scr_scene s, const scr_frame* frames, int n, const 
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
   for (int b0 = 0; b0 < n; b0 += s->ws.cap) {
     const int nb = std::min(s->ws.cap, n - b0);
-    for (int i = 0; i < nb; ++i) {
-      const scr_frame& fr = frames[b0 + i];
-      if (!fr.depth || !fr.rgb) return SCR_E_ARG;
-      SCR_CUDA(cudaMemcpyAsync(s->ws.depth + i * WH, fr.depth, WH * sizeof(float), cudaMemcpyHostToDevice, s->stream));
-      SCR_CUDA(cudaMemcpyAsync(s->ws.rgb + i * WH * 3, fr.rgb, WH * 3, cudaMemcpyHostToDevice, s->stream));
+    for (int i = 0; i < nb; ++i)
+      if (!frames[b0 + i].depth || !frames[b0 + i].rgb) return SCR_E_ARG;
+    {  // this call's frames, contiguous on the device's copy stream (staging is free: the
+       // previous call on this lane synchronised its stream)
+      std::lock_guard<std::mutex> lk(s->dev->copy_mu);
+      for (int i = 0; i < nb; ++i) {
+        const scr_frame& fr = frames[b0 + i];
+        SCR_CUDA(cudaMemcpyAsync(s->ws.depth + i * WH, fr.depth, WH * sizeof(float), cudaMemcpyHostToDevice,
+                                 s->dev->copy));
+        SCR_CUDA(cudaMemcpyAsync(s->ws.rgb + i * WH * 3, fr.rgb, WH * 3, cudaMemcpyHostToDevice, s->dev->copy));
+      }
+      SCR_CUDA(cudaEventRecord(s->ws.ev_upload, s->dev->copy));
     }
+    SCR_CUDA(cudaStreamWaitEvent(s->stream, s->ws.ev_upload, 0));
     SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, nb));
     SCR_TRY(run_cascade(s, nb, stages, modes, thr, nstages, seeds + b0, out + b0));
   }
@@ -1981,7 +1980,9 @@ scr_status scr_cascade_frameset(scr_scene s, scr_frameset fs, const int32_t* idx
     if (idx[i] < 0 || idx[i] >= fs->cap) return SCR_E_ARG;
   for (int b0 = 0; b0 < n; b0 += s->ws.cap) {
     const int nb = std::min(s->ws.cap, n - b0);
-    SCR_CUDA(cudaMemcpyAsync(s->ws.status, idx + b0, nb * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    // the previous chunk's copy from h_fsidx completed: run_cascade synchronised the stream
+    std::memcpy(s->ws.h_fsidx, idx + b0, nb * sizeof(int));
+    SCR_CUDA(cudaMemcpyAsync(s->ws.status, s->ws.h_fsidx, nb * sizeof(int), cudaMemcpyHostToDevice, s->stream));
     SCR_TRY(pack_frames(s, fs->depth, fs->rgb, s->ws.status, nb));
     SCR_TRY(run_cascade(s, nb, stages, modes, thr, nstages, seeds + b0, out + b0));
   }

@@ -646,6 +646,14 @@ scr_status alloc_workspace(scr_scene s, int max_batch) {
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.status, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.hctr, B)) != SCR_OK) return st;
+  if ((st = dalloc(&w.d_res, B)) != SCR_OK) return st;
+  SCR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w.h_res), B * sizeof(scr_result)));
+  SCR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w.h_idx), B * sizeof(int)));
+  SCR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w.h_fsidx), B * sizeof(int)));
+  SCR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w.h_seeds), B * sizeof(uint64_t)));
+  SCR_CUDA(cudaEventCreate(&w.ev_stage[0]));
+  SCR_CUDA(cudaEventCreate(&w.ev_stage[1]));
+  SCR_CUDA(cudaEventCreateWithFlags(&w.ev_upload, cudaEventDisableTiming));
   if ((st = dalloc(&w.ins_cnt, L)) != SCR_OK) return st;
   if ((st = dalloc(&w.ins_off, L + 1)) != SCR_OK) return st;
   if ((st = dalloc(&w.ins_cur, L)) != SCR_OK) return st;
@@ -701,12 +709,26 @@ scr_status scr_device_open(int ordinal, scr_device* out) {
   SCR_CUDA(cudaSetDevice(ordinal));
   scr_device d = new scr_device_s();
   d->ordinal = ordinal;
+  {
+    const cudaError_t e = cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete d;
+      return cuda_fail(e, "cudaStreamCreate(copy)");
+    }
+  }
   cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, ordinal);
   *out = d;
   return SCR_OK;
 }
 
-void scr_device_close(scr_device d) { delete d; }
+void scr_device_close(scr_device d) {
+  if (!d) return;
+  if (d->copy) {
+    cudaSetDevice(d->ordinal);
+    cudaStreamDestroy(d->copy);
+  }
+  delete d;
+}
 
 scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const scr_forest_params* fp,
                             const scr_intrinsics* k, uint64_t adapt_seed, int max_batch, scr_scene* out) {
@@ -879,6 +901,12 @@ void scr_scene_destroy(scr_scene s) {
     s->d_count = nullptr; s->d_geom = nullptr; s->d_col = nullptr; s->d_cov = nullptr; s->d_prims = nullptr;
   }
   if (s->published) cudaEventDestroy(s->published);
+  for (cudaEvent_t e : {s->ws.ev_stage[0], s->ws.ev_stage[1], s->ws.ev_upload})
+    if (e) cudaEventDestroy(e);
+  for (void* h : {static_cast<void*>(s->ws.h_res), static_cast<void*>(s->ws.h_idx), static_cast<void*>(s->ws.h_fsidx),
+                  static_cast<void*>(s->ws.h_seeds)})
+    if (h) cudaFreeHost(h);
+  if (s->ws.d_res) cudaFree(s->ws.d_res);
   void* ptrs[] = {s->d_nodes, s->d_specs, s->d_entries, s->d_seen, s->d_count, s->d_geom, s->d_col, s->d_cov,
                   s->d_prims, s->ws.depth, s->ws.rgb, s->ws.tex, s->ws.gcount, s->ws.gpx, s->ws.gcam, s->ws.gslot,
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
