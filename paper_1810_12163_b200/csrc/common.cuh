@@ -681,6 +681,14 @@ SCR_DEV void hit_normal(const Prim* prims, int prim, int face, const float p[3],
   }
 }
 
+// Work-counter update aggregated over the active lanes of the warp (one atomic per warp, so
+// the in-library profiler does not serialise the kernels it measures). v < 2^32 per lane.
+SCR_DEV void work_add(unsigned long long* work, int id, unsigned v) {
+  const unsigned mask = __activemask();
+  const unsigned s = __reduce_add_sync(mask, v);
+  if (static_cast<int>(threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(&work[id], static_cast<unsigned long long>(s));
+}
+
 // ---- warp reductions in the canonical xor-butterfly order ------------------------------
 SCR_DEV double warp_sum_xor(double v) {
 #pragma unroll

@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
       __syncwarp();
     }
   }
-  if (work) atomicAdd(&work[W_GEN_ATTEMPTS], attempts_total);
+  if (work) work_add(work, W_GEN_ATTEMPTS, static_cast<unsigned>(attempts_total));
 }
 
 // Sample batch k of frame a: eta draws of uniform_int(G) from Rng::stream(seed, nmax + k).
@@ -767,9 +767,9 @@ __global__ void __launch_bounds__(256) k_energy_grouped(EnergyArgs ea, FrameRefs
     if (ea.kb == 0) ea.out[idx] = E;
     else ea.out[idx * ea.kb + b] = E;
   }
-  if (work && sevals) {
-    atomicAdd(&work[W_MODE_EVALS], evals);
-    atomicAdd(&work[W_SAMPLE_EVALS], sevals);
+  if (work) {
+    work_add(work, W_MODE_EVALS, static_cast<unsigned>(evals));
+    work_add(work, W_SAMPLE_EVALS, static_cast<unsigned>(sevals));
   }
 }
 
@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmAr
     lm_accum(H, x, pv.geom[mi], la.use_cov != 0, acc, true);
     ++terms;
   }
-  if (work) atomicAdd(&work[W_LM_TERMS], static_cast<unsigned long long>(terms));
+  if (work) work_add(work, W_LM_TERMS, static_cast<unsigned>(terms));
 #pragma unroll
   for (int k = 0; k < 28; ++k) acc[k] = warp_sum_xor(acc[k]);
   ls.need_assoc = 0;
@@ -1363,7 +1363,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
         if (h.prim >= 0 && h.t <= kRenderMaxDepth) v = make_uint2(__float_as_uint(h.t), h.prim | (h.face << 16));
         map[p] = v;
       }
-      if (work) atomicAdd(&work[W_RAY_PRIMS], tests);
+      if (work) work_add(work, W_RAY_PRIMS, static_cast<unsigned>(tests));
       cluster.sync();  // map complete and visible to the whole cluster
       const int iters = level == 2 ? 10 : (level == 1 ? 5 : 4);
       for (int it = 0; it < iters; ++it) {
@@ -1557,7 +1557,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       ++mutual;
       sum = __fadd_rn(sum, fabsf(__fsub_rn(dl, h.t)));
     }
-    if (work) atomicAdd(&work[W_RAY_PRIMS], tests);
+    if (work) work_add(work, W_RAY_PRIMS, static_cast<unsigned>(tests));
     cta_reduce_f32<1>(&sum, red, part);
     const int mutual_c = cta_isum(mutual, ired);
     const int synth_c = cta_isum(synth, ired);

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(128) k_leaves(ForestView fv, FrameGeom g, cons
   grec[2 * gidx] = make_int4(px, static_cast<int>(c.x), static_cast<int>((c.y & 0xffffffu) | (min(nm, 255) << 24)),
                          static_cast<int>(counts));
   reinterpret_cast<uint4*>(grec)[2 * gidx + 1] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-  if (work) atomicAdd(&work[W_NODE_VISITS], static_cast<unsigned long long>(visits));
+  if (work) work_add(work, W_NODE_VISITS, static_cast<unsigned>(visits));
   const double dd = static_cast<double>(d);
   const double X = ((static_cast<double>(x) - g.dcx) * dd) / g.dfx;
   const double Y = ((static_cast<double>(y) - g.dcy) * dd) / g.dfy;
