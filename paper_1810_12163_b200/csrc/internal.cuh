@@ -77,6 +77,7 @@ struct Workspace {
   float* depth = nullptr;     // staging for host uploads [cap * WH]
   uint8_t* rgb = nullptr;     // [cap * WH * 3]
   uint2* tex = nullptr;       // packed texels [cap * WH]: {depth or 0, rgb|valid<<24}
+  float* dplane = nullptr;    // live depth (or 0) per ICP pyramid level, dense: [cap][WH + WH/4 + WH/16]
   int* gcount = nullptr;      // [cap]
   int* gpx = nullptr;         // [cap * gmax] packed x | y << 16
   float4* gcam = nullptr;     // [cap * gmax] camera point (f32 of the f64 backprojection)

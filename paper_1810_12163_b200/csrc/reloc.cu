@@ -45,6 +45,7 @@ struct FrameRefs {  // per-batch views of the packed frames
   const int4* grec;    // interleaved 32-B pixel records: grec[2 i] = {x|y<<16, depth, rgb|nm<<24, counts},
   const uint4* gleaf;  // gleaf[2 i + 1] = 16-bit leaf ids (one sector per pixel)
   const uint2* tex;
+  const float* dplane;  // per frame: level-0, level-1, level-2 live depth planes
   int gmax, T;
 };
 
@@ -1305,7 +1306,8 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
   if (c >= ncand[a]) return;  // uniform over the cluster
   const int f = fr.fidx[a];
   const size_t cidx = static_cast<size_t>(a) * ia.cand_stride + c;
-  const uint2* tex = fr.tex + static_cast<size_t>(f) * g.W * g.H;
+  const size_t WHf = static_cast<size_t>(g.W) * g.H;
+  const float* dpl0 = fr.dplane + static_cast<size_t>(f) * (WHf + WHf / 4 + WHf / 16);
   uint2* map = maps + static_cast<size_t>(jl) * ia.map_stride;
   if (threadIdx.x == 0) Ts = cand[cidx];
   __syncthreads();
@@ -1319,6 +1321,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
     for (int level = 2; level >= 0; --level) {
       const int fs = 1 << level;
       const int Wl = g.W / fs, Hl = g.H / fs;
+      const float* dpl = dpl0 + (level == 0 ? 0 : (level == 1 ? WHf : WHf + WHf / 4));  // dense level plane
       const float fxl = static_cast<float>(g.dfx / fs), fyl = static_cast<float>(g.dfy / fs);
       const float cxl = static_cast<float>(g.dcx / fs), cyl = static_cast<float>(g.dcy / fs);
       const Pose Tref = Ts;
@@ -1387,7 +1390,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
           for (int u = 0; u < kIcpPix; ++u) {
             const int pp = p + u * kIcpLanes;
             divmod_w(pp, Wl, invWl, px[u].x, px[u].y);
-            px[u].dl = pp < npx ? __uint_as_float(tex[(px[u].y * fs) * g.W + px[u].x * fs].x) : 0.0f;
+            px[u].dl = pp < npx ? dpl[pp] : 0.0f;
           }
 #pragma unroll
           for (int u = 0; u < kIcpPix; ++u) {
@@ -1552,7 +1555,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       }
       if (h.prim < 0 || !(h.t <= kRenderMaxDepth) || !depth_valid(h.t)) continue;
       ++synth;
-      const float dl = __uint_as_float(tex[p].x);
+      const float dl = dpl0[p];
       if (!depth_valid(dl)) continue;
       ++mutual;
       sum = __fadd_rn(sum, fabsf(__fsub_rn(dl, h.t)));
@@ -1651,6 +1654,7 @@ FrameRefs frame_refs(scr_scene s) {
   fr.grec = s->ws.grec;
   fr.gleaf = reinterpret_cast<const uint4*>(s->ws.grec);
   fr.tex = s->ws.tex;
+  fr.dplane = s->ws.dplane;
   fr.gmax = s->ws.gmax;
   fr.T = s->T;
   return fr;

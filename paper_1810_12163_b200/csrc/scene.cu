@@ -62,15 +62,23 @@ scr_status cuda_fail(cudaError_t e, const char* what) {
 // Packs f32 depth + RGB8 into an 8-byte texel {depth or 0, r | g<<8 | b<<16 | valid<<24}.
 // Invalid pixels carry zero depth and zero colour, which is exactly what a probe
 // landing on them contributes (features.cpp:43-56), so K1 needs one load per probe.
+// Also writes the live depth planes of the ICP pyramid (levels 0-2, subsampled at (x f, y f)
+// like the association reads them), dense f32 with 0 for invalid depth.
 __global__ void k_pack(const float* __restrict__ depth_base, const uint8_t* __restrict__ rgb_base,
-                       const int* __restrict__ idx, int WH, uint2* __restrict__ tex) {
+                       const int* __restrict__ idx, int W, int H, uint2* __restrict__ tex,
+                       float* __restrict__ dplane) {
+  const int WH = W * H;
   const int f = blockIdx.y;
   const size_t src = idx ? static_cast<size_t>(idx[f]) : static_cast<size_t>(f);
   const float* dp = depth_base + src * WH;
   const uint8_t* cp = rgb_base + src * WH * 3;
   uint2* out = tex + static_cast<size_t>(f) * WH;
+  float* dl0 = dplane + static_cast<size_t>(f) * (WH + WH / 4 + WH / 16);
+  float* dl1 = dl0 + WH;
+  float* dl2 = dl1 + WH / 4;
+  const int W1 = W / 2, W2 = W / 4;
   const int stride = gridDim.x * blockDim.x;
-  if ((WH & 3) == 0) {  // 4 pixels per thread: 16-B depth, 12-B colour, 32-B texel stores
+  if ((W & 3) == 0 && (H & 3) == 0) {  // 4 pixels per thread: 16-B depth, 12-B colour, 32-B texel stores
     const float4* d4 = reinterpret_cast<const float4*>(dp);
     const uint3* c3 = reinterpret_cast<const uint3*>(cp);
     uint4* o4 = reinterpret_cast<uint4*>(out);
@@ -86,6 +94,11 @@ __global__ void k_pack(const float* __restrict__ depth_base, const uint8_t* __re
                              v1 ? __float_as_uint(d.y) : 0u, v1 ? (rgb1 | (1u << 24)) : 0u);
       o4[2 * q + 1] = make_uint4(v2 ? __float_as_uint(d.z) : 0u, v2 ? (rgb2 | (1u << 24)) : 0u,
                                  v3 ? __float_as_uint(d.w) : 0u, v3 ? (rgb3 | (1u << 24)) : 0u);
+      const float4 lv = make_float4(v0 ? d.x : 0.0f, v1 ? d.y : 0.0f, v2 ? d.z : 0.0f, v3 ? d.w : 0.0f);
+      reinterpret_cast<float4*>(dl0)[q] = lv;
+      const int p0 = 4 * q, y = p0 / W, x = p0 - y * W;  // x % 4 == 0
+      if ((y & 1) == 0) reinterpret_cast<float2*>(dl1)[((y >> 1) * W1 + (x >> 1)) >> 1] = make_float2(lv.x, lv.z);
+      if ((y & 3) == 0) dl2[(y >> 2) * W2 + (x >> 2)] = lv.x;
     }
     return;
   }
@@ -98,6 +111,11 @@ __global__ void k_pack(const float* __restrict__ depth_base, const uint8_t* __re
             (static_cast<uint32_t>(cp[3 * p + 2]) << 16) | (1u << 24);
     }
     out[p] = t;
+    const float lv = __uint_as_float(t.x);
+    dl0[p] = lv;
+    const int y = p / W, x = p - y * W;
+    if ((x & 1) == 0 && (y & 1) == 0 && (x >> 1) < W1 && (y >> 1) < H / 2) dl1[(y >> 1) * W1 + (x >> 1)] = lv;
+    if ((x & 3) == 0 && (y & 3) == 0 && (x >> 2) < W2 && (y >> 2) < H / 4) dl2[(y >> 2) * W2 + (x >> 2)] = lv;
   }
 }
 
@@ -636,6 +654,7 @@ scr_status alloc_workspace(scr_scene s, int max_batch) {
   if ((st = dalloc(&w.depth, B * WH)) != SCR_OK) return st;
   if ((st = dalloc(&w.rgb, B * WH * 3)) != SCR_OK) return st;
   if ((st = dalloc(&w.tex, B * WH)) != SCR_OK) return st;
+  if ((st = dalloc(&w.dplane, B * (WH + WH / 4 + WH / 16))) != SCR_OK) return st;
   if ((st = dalloc(&w.gcount, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.gpx, B * w.gmax)) != SCR_OK) return st;
   if ((st = dalloc(&w.gcam, B * w.gmax)) != SCR_OK) return st;
@@ -912,7 +931,7 @@ void scr_scene_destroy(scr_scene s) {
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
-                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
+                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.dplane, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
                   s->ws.ins_rank, s->ws.ins_total};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1010,7 +1029,8 @@ scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_
   Workspace& w = s->ws;
   const int W = s->k.width, H = s->k.height, WH = W * H;
   const int pack_blocks = (WH + 1023) / 1024 < 64 ? (WH + 1023) / 1024 : 64;
-  SCR_LAUNCH(s, K_PACK, (k_pack<<<dim3(pack_blocks, n), 256, 0, s->stream>>>(depth_base, rgb_base, d_idx, WH, w.tex)));
+  SCR_LAUNCH(s, K_PACK, (k_pack<<<dim3(pack_blocks, n), 256, 0, s->stream>>>(depth_base, rgb_base, d_idx, W, H, w.tex,
+                                                                           w.dplane)));
   SCR_LAUNCH(s, K_GRID, (k_grid<<<n, 1024, 0, s->stream>>>(w.tex, W, H, w.gmax, w.gcount, w.gpx)));
   SCR_LAUNCH(s, K_LEAVES,
              (k_leaves<<<dim3((w.gmax + 127) / 128, n), 128, 0, s->stream>>>(
