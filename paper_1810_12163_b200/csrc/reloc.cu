@@ -1456,37 +1456,28 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
         // itself. Partials alternate between two buffers, so a CTA that runs ahead into the
         // next iteration never overwrites what a slower CTA is still reading.
         double* pb = part2[pbuf];
-        int* ib = ipart2[pbuf];
-        cta_reduce_f32<28>(acc, red, pb);
-        const int inl_c = cta_isum(inl, ired);
-        const int valid_c = cta_isum(valid, ired);
-        if (threadIdx.x == 0) {
-          ib[0] = inl_c;
-          ib[1] = valid_c;
-        }
+        // the inlier / valid counts ride along as two more values (exact small integers)
+        float vals[30];
+#pragma unroll
+        for (int k = 0; k < 28; ++k) vals[k] = acc[k];
+        vals[28] = static_cast<float>(inl);
+        vals[29] = static_cast<float>(valid);
+        cta_reduce_f32<30>(vals, red, pb);
         cluster.sync();  // all CTA partials of this iteration written
-        if (threadIdx.x < 28) {
+        if (threadIdx.x < 30) {
           double tot = cluster.map_shared_rank(pb, 0)[threadIdx.x];
           for (int r = 1; r < kIcpCtas; ++r) tot = tot + cluster.map_shared_rank(pb, r)[threadIdx.x];
           red[0][threadIdx.x] = tot;
         }
-        if (threadIdx.x == 32) {
-          int inl_t = 0, valid_t = 0;
-          for (int r = 0; r < kIcpCtas; ++r) {
-            inl_t += cluster.map_shared_rank(ib, r)[0];
-            valid_t += cluster.map_shared_rank(ib, r)[1];
-          }
-          ired[0] = inl_t;
-          ired[1] = valid_t;
-        }
         __syncthreads();
         if (threadIdx.x == 0) {
           const double* tot = red[0];
-          const int inl_t = ired[0];
-          if (work && rank == 0) atomicAdd(&work[W_ICP_TERMS], static_cast<unsigned long long>(ired[1]));
+          const int inl_t = static_cast<int>(tot[28]);
+          const int valid_t = static_cast<int>(tot[29]);
+          if (work && rank == 0) atomicAdd(&work[W_ICP_TERMS], static_cast<unsigned long long>(valid_t));
           if (level == 0) {
             lstat[0] = inl_t;
-            lstat[1] = ired[1];
+            lstat[1] = valid_t;
             lstat_r2 = tot[27];
           }
           stop_level = (inl_t < 6 || !icp_step(tot, &Ts)) ? 1 : 0;
