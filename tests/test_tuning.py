@@ -1,0 +1,92 @@
+"""Appendix-B tuner: CPU KATs of the cost and the
+coordinate descent, and a small GPU-batched tune_single run."""
+import math
+
+import pytest
+
+
+def test_cost_kats():
+    from paper_1810_12163_b200.tuning import cost
+
+    assert cost(1.0, 10.0, 50.0) == 0.0
+    assert abs(cost(0.9, 10.0, 50.0) - 0.01) < 1e-15
+    assert math.isinf(cost(0.99, 60.0, 50.0))
+    with pytest.raises(ValueError):
+        cost(1.5, 1.0, 2.0)
+
+
+def test_coordinate_descent_separable_quadratic():
+    from paper_1810_12163_b200.tuning import ParamDomain, coordinate_descent
+
+    doms = [ParamDomain("a", [0, 1, 2, 3, 4]), ParamDomain("b", [-2, -1, 0, 1]), ParamDomain("c", [0.5, 1.5, 2.5])]
+    calls = []
+
+    def f(x):
+        calls.append(dict(x))
+        return (x["a"] - 3) ** 2 + (x["b"] + 1) ** 2 + (x["c"] - 1.5) ** 2
+
+    r = coordinate_descent(doms, f, {"a": 0, "b": 0, "c": 0.5}, max_sweeps=10)
+    assert r.assignment == {"a": 3, "b": -1, "c": 1.5} and r.cost == 0.0
+    assert r.sweeps <= 2
+    assert all(x >= y for x, y in zip(r.history, r.history[1:]))  # per-sweep best is non-increasing
+    assert r.evaluations == len({tuple(sorted(c.items())) for c in calls}) == len(calls)  # memoised
+
+
+def test_coordinate_descent_ties_keep_current_and_exhaustive_single_domain():
+    from paper_1810_12163_b200.tuning import ParamDomain, coordinate_descent
+
+    r = coordinate_descent([ParamDomain("a", [0, 1, 2])], lambda x: 1.0, {"a": 1})
+    assert r.assignment == {"a": 1}
+    vals = {0: 3.0, 1: 2.0, 2: 0.5, 3: 0.7}
+    r = coordinate_descent([ParamDomain("a", list(vals))], lambda x: vals[x["a"]], {"a": 0})
+    assert r.assignment == {"a": 2}  # single domain = exhaustive search
+    r = coordinate_descent([ParamDomain("a", [0, 1])], lambda x: math.inf, {"a": 0})
+    assert r.assignment == {"a": 0}  # all infinite -> start returned
+
+
+def test_memo_concurrent_insert_or_get():
+    import threading
+
+    from paper_1810_12163_b200.tuning import Memo
+
+    n = [0]
+    lock = threading.Lock()
+
+    def f(x):
+        with lock:
+            n[0] += 1
+        return x["v"] * 2.0
+
+    m = Memo(f)
+    ths = [threading.Thread(target=m, args=({"v": i % 3},)) for i in range(30)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert n[0] == 3 and m.evaluations == 3 and m({"v": 2}) == 4.0
+
+
+@pytest.mark.gpu
+def test_tune_single_gpu(oracle, gpu_device):
+    import paper_1810_12163_b200 as P
+    from paper_1810_12163_b200.tuning import GpuObjective, ParamDomain, Sequences, tune_single
+    from world import OracleWorld
+
+    import oracle_ffi as of
+
+    w = OracleWorld(oracle, scene_seed=8, n_adapt=20, n_test=6, forest=of.FOREST_CASCADE, cluster=False)
+
+    def make_scene(fp):
+        s = P.Scene(gpu_device, w.blob, P.forest_params("cascade", **fp), P.intrinsics(), max_batch=8)
+        s.set_model(w.prims)
+        return s
+
+    seqs = Sequences([((list(w.D), list(w.RGB), w.adapt_poses), (w.Dt, w.RGBt, w.test_poses))])
+    obj = GpuObjective(make_scene, seqs, t_max=1e9, base_profile="fast", mode="icp")
+    doms = [ParamDomain("max_gen_iters", [50, 500]), ParamDomain("n_max", [256, 2048])]
+    r1 = tune_single(doms, obj, {"max_gen_iters": 50, "n_max": 256})
+    r2 = tune_single(doms, obj, {"max_gen_iters": 50, "n_max": 256})
+    assert r1.assignment == r2.assignment and r1.cost == r2.cost  # deterministic (memoised re-run)
+    fast = obj.memo({"max_gen_iters": 500, "n_max": 2048})  # the Table 4 Fast profile is in the domain
+    assert r1.cost <= fast
+    obj.close()
