@@ -67,6 +67,8 @@ def to_pose(pose) -> N.Pose:
         return pose
     if hasattr(pose, "R") and hasattr(pose, "t"):
         R, t = pose.R, pose.t
+    elif isinstance(pose, np.ndarray) and pose.shape == (4, 4):  # camera->world matrix
+        R, t = pose[:3, :3], pose[:3, 3]
     else:
         R, t = pose
     p = N.Pose()

@@ -90,3 +90,28 @@ def test_tune_single_gpu(oracle, gpu_device):
     fast = obj.memo({"max_gen_iters": 500, "n_max": 2048})  # the Table 4 Fast profile is in the domain
     assert r1.cost <= fast
     obj.close()
+
+
+def test_tune_cascade_step_order_shares_forest_params():
+    """Appendix B.2 on stand-in objectives: stage 1 tunes forest + RANSAC, the later stages
+    only RANSAC with phi* fixed, then the thresholds."""
+    from paper_1810_12163_b200.tuning import Memo, ParamDomain, tune_cascade
+
+    class Fake:
+        def __init__(self, best_nmax, best_tau):
+            self.base = "fast"
+            self.memo = Memo(lambda a: abs(a.get("n_max", 0) - best_nmax) + abs(a.get("tau", 0) - best_tau))
+            self.parallel = None
+
+        def close(self):
+            pass
+
+    objs = [Fake(1024, 0.2), Fake(2048, 0.05), Fake(512, 0.05)]
+    doms = [[ParamDomain("n_max", [256, 512, 1024, 2048]), ParamDomain("tau", [0.05, 0.2])]] * 3
+    starts = [{"n_max": 256, "tau": 0.05}] * 3
+    cfg, res = tune_cascade(doms, objs, starts, [0.03, 0.05, 0.075],
+                            lambda c: abs(c.thresholds[0] - 0.05) + abs(c.thresholds[1] - 0.075))
+    assert res[0].assignment == {"n_max": 1024, "tau": 0.2}
+    assert res[1].assignment["tau"] == 0.2 and res[2].assignment["tau"] == 0.2  # shared phi*
+    assert [s.n_max for s in cfg.stages] == [1024, 2048, 512]
+    assert list(cfg.thresholds) == [0.05, 0.075]
