@@ -114,6 +114,25 @@ void* scr_scene_stream(scr_scene s); /* cudaStream_t all scene work runs on */
 /* SceneModel used by ICP + ranking: analytic synthetic scene */
 scr_status scr_scene_set_analytic_model(scr_scene s, const scr_prim* prims, int n_prims);
 
+/* ---- TSDF scene model (scene_model; A13) -----------------------
+ * Dense voxel volume on the device: voxel (i,j,k) centre = origin + (idx + 0.5) * voxel,
+ * truncation `trunc` (SPEC default 4 voxels). */
+typedef struct scr_tsdf_s* scr_tsdf;
+scr_status scr_tsdf_create(scr_device dev, const float origin[3], float voxel, int nx, int ny, int nz, float trunc,
+                           scr_tsdf* out);
+void scr_tsdf_destroy(scr_tsdf v);
+/* fuse_frame: projective TSDF update with the frame's depth at `pose`
+ * (camera -> world); weight cap 128. Single writer. */
+scr_status scr_tsdf_fuse(scr_tsdf v, const scr_intrinsics* k, const float* depth, const scr_pose* pose);
+/* raycast_depth of the volume: z-depth per pixel (0 = no hit) and the
+ * packed surface normal (0xffffffff = unavailable; normals may be null). */
+scr_status scr_tsdf_raycast(scr_tsdf v, const scr_intrinsics* k, const scr_pose* pose, float* depth,
+                            uint32_t* normals);
+scr_status scr_tsdf_download(scr_tsdf v, float* tsdf, float* weight);
+/* ICP + ranking of the scene use the fused volume instead of the analytic model (null:
+ * back to the analytic model). The volume must outlive its use by the scene. */
+scr_status scr_scene_set_tsdf_model(scr_scene s, scr_tsdf v);
+
 /* ---- adaptation --------------------------------------------- */
 /* integrate_frame(state, forest, frame, pose) — SPEC.md:348-356 */
 scr_status scr_train(scr_scene s, const scr_frame* frame, const scr_pose* pose);

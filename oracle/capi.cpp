@@ -251,6 +251,38 @@ int or_forest_leaves(void* fp, const float* depth, const uint8_t* rgb, int w, in
 }
 
 // ---- scene ---------------------------------------------------------------------
+// ---- TSDF model (oracle/tsdf.cpp) ----
+void* or_tsdf_create(const float* origin, float voxel, int nx, int ny, int nz, float trunc) {
+  return new Tsdf(tsdf_create(origin, voxel, nx, ny, nz, trunc));
+}
+void or_tsdf_free(void* v) { delete static_cast<Tsdf*>(v); }
+void or_tsdf_fuse(void* v, const float* depth, const or_intrinsics* k, const or_pose* T) {
+  tsdf_fuse(*static_cast<Tsdf*>(v), depth, to_k(*k), to_pose(T->R, T->t));
+}
+void or_tsdf_dump(void* v, float* tsdf, float* weight) {
+  const Tsdf& t = *static_cast<Tsdf*>(v);
+  std::copy(t.tsdf.begin(), t.tsdf.end(), tsdf);
+  std::copy(t.weight.begin(), t.weight.end(), weight);
+}
+void or_tsdf_raycast(void* v, const or_pose* T, const or_intrinsics* k, float* depth, uint32_t* nrm) {
+  const Tsdf& t = *static_cast<Tsdf*>(v);
+  const Pose P = to_pose(T->R, T->t);
+  const Intrinsics K = to_k(*k);
+  float R[9], tf[3];
+  for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(P.R[i]);
+  for (int i = 0; i < 3; ++i) tf[i] = static_cast<float>(P.t[i]);
+  for (int y = 0; y < K.height; ++y)
+    for (int x = 0; x < K.width; ++x) {
+      float d = 0.0f;
+      uint32_t n = 0xffffffffu;
+      if (!tsdf_raycast_pixel(t, R, tf, K, x, y, &d, &n)) d = 0.0f;
+      depth[static_cast<size_t>(y) * K.width + x] = d;
+      if (nrm) nrm[static_cast<size_t>(y) * K.width + x] = n;
+    }
+}
+// the scene's ICP / ranking model becomes the volume (nullptr: back to the analytic model)
+void or_scene_set_tsdf(void* scene, void* v) { static_cast<Scene*>(scene)->tsdf = static_cast<const Tsdf*>(v); }
+
 void* or_scene_generate(uint64_t seed, int complexity) { return new Scene(generate_synthetic_scene(seed, complexity)); }
 void* or_scene_from_prims(const or_prim* p, int n) {
   Scene* s = new Scene();

@@ -107,9 +107,19 @@ struct Prim {
   float cell = 0.2f;
   uint32_t tex_seed = 0;
 };
+// TSDF scene model (oracle/tsdf.cpp, A13)
+struct Tsdf {
+  float origin[3] = {0, 0, 0};
+  float voxel = 0.01f, trunc = 0.04f;
+  int nx = 0, ny = 0, nz = 0;
+  std::vector<float> tsdf, weight;  // x fastest
+};
+constexpr int kTsdfMaxSteps = 1024;
+
 struct Scene {
   std::vector<Prim> prims;
   float room[3] = {4.0f, 3.0f, 2.5f};
+  const Tsdf* tsdf = nullptr;  // when set, ICP and ranking use the fused model instead
 };
 Scene generate_synthetic_scene(uint64_t seed, int complexity);
 struct Hit {
@@ -120,6 +130,13 @@ struct Hit {
 Hit raycast_pixel(const Scene& s, const float Rf[9], const float tf[3], const Intrinsics& k, int x, int y);
 void hit_normal(const Scene& s, const Hit& h, const float p[3], float n[3]);
 constexpr float kRenderMaxDepth = 6.0f;
+Tsdf tsdf_create(const float origin[3], float voxel, int nx, int ny, int nz, float trunc);
+void tsdf_fuse(Tsdf& v, const float* depth, const Intrinsics& k, const Pose& T);
+bool tsdf_sample(const Tsdf& v, const float p[3], float* F);
+bool tsdf_raycast_pixel(const Tsdf& v, const float R[9], const float tf[3], const Intrinsics& k, int x, int y,
+                        float* t, uint32_t* nrm);
+uint32_t pack_normal(const float n[3]);
+void unpack_normal(uint32_t p, float n[3]);
 void render_frame(const Scene& s, const Pose& T, const Intrinsics& k, float* depth, uint8_t* rgb);
 void generate_trajectory(uint64_t seed, int n, int kind, Pose* out);  // kind 0 = adapt, 1 = test
 

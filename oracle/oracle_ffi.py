@@ -172,6 +172,12 @@ class Oracle:
             "or_integrate_batch": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(Pose), C.c_int,
                                              C.c_int]),
             "or_grid_count": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(i32), C.c_int]),
+            "or_tsdf_create": (vp, [P(flt), flt, C.c_int, C.c_int, C.c_int, flt]),
+            "or_tsdf_free": (None, [vp]),
+            "or_tsdf_fuse": (None, [vp, P(flt), P(Intrinsics), P(Pose)]),
+            "or_tsdf_dump": (None, [vp, P(flt), P(flt)]),
+            "or_tsdf_raycast": (None, [vp, P(Pose), P(Intrinsics), P(flt), P(C.c_uint32)]),
+            "or_scene_set_tsdf": (None, [vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -296,6 +302,28 @@ class Oracle:
         if rc:
             raise RuntimeError(self.err())
         return list(out)
+
+    # ---- TSDF model ----
+    def tsdf_create(self, origin, voxel, dims, trunc=None):
+        o = np.ascontiguousarray(origin, np.float32)
+        return self.lib.or_tsdf_create(_ptr(o, C.c_float), float(voxel), int(dims[0]), int(dims[1]), int(dims[2]),
+                                       float(4 * voxel if trunc is None else trunc))
+
+    def tsdf_fuse(self, vol, depth, k, pose):
+        d = np.ascontiguousarray(depth, np.float32)
+        self.lib.or_tsdf_fuse(vol, _ptr(d, C.c_float), C.byref(k), C.byref(pose))
+
+    def tsdf_dump(self, vol, dims):
+        n = int(dims[0]) * int(dims[1]) * int(dims[2])
+        t, w = np.zeros(n, np.float32), np.zeros(n, np.float32)
+        self.lib.or_tsdf_dump(vol, _ptr(t, C.c_float), _ptr(w, C.c_float))
+        return t, w
+
+    def tsdf_raycast(self, vol, pose, k):
+        d = np.zeros((k.height, k.width), np.float32)
+        nrm = np.zeros((k.height, k.width), np.uint32)
+        self.lib.or_tsdf_raycast(vol, C.byref(pose), C.byref(k), _ptr(d, C.c_float), _ptr(nrm, C.c_uint32))
+        return d, nrm
 
     def ransac(self, forest, state, depth, rgb, k, params, seed):
         d = np.ascontiguousarray(depth, np.float32)

@@ -35,8 +35,14 @@ void render_model_map(const Scene& s, const Pose& T, const Intrinsics& k, ModelM
   for (int y = 0; y < m.h; ++y)
     for (int x = 0; x < m.w; ++x) {
       const size_t idx = static_cast<size_t>(y) * m.w + x;
-      const Hit h = raycast_pixel(s, R, tf, k, x, y);
-      if (h.prim < 0 || !(h.t <= kRenderMaxDepth)) continue;
+      Hit h{0.0f, -1, -1};
+      uint32_t packed = 0xffffffffu;
+      if (s.tsdf) {  // fused model: hit + packed normal (A13)
+        if (!tsdf_raycast_pixel(*s.tsdf, R, tf, k, x, y, &h.t, &packed) || packed == 0xffffffffu) continue;
+      } else {
+        h = raycast_pixel(s, R, tf, k, x, y);
+        if (h.prim < 0 || !(h.t <= kRenderMaxDepth)) continue;
+      }
       const float dcx = (static_cast<float>(x) - static_cast<float>(k.cx)) / static_cast<float>(k.fx);
       const float dcy = (static_cast<float>(y) - static_cast<float>(k.cy)) / static_cast<float>(k.fy);
       float p[3];
@@ -45,7 +51,8 @@ void render_model_map(const Scene& s, const Pose& T, const Intrinsics& k, ModelM
         p[i] = std::fma(h.t, di, tf[i]);
       }
       float nn[3];
-      hit_normal(s, h, p, nn);
+      if (s.tsdf) unpack_normal(packed, nn);
+      else hit_normal(s, h, p, nn);
       for (int i = 0; i < 3; ++i) {
         m.v[3 * idx + i] = p[i];
         m.n[3 * idx + i] = nn[i];
@@ -231,6 +238,12 @@ void raycast_depth(const Scene& s, const Pose& T, const Intrinsics& k, float* ou
   for (int i = 0; i < 3; ++i) tf[i] = static_cast<float>(T.t[i]);
   for (int y = 0; y < k.height; ++y)
     for (int x = 0; x < k.width; ++x) {
+      if (s.tsdf) {
+        float t;
+        uint32_t nrm;
+        out[static_cast<size_t>(y) * k.width + x] = tsdf_raycast_pixel(*s.tsdf, R, tf, k, x, y, &t, &nrm) ? t : 0.0f;
+        continue;
+      }
       const Hit h = raycast_pixel(s, R, tf, k, x, y);
       out[static_cast<size_t>(y) * k.width + x] = (h.prim >= 0 && h.t <= kRenderMaxDepth) ? h.t : 0.0f;
     }

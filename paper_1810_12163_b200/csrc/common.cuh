@@ -666,6 +666,105 @@ SCR_DEV bool prim_in_view(const Prim& q, const float R[9], const float o[3], flo
   return prim_in_frustum(q, R, o, fx, fy, cx, cy, -0.5f, W - 0.5f, -0.5f, H - 0.5f);
 }
 
+// ---- TSDF scene model (oracle/tsdf.cpp restated; A13) ----------------------------
+struct TsdfView {
+  const float2* vox = nullptr;  // {tsdf, weight}, x fastest
+  float ox = 0, oy = 0, oz = 0, voxel = 0, trunc = 0;
+  int nx = 0, ny = 0, nz = 0;
+};
+constexpr int kTsdfMaxSteps = 1024;
+
+SCR_DEV float tsdf_lerp(float a, float b, float t) { return __fmaf_rn(t, __fsub_rn(b, a), a); }
+
+SCR_DEV bool tsdf_sample(const TsdfView& v, float px, float py, float pz, float* F) {
+  const float g0 = __fsub_rn(__fdiv_rn(__fsub_rn(px, v.ox), v.voxel), 0.5f);
+  const float g1 = __fsub_rn(__fdiv_rn(__fsub_rn(py, v.oy), v.voxel), 0.5f);
+  const float g2 = __fsub_rn(__fdiv_rn(__fsub_rn(pz, v.oz), v.voxel), 0.5f);
+  const float f0 = floorf(g0), f1 = floorf(g1), f2 = floorf(g2);
+  const int i0 = static_cast<int>(f0), i1 = static_cast<int>(f1), i2 = static_cast<int>(f2);
+  if (i0 < 0 || i1 < 0 || i2 < 0 || i0 + 1 >= v.nx || i1 + 1 >= v.ny || i2 + 1 >= v.nz) return false;
+  const float r0 = __fsub_rn(g0, f0), r1 = __fsub_rn(g1, f1), r2 = __fsub_rn(g2, f2);
+  float c[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const size_t idx = (static_cast<size_t>(i2 + (q >> 2)) * v.ny + (i1 + ((q >> 1) & 1))) * v.nx + (i0 + (q & 1));
+    const float2 e = v.vox[idx];
+    if (!(e.y > 0.0f)) return false;
+    c[q] = e.x;
+  }
+  const float c00 = tsdf_lerp(c[0], c[1], r0), c10 = tsdf_lerp(c[2], c[3], r0);
+  const float c01 = tsdf_lerp(c[4], c[5], r0), c11 = tsdf_lerp(c[6], c[7], r0);
+  *F = tsdf_lerp(tsdf_lerp(c00, c10, r1), tsdf_lerp(c01, c11, r1), r2);
+  return true;
+}
+
+SCR_DEV uint32_t tsdf_pack_normal(float n0, float n1, float n2) {
+  const float s = __fadd_rn(__fadd_rn(fabsf(n0), fabsf(n1)), fabsf(n2));
+  float u = __fdiv_rn(n0, s), w = __fdiv_rn(n1, s);
+  if (n2 < 0.0f) {
+    const float uu = __fmul_rn(__fsub_rn(1.0f, fabsf(w)), u >= 0.0f ? 1.0f : -1.0f);
+    const float ww = __fmul_rn(__fsub_rn(1.0f, fabsf(u)), w >= 0.0f ? 1.0f : -1.0f);
+    u = uu;
+    w = ww;
+  }
+  const int qu = max(-32767, min(32767, static_cast<int>(floorf(__fadd_rn(__fmul_rn(u, 32767.0f), 0.5f)))));
+  const int qw = max(-32767, min(32767, static_cast<int>(floorf(__fadd_rn(__fmul_rn(w, 32767.0f), 0.5f)))));
+  return (static_cast<uint32_t>(qu) & 0xffffu) | (static_cast<uint32_t>(qw) << 16);
+}
+
+SCR_DEV void tsdf_unpack_normal(uint32_t p, float n[3]) {
+  const float u = __fdiv_rn(static_cast<float>(static_cast<int16_t>(p & 0xffffu)), 32767.0f);
+  const float w = __fdiv_rn(static_cast<float>(static_cast<int16_t>(p >> 16)), 32767.0f);
+  float x = u, y = w;
+  const float z = __fsub_rn(__fsub_rn(1.0f, fabsf(u)), fabsf(w));
+  if (z < 0.0f) {
+    x = __fmul_rn(__fsub_rn(1.0f, fabsf(w)), u >= 0.0f ? 1.0f : -1.0f);
+    y = __fmul_rn(__fsub_rn(1.0f, fabsf(u)), w >= 0.0f ? 1.0f : -1.0f);
+  }
+  const float len = __fsqrt_rn(__fmaf_rn(x, x, __fmaf_rn(y, y, __fmul_rn(z, z))));
+  n[0] = __fdiv_rn(x, len);
+  n[1] = __fdiv_rn(y, len);
+  n[2] = __fdiv_rn(z, len);
+}
+
+// March one ray o + t d (d = R (dcx, dcy, 1), so t is the camera depth): hit at the first
+// known F <= 0 after a known F > 0, refined linearly; *nrm = packed normal or 0xffffffff.
+template <typename FP>
+SCR_DEV bool tsdf_raycast_ray(const TsdfView& v, FP o, const float d[3], float* t_out, uint32_t* nrm) {
+  float t = 0.2f, tp = 0.0f, Fp = 0.0f;
+  bool prev = false;
+  for (int it = 0; it < kTsdfMaxSteps && t <= kRenderMaxDepth; ++it) {
+    float F;
+    if (tsdf_sample(v, __fmaf_rn(t, d[0], o[0]), __fmaf_rn(t, d[1], o[1]), __fmaf_rn(t, d[2], o[2]), &F)) {
+      if (prev && Fp > 0.0f && F <= 0.0f) {
+        const float ts = __fmaf_rn(__fsub_rn(t, tp), __fdiv_rn(Fp, __fsub_rn(Fp, F)), tp);
+        if (!(ts <= kRenderMaxDepth)) return false;
+        *t_out = ts;
+        *nrm = 0xffffffffu;
+        const float q0 = __fmaf_rn(ts, d[0], o[0]), q1 = __fmaf_rn(ts, d[1], o[1]), q2 = __fmaf_rn(ts, d[2], o[2]);
+        float gp[3], gm[3];
+        if (!tsdf_sample(v, __fadd_rn(q0, v.voxel), q1, q2, &gp[0]) || !tsdf_sample(v, __fsub_rn(q0, v.voxel), q1, q2, &gm[0]) ||
+            !tsdf_sample(v, q0, __fadd_rn(q1, v.voxel), q2, &gp[1]) || !tsdf_sample(v, q0, __fsub_rn(q1, v.voxel), q2, &gm[1]) ||
+            !tsdf_sample(v, q0, q1, __fadd_rn(q2, v.voxel), &gp[2]) || !tsdf_sample(v, q0, q1, __fsub_rn(q2, v.voxel), &gm[2]))
+          return true;
+        const float g0 = __fsub_rn(gp[0], gm[0]), g1 = __fsub_rn(gp[1], gm[1]), g2 = __fsub_rn(gp[2], gm[2]);
+        const float len = __fsqrt_rn(__fmaf_rn(g0, g0, __fmaf_rn(g1, g1, __fmul_rn(g2, g2))));
+        if (!(len > 0.0f)) return true;
+        *nrm = tsdf_pack_normal(__fdiv_rn(g0, len), __fdiv_rn(g1, len), __fdiv_rn(g2, len));
+        return true;
+      }
+      prev = true;
+      Fp = F;
+      tp = t;
+      t = __fadd_rn(t, F > 0.0f ? fmaxf(__fmul_rn(F, v.trunc), v.voxel) : v.voxel);
+    } else {
+      prev = false;
+      t = __fadd_rn(t, v.trunc);
+    }
+  }
+  return false;
+}
+
 SCR_DEV void hit_normal(const Prim* prims, int prim, int face, const float p[3], float n[3]) {
   if (face < 6) {
     n[0] = n[1] = n[2] = 0.0f;

@@ -157,6 +157,7 @@ struct scr_scene_s {
   float* d_cov = nullptr;   // 6 per mode (dumps only)
   scr::Prim* d_prims = nullptr;
   int n_prims = 0;
+  scr_tsdf tsdf_model = nullptr;  // ICP / ranking model when set (else the analytic prims)
   scr::Workspace ws;
   // relocalisation lanes (scr_scene_fork): a lane shares the parent's read-only device
   // state (forest, predictions, model) and owns a stream + workspace of its own
@@ -199,6 +200,8 @@ inline unsigned long long* work_ptr(scr_scene s) { return s->prof.on ? s->prof.d
     (s)->prof.launches[(kid)]++;                                  \
   } while (0)
 
+// tsdf.cu
+TsdfView tsdf_view(scr_tsdf v);
 // scene.cu
 scr_status refresh_lane(scr_scene s);
 scr_status publish(scr_scene s);

@@ -1280,11 +1280,15 @@ SCR_DEV void divmod_w(int p, int W, float invW, int& x, int& y) {
 #ifndef SCR_ICP_MINB
 #define SCR_ICP_MINB 4
 #endif
+// kTsdf: the scene model is a fused TSDF volume (A13) instead of the analytic
+// primitives; map entries then carry {t, packed normal} instead of {t, prim | face << 16}.
+template <bool kTsdf>
 __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, SCR_ICP_MINB)
     k_icp_score(IcpArgs ia, FrameGeom g, FrameRefs fr, const Prim* __restrict__ prims, int nprims,
                 const Pose* __restrict__ cand, const int* __restrict__ ncand, uint2* __restrict__ maps,
                 Pose* __restrict__ out_pose, int* __restrict__ out_conv, double* __restrict__ out_rms,
-                double* __restrict__ out_inl, double* __restrict__ out_score, unsigned long long* __restrict__ work) {
+                double* __restrict__ out_inl, double* __restrict__ out_score, unsigned long long* __restrict__ work,
+                TsdfView tv) {
   __shared__ double red[kIcpThreads / 32][32];
   __shared__ double part2[2][32];  // this CTA's f64 partials, double-buffered by iteration parity
   __shared__ int ipart2[2][4];     // (read by every CTA of the cluster over DSMEM)
@@ -1341,9 +1345,14 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       // K8: model map of this level at the reference pose (split over the cluster)
       if (work && rank == 0 && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(Wl * Hl));
       fill_ray_tables(Wl, Hl, fxl, fyl, cxl, cyl, s_dcx, s_dcy);  // synced by build_plist
-      build_plist(prims, nprims, Rr, tr, fxl, fyl, cxl, cyl, Wl, Hl, s_plist, &s_pn);
-      const int npl = s_pn;
-      const bool tiled = npl <= 32 && (Wl % kTileW) == 0;
+      int npl = 0;
+      if (!kTsdf) {
+        build_plist(prims, nprims, Rr, tr, fxl, fyl, cxl, cyl, Wl, Hl, s_plist, &s_pn);
+        npl = s_pn;
+      } else {
+        __syncthreads();  // ray tables visible
+      }
+      const bool tiled = !kTsdf && npl <= 32 && (Wl % kTileW) == 0;
       if (tiled) build_tile_masks(prims, s_plist, npl, Rr, tr, fxl, fyl, cxl, cyl, Wl, Hl, s_tmask);
       unsigned long long tests = 0;
       const int twl = Wl / kTileW;
@@ -1353,17 +1362,23 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
         divmod_w(p, Wl, invWl, x, y);
         float d[3];
         ray_dir_tab(Rr, s_dcx[x], s_dcy[y], d);
-        Hit h;
-        if (tiled) {
-          const uint32_t m = s_tmask[(y / kTileH) * twl + x / kTileW];
-          tests += __popc(m);
-          h = raycast_mask(prims, s_plist, m, tr, d);
-        } else {
-          tests += npl;
-          h = raycast_list(prims, s_plist, npl, tr, d);
-        }
         uint2 v = make_uint2(0u, 0xffffffffu);
-        if (h.prim >= 0 && h.t <= kRenderMaxDepth) v = make_uint2(__float_as_uint(h.t), h.prim | (h.face << 16));
+        if (kTsdf) {
+          float t;
+          uint32_t nrm;
+          if (tsdf_raycast_ray(tv, tr, d, &t, &nrm) && nrm != 0xffffffffu) v = make_uint2(__float_as_uint(t), nrm);
+        } else {
+          Hit h;
+          if (tiled) {
+            const uint32_t m = s_tmask[(y / kTileH) * twl + x / kTileW];
+            tests += __popc(m);
+            h = raycast_mask(prims, s_plist, m, tr, d);
+          } else {
+            tests += npl;
+            h = raycast_list(prims, s_plist, npl, tr, d);
+          }
+          if (h.prim >= 0 && h.t <= kRenderMaxDepth) v = make_uint2(__float_as_uint(h.t), h.prim | (h.face << 16));
+        }
         map[p] = v;
       }
       if (work) work_add(work, W_RAY_PRIMS, static_cast<unsigned>(tests));
@@ -1431,7 +1446,8 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
             ray_dir_tab(Rr, s_dcx[ui], s_dcy[vi], dm);
 #pragma unroll
             for (int i = 0; i < 3; ++i) m[i] = __fmaf_rn(th, dm[i], tr[i]);
-            hit_normal(prims, static_cast<int>(mv[u].y & 0xffffu), static_cast<int>(mv[u].y >> 16), m, nn);
+            if (kTsdf) tsdf_unpack_normal(mv[u].y, nn);
+            else hit_normal(prims, static_cast<int>(mv[u].y & 0xffffu), static_cast<int>(mv[u].y >> 16), m, nn);
             const float* pw = px[u].pw;
             const float df0 = __fsub_rn(pw[0], m[0]), df1 = __fsub_rn(pw[1], m[1]), df2 = __fsub_rn(pw[2], m[2]);
             const float dist2 = __fmaf_rn(df0, df0, __fmaf_rn(df1, df1, __fmul_rn(df2, df2)));
@@ -1523,9 +1539,14 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
     if (work && rank == 0 && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(g.W * g.H));
     __syncthreads();
     fill_ray_tables(g.W, g.H, g.fx, g.fy, g.cx, g.cy, s_dcx, s_dcy);
-    build_plist(prims, nprims, R, t, g.fx, g.fy, g.cx, g.cy, g.W, g.H, s_plist, &s_pn);
-    const int npl = s_pn;
-    const bool tiled = npl <= 32 && (g.W % kTileW) == 0;
+    int npl = 0;
+    if (!kTsdf) {
+      build_plist(prims, nprims, R, t, g.fx, g.fy, g.cx, g.cy, g.W, g.H, s_plist, &s_pn);
+      npl = s_pn;
+    } else {
+      __syncthreads();
+    }
+    const bool tiled = !kTsdf && npl <= 32 && (g.W % kTileW) == 0;
     if (tiled) build_tile_masks(prims, s_plist, npl, R, t, g.fx, g.fy, g.cx, g.cy, g.W, g.H, s_tmask);
     unsigned long long tests = 0;
     const int tw0 = g.W / kTileW;
@@ -1536,7 +1557,10 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       float d[3];
       ray_dir_tab(R, s_dcx[x], s_dcy[y], d);
       Hit h;
-      if (tiled) {
+      if (kTsdf) {
+        uint32_t nrm;
+        h.prim = tsdf_raycast_ray(tv, t, d, &h.t, &nrm) ? 0 : -1;
+      } else if (tiled) {
         const uint32_t m = s_tmask[(y / kTileH) * tw0 + x / kTileW];
         tests += __popc(m);
         h = raycast_mask(prims, s_plist, m, t, d);
@@ -1782,10 +1806,17 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
     const int nj = std::min(w.icp_cap, njobs - j0);
     IcpArgs ia{w.ncull_cap, jobs_per, mode != SCR_MODE_RAW ? 1 : 0, j0,
                static_cast<size_t>(s->k.width) * s->k.height};
-    SCR_LAUNCH(s, K_ICP,
-               (k_icp_score<<<nj * kIcpCtas, kIcpThreads, 0, s->stream>>>(ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand,
-                                                       w.icp_map, w.icp_pose, w.icp_conv, w.icp_rms, w.icp_inl,
-                                                       w.icp_score, wk)));
+    if (s->tsdf_model) {
+      SCR_LAUNCH(s, K_ICP,
+                 (k_icp_score<true><<<nj * kIcpCtas, kIcpThreads, 0, s->stream>>>(
+                     ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand, w.icp_map, w.icp_pose, w.icp_conv,
+                     w.icp_rms, w.icp_inl, w.icp_score, wk, tsdf_view(s->tsdf_model))));
+    } else {
+      SCR_LAUNCH(s, K_ICP,
+                 (k_icp_score<false><<<nj * kIcpCtas, kIcpThreads, 0, s->stream>>>(
+                     ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand, w.icp_map, w.icp_pose, w.icp_conv,
+                     w.icp_rms, w.icp_inl, w.icp_score, wk, TsdfView{})));
+    }
   }
   SCR_LAUNCH(s, K_FINALIZE,
              (k_finalize<<<(nA + 127) / 128, 128, 0, s->stream>>>(nA, mode, w.ncull_cap, w.cand, w.ncand, w.icp_pose,
@@ -1924,7 +1955,7 @@ scr_status scr_cascade_batch(scr_scene s, const scr_frame* frames, int n, const 
   if (!s) return SCR_E_ARG;
   SCR_TRY(check_stage_args(n, stages, modes, nstages, seeds, out));
   if (nstages > 1 && !thr) return SCR_E_ARG;
-  if (!(s->parent ? s->parent->d_prims : s->d_prims)) {  // every mode scores against the model (A11)
+  if (!(s->parent ? (s->parent->d_prims || s->parent->tsdf_model) : (s->d_prims || s->tsdf_model))) {  // every mode scores against the model (A11)
     set_error("relocalise: no scene model set (scr_scene_set_analytic_model)");
     return SCR_E_ARG;
   }
@@ -1965,7 +1996,7 @@ scr_status scr_cascade_frameset(scr_scene s, scr_frameset fs, const int32_t* idx
   if (!s || !fs || (!idx && n > 0)) return SCR_E_ARG;
   SCR_TRY(check_stage_args(n, stages, modes, nstages, seeds, out));
   if (nstages > 1 && !thr) return SCR_E_ARG;
-  if (!(s->parent ? s->parent->d_prims : s->d_prims)) {
+  if (!(s->parent ? (s->parent->d_prims || s->parent->tsdf_model) : (s->d_prims || s->tsdf_model))) {
     set_error("relocalise: no scene model set (scr_scene_set_analytic_model)");
     return SCR_E_ARG;
   }
@@ -2000,7 +2031,7 @@ scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_pa
   scr_result* d_res = nullptr;
   SCR_CUDA(cudaMalloc(&d_res, sizeof(scr_result)));
   // raw mode still needs a model for the score; skip ICP work by using raw
-  const bool have_model = s->d_prims != nullptr;
+  const bool have_model = s->d_prims != nullptr || s->tsdf_model != nullptr;
   if (!have_model) {
     set_error("scr_debug_ransac: no scene model set");
     cudaFree(d_res);
@@ -2044,7 +2075,7 @@ scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_pa
 
 scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, scr_pose* out, int* converged,
                          double* rms, double* inlier_frac, double* score) {
-  if (!s || !f || !init || !s->d_prims) return SCR_E_ARG;
+  if (!s || !f || !init || !(s->d_prims || s->tsdf_model)) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
@@ -2058,10 +2089,17 @@ scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, 
   SCR_CUDA(cudaMemcpyAsync(s->ws.ncand, &one, sizeof(int), cudaMemcpyHostToDevice, s->stream));
   SCR_CUDA(cudaMemcpyAsync(s->ws.cand, init, sizeof(Pose), cudaMemcpyHostToDevice, s->stream));
   IcpArgs ia{s->ws.ncull_cap, 1, 1, 0, WH};
-  SCR_LAUNCH(s, K_ICP,
-             (k_icp_score<<<kIcpCtas, kIcpThreads, 0, s->stream>>>(ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand,
-                                                    s->ws.ncand, s->ws.icp_map, s->ws.icp_pose, s->ws.icp_conv,
-                                                    s->ws.icp_rms, s->ws.icp_inl, s->ws.icp_score, nullptr)));
+  if (s->tsdf_model) {
+    SCR_LAUNCH(s, K_ICP, (k_icp_score<true><<<kIcpCtas, kIcpThreads, 0, s->stream>>>(
+                             ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand, s->ws.ncand, s->ws.icp_map,
+                             s->ws.icp_pose, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.icp_score, nullptr,
+                             tsdf_view(s->tsdf_model))));
+  } else {
+    SCR_LAUNCH(s, K_ICP, (k_icp_score<false><<<kIcpCtas, kIcpThreads, 0, s->stream>>>(
+                             ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand, s->ws.ncand, s->ws.icp_map,
+                             s->ws.icp_pose, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.icp_score, nullptr,
+                             TsdfView{})));
+  }
   SCR_CUDA(cudaGetLastError());
   SCR_CUDA(cudaStreamSynchronize(s->stream));
   SCR_CUDA(cudaMemcpy(out, s->ws.icp_pose, sizeof(Pose), cudaMemcpyDeviceToHost));

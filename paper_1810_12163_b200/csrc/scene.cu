@@ -698,6 +698,7 @@ scr_status refresh_lane(scr_scene s) {
   s->d_cov = p->d_cov;
   s->d_prims = p->d_prims;
   s->n_prims = p->n_prims;
+  s->tsdf_model = p->tsdf_model;
   s->cursor = p->cursor;
   if (p->published && s->stream) SCR_CUDA(cudaStreamWaitEvent(s->stream, p->published, 0));
   return SCR_OK;
@@ -918,6 +919,7 @@ void scr_scene_destroy(scr_scene s) {
     s->parent->lanes--;
     s->d_nodes = nullptr; s->d_specs = nullptr; s->d_entries = nullptr; s->d_seen = nullptr;
     s->d_count = nullptr; s->d_geom = nullptr; s->d_col = nullptr; s->d_cov = nullptr; s->d_prims = nullptr;
+    s->tsdf_model = nullptr;
   }
   if (s->published) cudaEventDestroy(s->published);
   for (cudaEvent_t e : {s->ws.ev_stage[0], s->ws.ev_stage[1], s->ws.ev_upload})
@@ -1409,7 +1411,7 @@ scr_status scr_frameset_upload(scr_frameset fs, int first, const scr_frame* fram
 scr_status scr_frameset_render(scr_frameset fs, int first, const scr_pose* poses, int n) {
   if (!fs || first < 0 || n < 0 || first + n > fs->cap || !poses) return SCR_E_ARG;
   scr_scene s = fs->scene;
-  if (!(s->parent ? s->parent->d_prims : s->d_prims)) {
+  if (!(s->parent ? (s->parent->d_prims || s->parent->tsdf_model) : (s->d_prims || s->tsdf_model))) {
     set_error("scr_frameset_render: no analytic model set");
     return SCR_E_ARG;
   }
@@ -1441,6 +1443,24 @@ scr_status scr_frameset_download(scr_frameset fs, int first, int n, float* depth
   if (depth) SCR_CUDA(cudaMemcpy(depth, fs->depth + first * WH, n * WH * sizeof(float), cudaMemcpyDeviceToHost));
   if (rgb) SCR_CUDA(cudaMemcpy(rgb, fs->rgb + first * WH * 3, n * WH * 3, cudaMemcpyDeviceToHost));
   return SCR_OK;
+}
+
+static scr_status scr_scene_set_tsdf_model_impl(scr_scene s, scr_tsdf v) {
+  if (!s) return SCR_E_ARG;
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_CUDA(cudaStreamSynchronize(s->stream));
+  s->tsdf_model = v;
+  return SCR_OK;
+}
+
+scr_status scr_scene_set_tsdf_model(scr_scene s, scr_tsdf v) {
+  if (s && s->parent) {
+    set_error("scr_scene_set_tsdf_model: a relocalisation lane is read-only; set the model on its scene");
+    return SCR_E_ARG;
+  }
+  scr_status st = scr_scene_set_tsdf_model_impl(s, v);
+  if (st == SCR_OK && s) st = publish(s);
+  return st;
 }
 
 // Updates of shared scene state: refused on lanes, published to lanes when done.

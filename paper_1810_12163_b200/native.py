@@ -109,6 +109,12 @@ SIGNATURES = {
                                    _P(_vp)]),
     "scr_scene_destroy": (None, [_vp]),
     "scr_scene_fork": (C.c_int, [_vp, C.c_int, _P(_vp)]),
+    "scr_tsdf_create": (C.c_int, [_vp, _P(C.c_float), C.c_float, C.c_int, C.c_int, C.c_int, C.c_float, _P(_vp)]),
+    "scr_tsdf_destroy": (None, [_vp]),
+    "scr_tsdf_fuse": (C.c_int, [_vp, _P(Intrinsics), _P(C.c_float), _P(Pose)]),
+    "scr_tsdf_raycast": (C.c_int, [_vp, _P(Intrinsics), _P(Pose), _P(C.c_float), _P(C.c_uint32)]),
+    "scr_tsdf_download": (C.c_int, [_vp, _P(C.c_float), _P(C.c_float)]),
+    "scr_scene_set_tsdf_model": (C.c_int, [_vp, _vp]),
     "scr_scene_total_leaves": (_i64, [_vp]),
     "scr_scene_stream": (_vp, [_vp]),
     "scr_scene_set_analytic_model": (C.c_int, [_vp, _vp, C.c_int]),

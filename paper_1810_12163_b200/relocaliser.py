@@ -206,6 +206,12 @@ class Scene:
         kernels = {names[i].decode(): {"ms": ms[i], "launches": n[i]} for i in range(k)}
         return {"kernels": kernels, "work": {w: int(work[i]) for i, w in enumerate(self.WORK_NAMES)}}
 
+    def set_tsdf_model(self, volume: "TsdfVolume | None"):
+        """ICP and ranking use the fused volume (None: back to the analytic model)."""
+        N.check(self.lib.scr_scene_set_tsdf_model(self.handle, volume.handle if volume else None),
+                "scr_scene_set_tsdf_model")
+        self._tsdf = volume  # keep it alive while the scene uses it
+
     def set_model(self, prims: np.ndarray):
         prims = np.ascontiguousarray(prims, N.PRIM_DTYPE)
         N.check(self.lib.scr_scene_set_analytic_model(self.handle, prims.ctypes.data, prims.size),
@@ -365,6 +371,50 @@ def generate_trajectory(seed: int, n: int, kind: int) -> list:
     arr = (N.Pose * n)()
     N.load().scr_generate_trajectory(seed, n, kind, arr)
     return list(arr)
+
+
+class TsdfVolume:
+    """Dense TSDF scene model on the device (scr_tsdf_*). fuse = fuse_frame,
+    raycast = raycast_depth (z-depth + packed normals)."""
+
+    def __init__(self, device: Device, origin, voxel: float, dims, trunc: float | None = None):
+        self.lib, self.device = device.lib, device
+        self.dims = tuple(int(d) for d in dims)
+        o = np.ascontiguousarray(origin, np.float32)
+        h = C.c_void_p()
+        N.check(self.lib.scr_tsdf_create(device.handle, N.ptr(o, C.c_float), float(voxel), *self.dims,
+                                         float(4 * voxel if trunc is None else trunc), C.byref(h)), "scr_tsdf_create")
+        self.handle = h
+
+    def fuse(self, depth, pose, k: N.Intrinsics):
+        d = np.ascontiguousarray(depth, np.float32)
+        p = to_pose(pose)
+        N.check(self.lib.scr_tsdf_fuse(self.handle, C.byref(k), N.ptr(d, C.c_float), C.byref(p)), "fuse_frame")
+
+    def raycast(self, pose, k: N.Intrinsics):
+        d = np.zeros((k.height, k.width), np.float32)
+        n = np.zeros((k.height, k.width), np.uint32)
+        p = to_pose(pose)
+        N.check(self.lib.scr_tsdf_raycast(self.handle, C.byref(k), C.byref(p), N.ptr(d, C.c_float),
+                                          N.ptr(n, C.c_uint32)), "raycast_depth")
+        return d, n
+
+    def download(self):
+        n = self.dims[0] * self.dims[1] * self.dims[2]
+        t, w = np.zeros(n, np.float32), np.zeros(n, np.float32)
+        N.check(self.lib.scr_tsdf_download(self.handle, N.ptr(t, C.c_float), N.ptr(w, C.c_float)), "tsdf download")
+        return t, w
+
+    def close(self):
+        if self.handle:
+            self.lib.scr_tsdf_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class FrameSet:
