@@ -154,6 +154,33 @@ class Device {
   scr_device d_ = nullptr;
 };
 
+// TsdfVolume: dense TSDF scene model on the device; fuse = fuse_frame,
+// raycast = raycast_depth (z-depth, 0 = no hit; packed normals optional).
+class TsdfVolume {
+ public:
+  TsdfVolume(Device& dev, const float origin[3], float voxel, int nx, int ny, int nz, float trunc = 0.0f) {
+    check(scr_tsdf_create(dev.handle(), origin, voxel, nx, ny, nz, trunc > 0.0f ? trunc : 4.0f * voxel, &v_),
+          "TsdfVolume");
+  }
+  ~TsdfVolume() {
+    if (v_) scr_tsdf_destroy(v_);
+  }
+  TsdfVolume(const TsdfVolume&) = delete;
+  TsdfVolume& operator=(const TsdfVolume&) = delete;
+  void fuse_frame(const PinholeIntrinsics& k, const float* depth, const RigidTransform& pose) {
+    check(scr_tsdf_fuse(v_, &k, depth, &pose), "fuse_frame");
+  }
+  std::vector<float> raycast_depth(const PinholeIntrinsics& k, const RigidTransform& pose) {
+    std::vector<float> d(static_cast<size_t>(k.width) * k.height);
+    check(scr_tsdf_raycast(v_, &k, &pose, d.data(), nullptr), "raycast_depth");
+    return d;
+  }
+  scr_tsdf handle() const { return v_; }
+
+ private:
+  scr_tsdf v_ = nullptr;
+};
+
 class Relocaliser {
  public:
   Relocaliser(Device& dev, const std::vector<uint8_t>& forest_blob, const ForestParams& fp,
@@ -179,6 +206,10 @@ class Relocaliser {
 
   void set_scene_model(const std::vector<scr_prim>& prims) {
     check(scr_scene_set_analytic_model(s_, prims.data(), static_cast<int>(prims.size())), "set_scene_model");
+  }
+  // ICP and ranking on a fused model (the volume must outlive its use; nullptr: analytic)
+  void set_scene_model(const TsdfVolume* volume) {
+    check(scr_scene_set_tsdf_model(s_, volume ? volume->handle() : nullptr), "set_scene_model");
   }
   // integrate_frame: throws UnreliablePose if !frame.pose_reliable
   void integrate_frame(const RgbdFrame& frame, const RigidTransform& pose) {
