@@ -447,9 +447,12 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
 }
 
 // Sample batch k of frame a: eta draws of uniform_int(G) from Rng::stream(seed, nmax + k).
-__global__ void k_draw_samples(FrameRefs fr, const uint64_t* __restrict__ seeds, int nA, int nmax, int eta, int batch,
+// Sample batches 0..K of every frame in one launch: thread (frame a, batch blockIdx.y)
+// draws the batch's eta pixels from its own stream Rng::stream(seed, N_max + batch) (A2).
+__global__ void k_draw_samples(FrameRefs fr, const uint64_t* __restrict__ seeds, int nA, int nmax, int eta,
                                int scap, int* __restrict__ samples) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  const int batch = blockIdx.y;
   if (a >= nA) return;
   const uint64_t G = static_cast<uint64_t>(fr.gcount[fr.fidx[a]]);
   int* out = samples + static_cast<size_t>(a) * scap + static_cast<size_t>(batch) * eta;
@@ -458,8 +461,8 @@ __global__ void k_draw_samples(FrameRefs fr, const uint64_t* __restrict__ seeds,
     return;
   }
   Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(nmax) + static_cast<uint64_t>(batch));
-  const uint64_t mG = barrett_m(G);
-  for (int i = 0; i < eta; ++i) out[i] = static_cast<int>(rng_uniform_int_m(rng, G, mG));
+  const uint64_t mG = barrett_m(G), tG = mod_barrett(0 - G, G, mG);
+  for (int i = 0; i < eta; ++i) out[i] = static_cast<int>(draw_exact(rng, G, mG, tG));
 }
 
 // ================================ K5: Eq. 5 energy =========================================
@@ -1729,8 +1732,8 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
                                                                                   w.hctr, w.hyp, w.hok, w.hiters,
                                                                                   wk)));
   SCR_LAUNCH(s, K_SAMPLES,
-             (k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, 0, w.samples_cap,
-                                                                   w.samples)));
+             (k_draw_samples<<<dim3((nA + 63) / 64, K + 1), 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta,
+                                                                                w.samples_cap, w.samples)));
   SCR_LAUNCH(s, K_COMPACT,
              (k_compact<<<nA, kCompactThreads, 0, s->stream>>>(w.hyp, w.hok, p.n_max, w.hypc, w.hslot, w.hvalid)));
   {
@@ -1747,9 +1750,6 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
                  w.cenergy, w.cslot, w.ncand, w.ncull_cap)));
   LmArgs la{0, w.samples_cap, w.ncull_cap, p.n_out, p.use_cov};
   for (int k = 1; k <= K; ++k) {
-    SCR_LAUNCH(s, K_SAMPLES,
-               (k_draw_samples<<<(nA + 63) / 64, 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta, k,
-                                                                     w.samples_cap, w.samples)));
     const int ns = p.eta * (k + 1);
     if (p.pose_update) {
       la.ns = ns;
