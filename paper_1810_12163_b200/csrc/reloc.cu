@@ -591,11 +591,16 @@ struct EnergyArgs {
 // for the re-scoring of the <= 64 survivors.
 constexpr int kSmallHyps = 64;
 
-__global__ void __launch_bounds__(256) k_energy_small(EnergyArgs ea, FrameRefs fr, PredView pv,
+#ifndef SCR_ES_THREADS
+#define SCR_ES_THREADS 512
+#endif
+constexpr int kEsThreads = SCR_ES_THREADS;  // warps per frame-tile: more samples in flight per frame
+
+__global__ void __launch_bounds__(kEsThreads) k_energy_small(EnergyArgs ea, FrameRefs fr, PredView pv,
                                                       unsigned long long* __restrict__ work) {
   extern __shared__ float es_e[];  // [kSmallHyps][eta + 1]
   __shared__ float s_pose[kSmallHyps][12];
-  __shared__ float4 s_modes[8 * 96];  // per-warp staging: 32 modes x 3 float4
+  __shared__ float4 s_modes[(kEsThreads / 32) * 96];  // per-warp staging: 32 modes x 3 float4
   const int a = blockIdx.z, b = ea.batch0 + blockIdx.y;
   const int n_all = ea.nper ? ea.nper[a] : ea.stride;
   if (n_all <= ea.min_n) return;
@@ -1739,7 +1744,7 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   {
     EnergyArgs ea{w.hypc, nullptr, p.n_max, w.hvalid, 0, w.samples, w.samples_cap, p.eta, 0, w.henergy, 0};
     const size_t smem = static_cast<size_t>(kSmallHyps) * (p.eta + 1) * sizeof(float);
-    SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<dim3((p.n_max + kSmallHyps - 1) / kSmallHyps, 1, nA), 256, smem,
+    SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<dim3((p.n_max + kSmallHyps - 1) / kSmallHyps, 1, nA), kEsThreads, smem,
                                                s->stream>>>(ea, fr, pv, wk)));
   }
   int P = 1;
@@ -1776,7 +1781,7 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
       const size_t smem_g = static_cast<size_t>(2 * L) * (p.eta + 1) * sizeof(float);
       if (L >= 32) {
         const size_t smem_small = static_cast<size_t>(kSmallHyps) * (p.eta + 1) * sizeof(float);
-        SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<grid, 256, smem_small, s->stream>>>(ea, fr, pv, wk)));
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<grid, kEsThreads, smem_small, s->stream>>>(ea, fr, pv, wk)));
       } else if (L == 16) {
         SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<16><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
       } else if (L == 8) {
