@@ -693,8 +693,13 @@ __global__ void __launch_bounds__(kEsThreads) k_energy_small(EnergyArgs ea, Fram
 // sample's predicted modes tree by tree with direct loads (the group's lanes read the same
 // addresses); the per-sample minimum does not depend on the mode order, and the batch sum
 // is taken in sample order exactly as in k_energy_small.
+#ifndef SCR_EG_THREADS
+#define SCR_EG_THREADS 512
+#endif
+constexpr int kEgThreads = SCR_EG_THREADS;
+
 template <int L>
-__global__ void __launch_bounds__(256) k_energy_grouped(EnergyArgs ea, FrameRefs fr, PredView pv,
+__global__ void __launch_bounds__(kEgThreads) k_energy_grouped(EnergyArgs ea, FrameRefs fr, PredView pv,
                                                         unsigned long long* __restrict__ work) {
   constexpr int G = 32 / L;
   extern __shared__ float es_e[];  // [2 L][eta + 1]
@@ -1783,15 +1788,15 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
         const size_t smem_small = static_cast<size_t>(kSmallHyps) * (p.eta + 1) * sizeof(float);
         SCR_LAUNCH(s, K_ENERGY, (k_energy_small<<<grid, kEsThreads, smem_small, s->stream>>>(ea, fr, pv, wk)));
       } else if (L == 16) {
-        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<16><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<16><<<grid, kEgThreads, smem_g, s->stream>>>(ea, fr, pv, wk)));
       } else if (L == 8) {
-        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<8><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<8><<<grid, kEgThreads, smem_g, s->stream>>>(ea, fr, pv, wk)));
       } else if (L == 4) {
-        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<4><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<4><<<grid, kEgThreads, smem_g, s->stream>>>(ea, fr, pv, wk)));
       } else if (L == 2) {
-        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<2><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<2><<<grid, kEgThreads, smem_g, s->stream>>>(ea, fr, pv, wk)));
       } else {
-        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<1><<<grid, 256, smem_g, s->stream>>>(ea, fr, pv, wk)));
+        SCR_LAUNCH(s, K_ENERGY, (k_energy_grouped<1><<<grid, kEgThreads, smem_g, s->stream>>>(ea, fr, pv, wk)));
       }
       SCR_LAUNCH(s, K_ENERGY, (k_energy_sum<<<nA, 64, 0, s->stream>>>(w.ncand, p.n_out, w.ncull_cap, kEnergyBatches,
                                                                       b0, k, p.pose_update ? nullptr : w.cenergy,
