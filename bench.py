@@ -397,8 +397,9 @@ def run_ours(args):
     def roof(name):
         k = kern[name]
         m = kernel_model(name, prof["work"])
+        tk = traffic.get(name) or next((v for kk, v in traffic.items() if kk.startswith(name + "<")), {})
         r = {"kernel": name, "kernel_ms": round(k["ms"], 3), "launches": k["launches"],
-             "traffic": traffic.get(name, {}).get("dram_bytes_per_launch")}
+             "traffic": tk.get("dram_bytes_per_launch")}
         if m is None or k["ms"] <= 0:
             r.update({"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None})
             return r
