@@ -192,6 +192,10 @@ scr_status scr_debug_cluster(scr_scene s, const scr_entry* e, int n, scr_mode* o
 scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_params* p, uint64_t seed,
                             int32_t* gen_slots, scr_pose* gen_poses, int* n_gen, int32_t* surv_slots,
                             scr_pose* surv_poses, float* surv_energy, int* n_surv);
+/* generation test hook: mode 1 treats every triplet passing checks 1-3 as a possibly degenerate
+   Kabsch ("suspect", decided by the exact finisher; overflows the per-frame list and exercises the
+   exact continuation), 0 restores the normal classification. Results are identical either way. */
+scr_status scr_debug_generation_mode(scr_scene s, int mode);
 scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, scr_pose* out, int* converged,
                          double* rms, double* inlier_frac, double* score);
 /* number of kernel launches issued by this scene so far (bench accounting) */

@@ -22,7 +22,7 @@ scr_status cuda_fail(cudaError_t e, const char* what);
 // ---- in-library profiler: CUDA events around every launch on the scene stream --------
 enum KernelId {
   K_PACK, K_GRID, K_LEAVES, K_HYPGEN, K_SAMPLES, K_ENERGY, K_SELECT, K_LM, K_ICP, K_FINALIZE, K_INSERT, K_RQS,
-  K_RENDER, K_COMPACT, K_COUNT
+  K_RENDER, K_COMPACT, K_HYPFIN, K_COUNT
 };
 // device work counters (u64), indexed by W_*; meaning documented in DESIGN.md "Roofline"
 enum WorkId {
@@ -89,7 +89,9 @@ struct Workspace {
   int nmax_cap = 0, ncull_cap = 0, samples_cap = 0;
   Pose* hyp = nullptr;        // [cap * nmax]
   float* henergy = nullptr;   // [cap * nmax]
-  int* hok = nullptr;         // [cap * nmax]
+  int* hok = nullptr;         // [cap * nmax] 0 failed, 1 generated, 2 tentative (k_hypgen -> k_hypfin)
+  int4* hcand = nullptr;      // [cap * nmax * 2] tentative triplet {attempt, g0, g1, g2}, {m0, m1, m2, -}
+  int4* sus = nullptr;        // [cap * kMaxSuspects * 2] passing triplets whose Kabsch may be degenerate
   int* hiters = nullptr;      // [cap * nmax]
   Pose* hypc = nullptr;       // generated hypotheses compacted in slot order [cap * nmax]
   int* hslot = nullptr;       // their generation slots [cap * nmax]
@@ -113,7 +115,7 @@ struct Workspace {
   int* fidx = nullptr;        // active frame list [cap]
   uint64_t* seeds = nullptr;  // [cap]
   int* status = nullptr;      // [cap] frame-set indices for pack_frames
-  int* hctr = nullptr;        // [cap] per-frame generation slot counters
+  int* hctr = nullptr;        // [2 * cap] per-frame generation slot counters, then suspect counts
   // reservoir insertion scratch (one frame)
   unsigned* ins_cnt = nullptr;  // [L]
   unsigned* ins_off = nullptr;  // [L + 1]
@@ -146,6 +148,7 @@ struct scr_scene_s {
   int64_t L = 0;
   int64_t cursor = 0;
   std::vector<int> node_base, leaf_base;
+  int gen_force_suspect = 0;  // scr_debug_generation_mode
   bool leaves16 = true;  // every tree has <= 65536 leaves (16-bit leaf ids in gleaf)
   int4* d_nodes = nullptr;
   short4* d_specs = nullptr;

@@ -32,6 +32,7 @@ struct GenParams {
   float colour_thresh;
   double rigidity_tol;
   int fast;  // per-pixel records usable (<= 5 trees, 16-bit leaf ids)
+  int force_suspect;  // test hook: every passing triplet is a suspect
   int leaf_base[kMaxTrees];
 };
 
@@ -128,18 +129,11 @@ SCR_DEV bool colour_ok(uint32_t col, float4 mc, float thresh) {
   return !(linf > thresh);
 }
 
-// Kabsch for a triplet that passed every check. Inlined: an out-of-line call inside the
-// attempt loop costs more (caller-saved registers around the call) than the extra code.
+// Kabsch for a triplet that passed every check (finisher kernel only).
 SCR_DEV bool kabsch3_cold(const double* cm, const double* w, Pose* T) { return kabsch3(cm, w, *T); }
 
-// Checks 2-3 (distances in f64) and Kabsch for a triplet whose colour
-// check passed. Camera points come precomputed (f64 backprojection, K1).
-// Scalars and pointers only: passing the kernel-parameter structs by reference would force
-// copies of them into local memory.
-// Checks 2-3 (distances in f64) and Kabsch for a triplet whose colour
-// check passed. Camera points come from the pixel records (x, y, depth): an f32 estimate
-// for a conservative pre-filter, then the exact f64 backprojection (geometry.hpp:194-199,
-// the same operations as K1) only for triplets the pre-filter keeps.
+// Exact f64 camera point of a pixel record (x, y, depth): geometry.hpp:194-199, the same
+// operations as K1.
 SCR_DEV void cam_point_f64(int4 rec, const FrameGeom& g, double out[3]) {
   const int x = rec.x & 0xffff, y = rec.x >> 16;
   const double dd = static_cast<double>(__int_as_float(rec.y));
@@ -148,36 +142,86 @@ SCR_DEV void cam_point_f64(int4 rec, const FrameGeom& g, double out[3]) {
   out[2] = dd;
 }
 
-SCR_DEV bool geometry_checks(double min_sq_dist, double rigidity_tol, const int4* grec, const FrameGeom& g,
-                             float ifx, float ify, const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1,
-                             int m2, Pose* T) {
+// f32 pre-filter of checks 2-3: rejects only triplets the exact f64 checks reject too (world
+// points are the same f32 values; the f32 camera points are within 1e-5 m of the f64 ones,
+// far inside the 1e-3 m / 1e-3 m^2 margins).
+SCR_DEV bool geometry_prefilter(double min_sq_dist, double rigidity_tol, const int4* grec, const FrameGeom& g,
+                                float ifx, float ify, const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1,
+                                int m2) {
   const float4 w0 = geom[m0].q0, w1 = geom[m1].q0, w2 = geom[m2].q0;
   const int4 r0 = grec[2 * g0], r1 = grec[2 * g1], r2 = grec[2 * g2];
-  {  // f32 pre-filter: rejects only triplets the exact f64 checks reject too (world points are
-     // the same f32 values; the f32 camera points are within 1e-5 m of the f64 ones, far
-     // inside the 1e-3 m / 1e-3 m^2 margins)
-    const int4 rr[3] = {r0, r1, r2};
-    float cf[3][3];
+  const int4 rr[3] = {r0, r1, r2};
+  float cf[3][3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float d = __int_as_float(rr[k].y);
-      cf[k][0] = (static_cast<float>(rr[k].x & 0xffff) - g.cx) * d * ifx;
-      cf[k][1] = (static_cast<float>(rr[k].x >> 16) - g.cy) * d * ify;
-      cf[k][2] = d;
-    }
-    const float4 wf[3] = {w0, w1, w2};
-    const float tolf = static_cast<float>(rigidity_tol) + 1e-3f;
-    const float closef = static_cast<float>(min_sq_dist) - 1e-3f;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
-      const float ax = wf[pa].x - wf[pb].x, ay = wf[pa].y - wf[pb].y, az = wf[pa].z - wf[pb].z;
-      const float bx = cf[pa][0] - cf[pb][0], by = cf[pa][1] - cf[pb][1], bz = cf[pa][2] - cf[pb][2];
-      const float dw2f = ax * ax + ay * ay + az * az, dc2f = bx * bx + by * by + bz * bz;
-      if (dw2f < closef) return false;
-      if (fabsf(sqrtf(dw2f) - sqrtf(dc2f)) > tolf) return false;
-    }
+  for (int k = 0; k < 3; ++k) {
+    const float d = __int_as_float(rr[k].y);
+    cf[k][0] = (static_cast<float>(rr[k].x & 0xffff) - g.cx) * d * ifx;
+    cf[k][1] = (static_cast<float>(rr[k].x >> 16) - g.cy) * d * ify;
+    cf[k][2] = d;
   }
+  const float4 wf[3] = {w0, w1, w2};
+  const float tolf = static_cast<float>(rigidity_tol) + 1e-3f;
+  const float closef = static_cast<float>(min_sq_dist) - 1e-3f;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
+    const float ax = wf[pa].x - wf[pb].x, ay = wf[pa].y - wf[pb].y, az = wf[pa].z - wf[pb].z;
+    const float bx = cf[pa][0] - cf[pb][0], by = cf[pa][1] - cf[pb][1], bz = cf[pa][2] - cf[pb][2];
+    const float dw2f = ax * ax + ay * ay + az * az, dc2f = bx * bx + by * by + bz * bz;
+    if (dw2f < closef) return false;
+    if (fabsf(sqrtf(dw2f) - sqrtf(dc2f)) > tolf) return false;
+  }
+  return true;
+}
+
+// Exact checks 2-3 (distances in f64) and Kabsch. Camera points are the
+// exact f64 backprojection of the records (geometry.hpp:194-199, the same operations as K1).
+// Scalars and pointers only: passing the kernel-parameter structs by reference would force
+// copies of them into local memory.
+// Kabsch on a triplet (kabsch3) is degenerate iff its computed singular values have
+// !(S0 > 0) || S1 < 1e-12 S0. The centred cross-covariance H of 3 pairs has rank <= 2, so
+// sigma0^2 sigma1^2 ~= e2 = sum of its squared 2x2 minors and sigma0^2 <= |H|_F^2: with
+// r = sqrt(e2) / |H|_F^2 <= sigma1 / sigma0 (up to ~1e-16 rounding), r > 1e-6 guarantees a
+// non-degenerate Kabsch by six orders of magnitude (the one-sided Jacobi SVD is accurate to
+// ~1e-15 S0). Triplets below that are "suspects" that k_hypfin decides with kabsch3 itself.
+SCR_DEV bool kabsch_clearly_regular(const double cm[9], const double w[9]) {
+  double cc[3], wc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    cc[k] = (cm[k] + cm[3 + k] + cm[6 + k]) / 3.0;
+    wc[k] = (w[k] + w[3 + k] + w[6 + k]) / 3.0;
+  }
+  double H[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) H[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) H[3 * r + c] += (w[3 * i + r] - wc[r]) * (cm[3 * i + c] - cc[c]);
+  double f2 = 0.0, e2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) f2 += H[i] * H[i];
+#pragma unroll
+  for (int r0 = 0; r0 < 3; ++r0)
+#pragma unroll
+    for (int r1 = r0 + 1; r1 < 3; ++r1)
+#pragma unroll
+      for (int c0 = 0; c0 < 3; ++c0)
+#pragma unroll
+        for (int c1 = c0 + 1; c1 < 3; ++c1) {
+          const double mnr = H[3 * r0 + c0] * H[3 * r1 + c1] - H[3 * r0 + c1] * H[3 * r1 + c0];
+          e2 += mnr * mnr;
+        }
+  return f2 > 0.0 && sqrt(e2) > 1e-6 * f2;
+}
+
+SCR_DEV bool distance_checks_f64(double min_sq_dist, double rigidity_tol, const int4* grec, const FrameGeom& g,
+                                 const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1, int m2,
+                                 double* cm_out, double* w_out, bool* regular = nullptr) {
+  const float4 w0 = geom[m0].q0, w1 = geom[m1].q0, w2 = geom[m2].q0;
+  const int4 r0 = grec[2 * g0], r1 = grec[2 * g1], r2 = grec[2 * g2];
   double w[9] = {w0.x, w0.y, w0.z, w1.x, w1.y, w1.z, w2.x, w2.y, w2.z};
   double cm[9];
   cam_point_f64(r0, g, cm);
@@ -198,10 +242,74 @@ SCR_DEV bool geometry_checks(double min_sq_dist, double rigidity_tol, const int4
 #pragma unroll
   for (int q = 0; q < 3; ++q)
     if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > rigidity_tol) return false;
+  if (cm_out) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      cm_out[i] = cm[i];
+      w_out[i] = w[i];
+    }
+  }
+  if (regular) *regular = kabsch_clearly_regular(cm, w);
+  return true;
+}
+
+SCR_DEV bool geometry_exact(double min_sq_dist, double rigidity_tol, const int4* grec, const FrameGeom& g,
+                            const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1, int m2, Pose* T) {
+  double cm[9], w[9];
+  if (!distance_checks_f64(min_sq_dist, rigidity_tol, grec, g, geom, g0, g1, g2, m0, m1, m2, cm, w)) return false;
   return kabsch3_cold(cm, w, T);
 }
 
+// One generation attempt on the exact sequential path (draw order A1/A7):
+// draws pixel, mode, pixel, mode, pixel, mode, colour-pair index from the slot stream with
+// rejection sampling, returns whether the attempt reached the colour check and passed it.
+SCR_DEV bool attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, const PredView& pv,
+                           const int* s_lbase, const uint64_t* s_m, const uint64_t* s_thr, size_t fbase, uint64_t G,
+                           uint64_t mG, uint64_t tG, bool fast, int& g0, int& g1, int& g2, int& m0, int& m1,
+                           int& m2) {
+  constexpr uint64_t m3 = 0x5555555555555555ull, t3 = 1;  // floor((2^64-1)/3), 2^64 mod 3
+  int p0 = 0, p1 = 0, p2 = 0, cc = 0;
+  int4 A0, A1, A2;
+  uint4 L0, L1, L2;
+  g0 = static_cast<int>(draw_exact(rng, G, mG, tG));
+  A0 = fr.grec[2 * (fbase + g0)];
+  L0 = fr.gleaf[2 * (fbase + g0) + 1];
+  const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
+  if (nm0 <= 0) return false;
+  p0 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
+  g1 = static_cast<int>(draw_exact(rng, G, mG, tG));
+  A1 = fr.grec[2 * (fbase + g1)];
+  L1 = fr.gleaf[2 * (fbase + g1) + 1];
+  const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
+  if (nm1 <= 0) return false;
+  p1 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
+  g2 = static_cast<int>(draw_exact(rng, G, mG, tG));
+  A2 = fr.grec[2 * (fbase + g2)];
+  L2 = fr.gleaf[2 * (fbase + g2) + 1];
+  const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
+  if (nm2 <= 0) return false;
+  p2 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
+  cc = static_cast<int>(draw_exact(rng, 3, m3, t3));
+  if (fast) {
+    m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), L0, p0);
+    m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), L1, p1);
+    m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), L2, p2);
+  } else {
+    m0 = mode_index(fr, pv.count, fbase + g0, p0);
+    m1 = mode_index(fr, pv.count, fbase + g1, p1);
+    m2 = mode_index(fr, pv.count, fbase + g2, p2);
+  }
+  const uint32_t col = static_cast<uint32_t>(cc == 0 ? A0.z : (cc == 1 ? A1.z : A2.z));
+  return colour_ok(col, pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)], gp.colour_thresh);
+}
+
 // Per-warp queue of colour-check survivors, evaluated 32 at a time at full SIMD width.
+// They get the f32 pre-filter and the exact f64 checks 2-3 here; Kabsch (a 3x3 f64 SVD) is
+// left to k_hypfin, which keeps the SVD's code and registers out of the attempt loop. A slot
+// stops at its first passing attempt whose Kabsch is provably regular (hok = 2, attempt +
+// triplet in hcand); passing attempts whose Kabsch may be degenerate are listed as per-frame
+// suspects and the slot goes on, so k_hypfin never has to re-run a slot's attempt chain
+// (unless the suspect list overflows).
 #ifndef SCR_HYPGEN_MINB
 #define SCR_HYPGEN_MINB 2  // resident CTAs per SM the register budget is sized for (16 warps)
 #endif
@@ -210,6 +318,7 @@ SCR_DEV bool geometry_checks(double min_sq_dist, double rigidity_tol, const int4
 #endif
 constexpr int kGenWarps = SCR_GEN_WARPS;  // warps per generation CTA
 constexpr int kGenQ = 64;
+constexpr int kMaxSuspects = 64;  // per frame: triplets whose Kabsch may be degenerate
 struct GenCand {
   int slot, owner_att;  // owner lane | attempt << 5
   int g0, g1, g2, m0, m1, m2;
@@ -217,8 +326,9 @@ struct GenCand {
 
 __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
                                                    const uint64_t* __restrict__ seeds, int* __restrict__ slot_ctr,
-                                                   Pose* __restrict__ hyp, int* __restrict__ hok,
-                                                   int* __restrict__ hiters, unsigned long long* __restrict__ work) {
+                                                   int4* __restrict__ hcand, int* __restrict__ hok,
+                                                   int* __restrict__ hiters, int* __restrict__ sus_cnt,
+                                                   int4* __restrict__ sus, unsigned long long* __restrict__ work) {
   __shared__ uint64_t s_m[kMaxModeUnion + 1];    // Barrett reciprocal for mode counts 1..400
   __shared__ uint64_t s_thr[kMaxModeUnion + 1];  // rejection threshold (2^64 mod n)
   __shared__ int s_lbase[kMaxTrees];
@@ -243,7 +353,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
   const uint64_t G = static_cast<uint64_t>(fr.gcount[f]);
   const uint64_t mG = G ? barrett_m(G) : 1, tG = G ? mod_barrett(0 - G, G, mG) : 0;
   const uint32_t G32 = static_cast<uint32_t>(G);
-  const uint64_t m3 = 0x5555555555555555ull, t3 = 1;  // floor((2^64-1)/3), 2^64 mod 3
+  const uint64_t m3 = 0x5555555555555555ull;  // floor((2^64-1)/3)
   const bool fast = gp.fast != 0;
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
   const float ifx = 1.0f / g.fx, ify = 1.0f / g.fy;  // f32 pre-filter only
@@ -329,52 +439,13 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
         }
       } else {  // exact sequential replay of the attempt from the saved stream state
         rng = saved;
-        int g0 = 0, g1 = 0, g2 = 0, p0 = 0, p1 = 0, p2 = 0, cc = 0;
-        int4 A0, A1, A2;
-        uint4 L0, L1, L2;
-        bool proceed = false;
-        g0 = static_cast<int>(draw_exact(rng, G, mG, tG));
-        A0 = fr.grec[2 * (fbase + g0)];
-        L0 = fr.gleaf[2 * (fbase + g0) + 1];
-        const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
-        if (nm0 > 0) {
-          p0 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
-          g1 = static_cast<int>(draw_exact(rng, G, mG, tG));
-          A1 = fr.grec[2 * (fbase + g1)];
-          L1 = fr.gleaf[2 * (fbase + g1) + 1];
-          const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
-          if (nm1 > 0) {
-            p1 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
-            g2 = static_cast<int>(draw_exact(rng, G, mG, tG));
-            A2 = fr.grec[2 * (fbase + g2)];
-            L2 = fr.gleaf[2 * (fbase + g2) + 1];
-            const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
-            if (nm2 > 0) {
-              p2 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
-              cc = static_cast<int>(draw_exact(rng, 3, m3, t3));
-              proceed = true;
-            }
-          }
-        }
-        if (proceed) {
-          int m0, m1, m2;
-          if (fast) {
-            m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), L0, p0);
-            m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), L1, p1);
-            m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), L2, p2);
-          } else {
-            m0 = mode_index(fr, pv.count, fbase + g0, p0);
-            m1 = mode_index(fr, pv.count, fbase + g1, p1);
-            m2 = mode_index(fr, pv.count, fbase + g2, p2);
-          }
-          const uint32_t col = static_cast<uint32_t>(cc == 0 ? A0.z : (cc == 1 ? A1.z : A2.z));
-          if (colour_ok(col, pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)], gp.colour_thresh)) {
-            push = true;
-            c.slot = slot;
-            c.owner_att = lane | (it << 5);
-            c.g0 = g0; c.g1 = g1; c.g2 = g2;
-            c.m0 = m0; c.m1 = m1; c.m2 = m2;
-          }
+        int g0, g1, g2, m0, m1, m2;
+        if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, s_thr, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2)) {
+          push = true;
+          c.slot = slot;
+          c.owner_att = lane | (it << 5);
+          c.g0 = g0; c.g1 = g1; c.g2 = g2;
+          c.m0 = m0; c.m1 = m1; c.m2 = m2;
         }
       }
       if (push) s_pend[wid][lane] += 1;
@@ -400,20 +471,37 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
       const int nproc = qn < 32 ? qn : 32;
       bool pass = false;
       int owner = 0, att = 0, eslot = -1;
-      Pose T;
+      GenCand e;
       if (lane < nproc) {
-        const GenCand e = q[lane];
+        e = q[lane];
         owner = e.owner_att & 31;
         att = e.owner_att >> 5;
         eslot = e.slot;
         if (s_cur[wid][owner] == eslot) {  // stale if the owner's slot was already resolved
-          pass = geometry_checks(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, ifx, ify, pv.geom, e.g0, e.g1, e.g2, e.m0, e.m1, e.m2, &T);
+          bool regular = true;
+          pass = geometry_prefilter(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, ifx, ify, pv.geom,
+                                    e.g0, e.g1, e.g2, e.m0, e.m1, e.m2) &&
+                 distance_checks_f64(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, pv.geom, e.g0, e.g1,
+                                     e.g2, e.m0, e.m1, e.m2, nullptr, nullptr, &regular);
+          if (pass && (!regular || gp.force_suspect)) {  // Kabsch may be degenerate: k_hypfin decides, the slot goes on
+            const int i = atomicAdd(&sus_cnt[a], 1);
+            if (i < kMaxSuspects) {
+              int4* sp = sus + 2 * (static_cast<size_t>(a) * kMaxSuspects + i);
+              sp[0] = make_int4(att, e.g0, e.g1, e.g2);
+              sp[1] = make_int4(e.m0, e.m1, e.m2, eslot);
+              pass = false;
+            }  // list full: stop here as usual, k_hypfin continues exactly if Kabsch fails
+          }
           atomicSub(&s_pend[wid][owner], 1);
           if (pass) atomicMin(&s_best[wid][owner], att);
         }
       }
       __syncwarp();
-      if (pass && s_best[wid][owner] == att) hyp[static_cast<size_t>(a) * gp.nmax + eslot] = T;
+      if (pass && s_best[wid][owner] == att) {
+        int4* hc = hcand + 2 * (static_cast<size_t>(a) * gp.nmax + eslot);
+        hc[0] = make_int4(att, e.g0, e.g1, e.g2);
+        hc[1] = make_int4(e.m0, e.m1, e.m2, 0);
+      }
       // drop the evaluated entries
       GenCand keep;
       const int rest = qn - nproc;
@@ -425,7 +513,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
       if (slot >= 0 && s_best[wid][lane] != 0x7fffffff) {
         const int best = s_best[wid][lane];
         const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
-        hok[out] = 1;
+        hok[out] = 2;  // tentative: k_hypfin decides
         hiters[out] = best + 1;
         attempts_total += static_cast<unsigned long long>(best + 1);
         s_best[wid][lane] = 0x7fffffff;
@@ -444,6 +532,112 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
     }
   }
   if (work) work_add(work, W_GEN_ATTEMPTS, static_cast<unsigned>(attempts_total));
+}
+
+// Exact finisher of generation: thread per (frame, slot). k_hypgen stopped a slot at its
+// first attempt passing the exact checks 2-3 with a clearly regular Kabsch (hok = 2,
+// triplet in hcand) and listed the earlier passing attempts whose Kabsch may be degenerate
+// ("suspects", per frame). The slot's result is its first attempt whose Kabsch succeeds
+// (SPEC.md:441-447): suspects in attempt order, then the recorded triplet. Only when the
+// suspect list overflowed can the recorded triplet itself be degenerate; the slot then
+// continues on the exact sequential path (stream replayed through the recorded attempt).
+constexpr int kFinThreads = 128;
+__global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
+                                                        const uint64_t* __restrict__ seeds,
+                                                        const int4* __restrict__ hcand, Pose* __restrict__ hyp,
+                                                        int* __restrict__ hok, int* __restrict__ hiters,
+                                                        const int* __restrict__ sus_cnt, const int4* __restrict__ sus,
+                                                        unsigned long long* __restrict__ work) {
+  __shared__ uint64_t s_m[kMaxModeUnion + 1];
+  __shared__ uint64_t s_thr[kMaxModeUnion + 1];
+  __shared__ int s_lbase[kMaxTrees];
+  __shared__ int4 s_sus[kMaxSuspects][2];
+  const int a = blockIdx.y;
+  const int slot = blockIdx.x * kFinThreads + threadIdx.x;
+  const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
+  const int ns = min(sus_cnt[a], kMaxSuspects);
+  for (int i = threadIdx.x; i < 2 * ns; i += blockDim.x) s_sus[i >> 1][i & 1] = sus[2 * static_cast<size_t>(a) * kMaxSuspects + i];
+  const bool clear = slot < gp.nmax && hok[out] == 2;
+#ifdef SCR_FIN_DEBUG
+  if (threadIdx.x == 0 && blockIdx.x == 0 && sus_cnt[a]) printf("hypfin-sus a=%d n=%d\n", a, sus_cnt[a]);
+#endif
+  if (!__syncthreads_or(clear) && ns == 0) return;
+  const int f = fr.fidx[a];
+  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  const int4* grec = fr.grec + 2 * fbase;
+  int4 c0 = make_int4(0x7fffffff, 0, 0, 0), c1 = make_int4(0, 0, 0, 0);
+  if (clear) {
+    c0 = hcand[2 * out];
+    c1 = hcand[2 * out + 1];
+  }
+  Pose T;
+  bool ok = false;
+  int res_it = 0;
+  if (slot < gp.nmax) {
+    int last = -1;
+    for (;;) {  // this slot's suspects before the recorded attempt, in attempt order
+      int best = -1, batt = c0.x;
+      for (int i = 0; i < ns; ++i)
+        if (s_sus[i][1].w == slot && s_sus[i][0].x > last && s_sus[i][0].x < batt) {
+          best = i;
+          batt = s_sus[i][0].x;
+        }
+      if (best < 0) break;
+      last = batt;
+      const int4 u0 = s_sus[best][0], u1 = s_sus[best][1];
+      if (geometry_exact(gp.min_sq_dist, gp.rigidity_tol, grec, g, pv.geom, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, &T)) {
+        ok = true;
+        res_it = u0.x + 1;
+        break;
+      }
+    }
+    if (!ok && clear &&
+        geometry_exact(gp.min_sq_dist, gp.rigidity_tol, grec, g, pv.geom, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, &T)) {
+      ok = true;
+      res_it = c0.x + 1;
+    }
+    if (ok) {
+      hyp[out] = T;
+      hok[out] = 1;
+      hiters[out] = res_it;
+    } else if (clear && ns < kMaxSuspects) {  // cannot happen: the recorded Kabsch is clearly regular
+      hok[out] = 0;
+    }
+  }
+  const bool cont = clear && !ok && ns >= kMaxSuspects;
+  if (!__syncthreads_or(cont)) return;
+  // continuation on the exact path (suspect list overflowed): the tables the draws need
+  for (int i = threadIdx.x; i <= kMaxModeUnion; i += blockDim.x) {
+    const uint64_t n = i ? static_cast<uint64_t>(i) : 1;
+    const uint64_t m = barrett_m(n);
+    s_m[i] = m;
+    s_thr[i] = mod_barrett(0 - n, n, m);
+  }
+  if (threadIdx.x < kMaxTrees) s_lbase[threadIdx.x] = gp.leaf_base[threadIdx.x];
+  __syncthreads();
+  if (!cont) return;
+  const uint64_t G = static_cast<uint64_t>(fr.gcount[f]);
+  const uint64_t mG = barrett_m(G), tG = mod_barrett(0 - G, G, mG);
+  const float ifx = 1.0f / g.fx, ify = 1.0f / g.fy;
+  const bool fast = gp.fast != 0;
+  Rng rng = rng_stream(seeds[a], static_cast<uint64_t>(slot));
+  const int att = c0.x;
+  int it = 0;
+  int g0, g1, g2, m0, m1, m2;
+  for (; it <= att; ++it)  // replay through the recorded attempt
+    attempt_exact(rng, gp, fr, pv, s_lbase, s_m, s_thr, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2);
+  for (; it < gp.max_iters && !ok; ++it) {
+    if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, s_thr, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2) &&
+        geometry_prefilter(gp.min_sq_dist, gp.rigidity_tol, grec, g, ifx, ify, pv.geom, g0, g1, g2, m0, m1, m2))
+      ok = geometry_exact(gp.min_sq_dist, gp.rigidity_tol, grec, g, pv.geom, g0, g1, g2, m0, m1, m2, &T);
+  }
+#ifdef SCR_FIN_DEBUG
+  printf("hypfin-cont a=%d slot=%d att=%d it=%d ok=%d\n", a, slot, att, it, ok ? 1 : 0);
+#endif
+  if (ok) hyp[out] = T;
+  hok[out] = ok ? 1 : 0;
+  hiters[out] = it;  // ok: the passing attempt + 1; otherwise max_iters
+  if (work) atomicAdd(&work[W_GEN_ATTEMPTS], static_cast<unsigned long long>(it - (att + 1)));
 }
 
 // Sample batch k of frame a: eta draws of uniform_int(G) from Rng::stream(seed, nmax + k).
@@ -1732,15 +1926,19 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   const FrameRefs fr = frame_refs(s);
   const PredView pv = s->pred_view();
   GenParams gp{p.max_gen_iters, p.n_max, p.min_sq_dist, p.colour_thresh, p.rigidity_tol,
-               (s->T <= 5 && s->leaves16) ? 1 : 0, {0}};
+               (s->T <= 5 && s->leaves16) ? 1 : 0, s->gen_force_suspect, {0}};
   for (int t = 0; t < s->T && t < kMaxTrees; ++t) gp.leaf_base[t] = s->leaf_base[t];
   unsigned long long* wk = work_ptr(s);
   SCR_CUDA(cudaMemsetAsync(w.hctr, 0, nA * sizeof(int), s->stream));  // per-frame slot counters
+  SCR_CUDA(cudaMemsetAsync(w.hctr + w.cap, 0, nA * sizeof(int), s->stream));  // per-frame suspect counts
   const int gen_threads = std::min(p.n_max, kGenThreadsPerFrame);
   SCR_LAUNCH(s, K_HYPGEN,
              (k_hypgen<<<dim3((gen_threads + kGenWarps * 32 - 1) / (kGenWarps * 32), nA), kGenWarps * 32, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds,
-                                                                                  w.hctr, w.hyp, w.hok, w.hiters,
-                                                                                  wk)));
+                                                                                  w.hctr, w.hcand, w.hok, w.hiters,
+                                                                                  w.hctr + w.cap, w.sus, wk)));
+  SCR_LAUNCH(s, K_HYPFIN,
+             (k_hypfin<<<dim3((p.n_max + kFinThreads - 1) / kFinThreads, nA), kFinThreads, 0, s->stream>>>(
+                 gp, s->geom, fr, pv, w.seeds, w.hcand, w.hyp, w.hok, w.hiters, w.hctr + w.cap, w.sus, wk)));
   SCR_LAUNCH(s, K_SAMPLES,
              (k_draw_samples<<<dim3((nA + 63) / 64, K + 1), 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta,
                                                                                 w.samples_cap, w.samples)));
@@ -1852,6 +2050,8 @@ scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int scap) {
     SCR_TRY(grow(&w.hyp, B * nmax));
     SCR_TRY(grow(&w.henergy, B * std::max(nmax, 64)));
     SCR_TRY(grow(&w.hok, B * nmax));
+    SCR_TRY(grow(&w.hcand, 2 * B * nmax));
+    SCR_TRY(grow(&w.sus, 2 * B * kMaxSuspects));
     SCR_TRY(grow(&w.hiters, B * nmax));
     SCR_TRY(grow(&w.hypc, B * nmax));
     SCR_TRY(grow(&w.hslot, B * nmax));
@@ -2081,6 +2281,15 @@ scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_pa
   }
   *n_surv = nc;
   return g == 0 ? SCR_E_NO_HYPOTHESES : SCR_OK;
+}
+
+scr_status scr_debug_generation_mode(scr_scene s, int mode) {
+  if (!s || mode < 0 || mode > 1) {
+    scr::set_error("scr_debug_generation_mode: bad scene or mode");
+    return SCR_E_ARG;
+  }
+  s->gen_force_suspect = mode;
+  return SCR_OK;
 }
 
 scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, scr_pose* out, int* converged,

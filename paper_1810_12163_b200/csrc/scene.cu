@@ -52,7 +52,7 @@ void prof_flush(scr_scene s) {
 
 const char* const kKernelNames[K_COUNT] = {"k_pack", "k_grid", "k_leaves", "k_hypgen", "k_draw_samples", "k_energy",
                                            "k_select", "k_lm", "k_icp_score", "k_finalize", "k_insert", "k_rqs",
-                                           "k_render", "k_compact"};
+                                           "k_render", "k_compact", "k_hypfin"};
 scr_status cuda_fail(cudaError_t e, const char* what) {
   g_err = std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what;
   return e == cudaErrorMemoryAllocation ? SCR_E_OOM : SCR_E_CUDA;
@@ -664,7 +664,7 @@ scr_status alloc_workspace(scr_scene s, int max_batch) {
   if ((st = dalloc(&w.fidx, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.status, B)) != SCR_OK) return st;
-  if ((st = dalloc(&w.hctr, B)) != SCR_OK) return st;
+  if ((st = dalloc(&w.hctr, 2 * B)) != SCR_OK) return st;  // slot counters, then suspect counts
   if ((st = dalloc(&w.d_res, B)) != SCR_OK) return st;
   SCR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w.h_res), B * sizeof(scr_result)));
   SCR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w.h_idx), B * sizeof(int)));
@@ -930,7 +930,7 @@ void scr_scene_destroy(scr_scene s) {
   if (s->ws.d_res) cudaFree(s->ws.d_res);
   void* ptrs[] = {s->d_nodes, s->d_specs, s->d_entries, s->d_seen, s->d_count, s->d_geom, s->d_col, s->d_cov,
                   s->d_prims, s->ws.depth, s->ws.rgb, s->ws.tex, s->ws.gcount, s->ws.gpx, s->ws.gcam, s->ws.gslot,
-                  s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hiters, s->ws.cand, s->ws.cenergy,
+                  s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hcand, s->ws.sus, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
                   s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.dplane, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,

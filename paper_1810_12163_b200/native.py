@@ -146,6 +146,7 @@ SIGNATURES = {
     "scr_debug_cluster": (C.c_int, [_vp, _vp, C.c_int, _vp, _P(_i32), _P(C.c_int)]),
     "scr_debug_ransac": (C.c_int, [_vp, _P(Frame), _P(RansacParams), _u64, _P(_i32), _P(Pose), _P(C.c_int),
                                    _P(_i32), _P(Pose), _P(_flt), _P(C.c_int)]),
+    "scr_debug_generation_mode": (C.c_int, [_vp, C.c_int]),
     "scr_debug_icp": (C.c_int, [_vp, _P(Frame), _P(Pose), _P(Pose), _P(C.c_int), _P(_dbl), _P(_dbl), _P(_dbl)]),
     "scr_kernel_launches": (_i64, [_vp]),
     "scr_profile_enable": (C.c_int, [_vp, C.c_int]),

@@ -336,6 +336,10 @@ class Scene:
                                        C.byref(ng), N.ptr(ss, C.c_int32), sp, N.ptr(se, C.c_float), C.byref(ns))
         return st, gs[: ng.value], list(gp)[: ng.value], ss[: ns.value], list(sp)[: ns.value], se[: ns.value]
 
+    def debug_generation_mode(self, mode: int) -> None:
+        """Test hook: 1 = every passing triplet goes through the exact suspect/continuation path."""
+        N.check(self.lib.scr_debug_generation_mode(self.handle, int(mode)), "debug_generation_mode")
+
     def debug_icp(self, depth, rgb, init):
         arr, keep = _frames([depth], [rgb])
         p = to_pose(init)

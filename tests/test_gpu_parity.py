@@ -106,12 +106,12 @@ def test_cluster_kernel_matches_oracle(oracle, gscene):
         assert gm.tobytes() == om.tobytes()
 
 
-def test_ransac_bit_exact(oracle, world, gscene):
-    for i in range(2):
+def _ransac_matches_oracle(oracle, world, gscene, frames):
+    import paper_1810_12163_b200 as P
+
+    for i in frames:
         for prof in ("default", "fast"):
             p = of.ransac_params(prof)
-            import paper_1810_12163_b200 as P
-
             gp = P.ransac_params(prof)
             st, gs, gpz, ss, sp, se = gscene.debug_ransac(world.Dt[i], world.RGBt[i], gp, 100 + i)
             rc, ogs, ogp, oss, osp, ose = oracle.ransac(world.forest, world.state, world.Dt[i], world.RGBt[i], K, p,
@@ -124,6 +124,21 @@ def test_ransac_bit_exact(oracle, world, gscene):
                 R, t = of.pose_np(b)
                 ga = np.array(a.R[:]).reshape(3, 3)
                 assert np.abs(ga - R).max() < 1e-9 and np.abs(np.array(a.t[:]) - t).max() < 1e-9
+
+
+def test_ransac_bit_exact(oracle, world, gscene):
+    _ransac_matches_oracle(oracle, world, gscene, range(2))
+
+
+def test_ransac_exact_finisher_paths(oracle, world, gscene):
+    """Every passing triplet routed through the generation finisher as a possibly degenerate
+    Kabsch: suspect ordering, suspect-list overflow and the exact sequential continuation must
+    all reproduce the sequential reference bit for bit."""
+    gscene.debug_generation_mode(1)
+    try:
+        _ransac_matches_oracle(oracle, world, gscene, range(1))
+    finally:
+        gscene.debug_generation_mode(0)
 
 
 def test_icp_matches_oracle(oracle, world, gscene):

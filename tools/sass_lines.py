@@ -37,6 +37,20 @@ def sass_rows(rep: str, kernel: str):
     return name, out
 
 
+def mangled_sub(kernel: str, demangled: str) -> str:
+    """Substring of the mangled name selecting exactly the profiled instantiation
+    (k_icp_score<(bool)0> -> k_icp_scoreILb0E); SASS_FN overrides."""
+    if os.environ.get("SASS_FN"):
+        return os.environ["SASS_FN"]
+    m = re.search(re.escape(kernel) + r"<\(bool\)(\d)>", demangled)
+    if m:
+        return f"{kernel}ILb{m.group(1)}E"
+    m = re.search(re.escape(kernel) + r"<(\d+)>", demangled)
+    if m:
+        return f"{kernel}ILi{m.group(1)}E"
+    return kernel
+
+
 def line_map(kernel_mangled_sub: str):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", LIB], cwd=tmp, capture_output=True)
@@ -69,7 +83,7 @@ def main():
     by_exec = len(sys.argv) > 4 and sys.argv[4] == "exec"
     name, rows = sass_rows(rep, kernel)
     base = int(rows[0]["Address"], 16)
-    lm = line_map(kernel)
+    lm = line_map(mangled_sub(kernel, name))
     samples = collections.Counter()
     execd = collections.Counter()
     tot = 0
@@ -100,7 +114,7 @@ def dump_line(rep: str, kernel: str, fname: str, line: int):
     """SASS of one source line with executed counts (debug helper)."""
     name, rows = sass_rows(rep, kernel)
     base = int(rows[0]["Address"], 16)
-    lm = line_map(kernel)
+    lm = line_map(mangled_sub(kernel, name))
     for r in rows:
         off = int(r["Address"], 16) - base
         if lm.get(off) == (fname, line):
