@@ -319,10 +319,18 @@ SCR_DEV bool attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, c
 constexpr int kGenWarps = SCR_GEN_WARPS;  // warps per generation CTA
 constexpr int kGenQ = 64;
 constexpr int kMaxSuspects = 64;  // per frame: triplets whose Kabsch may be degenerate
+// A queued colour-check survivor. Fast-path entries carry the three raw mode draws and are
+// resolved to mode indices in the evaluation phase (at full SIMD width, instead of by the
+// few passing lanes of every attempt round); exact-path entries carry resolved modes.
+constexpr int kCandResolved = 1 << 30;  // flag in slot: m0..m2 hold mode indices
 struct GenCand {
-  int slot, owner_att;  // owner lane | attempt << 5
-  int g0, g1, g2, m0, m1, m2;
+  int slot, owner_att;  // slot (| kCandResolved), owner lane | attempt << 5
+  int g0, g1, g2;
+  uint2 r0, r1, r2;     // raw 64-bit draws of the three modes, or {m, 0}
 };
+
+SCR_DEV uint64_t u64_of(uint2 v) { return static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32); }
+SCR_DEV uint2 u2_of(uint64_t v) { return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32)); }
 
 __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv,
                                                    const uint64_t* __restrict__ seeds, int* __restrict__ slot_ctr,
@@ -426,26 +434,21 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
           for (int j = 0; j < k; ++j) rng_next(rng);
         }
         if (full && colour_ok(static_cast<uint32_t>(Ac.z), mcol, gp.colour_thresh)) {
-          const int p0 = static_cast<int>(mod_barrett32(r0, nm0, s_m[nm0]));
-          const int p1 = static_cast<int>(mod_barrett32(r1, nm1, s_m[nm1]));
-          const int p2 = static_cast<int>(mod_barrett32(r2, nm2, s_m[nm2]));
           push = true;
           c.slot = slot;
           c.owner_att = lane | (it << 5);
           c.g0 = g0; c.g1 = g1; c.g2 = g2;
-          c.m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), fr.gleaf[2 * (fbase + g0) + 1], p0);
-          c.m1 = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), fr.gleaf[2 * (fbase + g1) + 1], p1);
-          c.m2 = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), fr.gleaf[2 * (fbase + g2) + 1], p2);
+          c.r0 = u2_of(r0); c.r1 = u2_of(r1); c.r2 = u2_of(r2);
         }
       } else {  // exact sequential replay of the attempt from the saved stream state
         rng = saved;
         int g0, g1, g2, m0, m1, m2;
         if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, s_thr, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2)) {
           push = true;
-          c.slot = slot;
+          c.slot = slot | kCandResolved;
           c.owner_att = lane | (it << 5);
           c.g0 = g0; c.g1 = g1; c.g2 = g2;
-          c.m0 = m0; c.m1 = m1; c.m2 = m2;
+          c.r0 = make_uint2(m0, 0); c.r1 = make_uint2(m1, 0); c.r2 = make_uint2(m2, 0);
         }
       }
       if (push) s_pend[wid][lane] += 1;
@@ -476,19 +479,34 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
         e = q[lane];
         owner = e.owner_att & 31;
         att = e.owner_att >> 5;
-        eslot = e.slot;
+        eslot = e.slot & ~kCandResolved;
         if (s_cur[wid][owner] == eslot) {  // stale if the owner's slot was already resolved
+          if (!(e.slot & kCandResolved)) {  // mode indices of the three raw draws (fast path)
+            const int4* gr = fr.grec + 2 * fbase;
+            const int4 A0 = gr[2 * e.g0], A1 = gr[2 * e.g1], A2 = gr[2 * e.g2];
+            const uint4 L0 = fr.gleaf[2 * (fbase + e.g0) + 1], L1 = fr.gleaf[2 * (fbase + e.g1) + 1],
+                        L2 = fr.gleaf[2 * (fbase + e.g2) + 1];
+            const uint32_t nm0 = static_cast<uint32_t>(A0.z) >> 24, nm1 = static_cast<uint32_t>(A1.z) >> 24,
+                           nm2 = static_cast<uint32_t>(A2.z) >> 24;
+            const int p0 = static_cast<int>(mod_barrett32(u64_of(e.r0), nm0, s_m[nm0]));
+            const int p1 = static_cast<int>(mod_barrett32(u64_of(e.r1), nm1, s_m[nm1]));
+            const int p2 = static_cast<int>(mod_barrett32(u64_of(e.r2), nm2, s_m[nm2]));
+            e.r0.x = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), L0, p0);
+            e.r1.x = mode_from_record(s_lbase, static_cast<uint32_t>(A1.w), L1, p1);
+            e.r2.x = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), L2, p2);
+          }
+          const int em0 = static_cast<int>(e.r0.x), em1 = static_cast<int>(e.r1.x), em2 = static_cast<int>(e.r2.x);
           bool regular = true;
           pass = geometry_prefilter(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, ifx, ify, pv.geom,
-                                    e.g0, e.g1, e.g2, e.m0, e.m1, e.m2) &&
+                                    e.g0, e.g1, e.g2, em0, em1, em2) &&
                  distance_checks_f64(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, pv.geom, e.g0, e.g1,
-                                     e.g2, e.m0, e.m1, e.m2, nullptr, nullptr, &regular);
+                                     e.g2, em0, em1, em2, nullptr, nullptr, &regular);
           if (pass && (!regular || gp.force_suspect)) {  // Kabsch may be degenerate: k_hypfin decides, the slot goes on
             const int i = atomicAdd(&sus_cnt[a], 1);
             if (i < kMaxSuspects) {
               int4* sp = sus + 2 * (static_cast<size_t>(a) * kMaxSuspects + i);
               sp[0] = make_int4(att, e.g0, e.g1, e.g2);
-              sp[1] = make_int4(e.m0, e.m1, e.m2, eslot);
+              sp[1] = make_int4(em0, em1, em2, eslot);
               pass = false;
             }  // list full: stop here as usual, k_hypfin continues exactly if Kabsch fails
           }
@@ -500,7 +518,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
       if (pass && s_best[wid][owner] == att) {
         int4* hc = hcand + 2 * (static_cast<size_t>(a) * gp.nmax + eslot);
         hc[0] = make_int4(att, e.g0, e.g1, e.g2);
-        hc[1] = make_int4(e.m0, e.m1, e.m2, 0);
+        hc[1] = make_int4(static_cast<int>(e.r0.x), static_cast<int>(e.r1.x), static_cast<int>(e.r2.x), 0);
       }
       // drop the evaluated entries
       GenCand keep;
