@@ -212,9 +212,14 @@ def run_ours(args):
 
     rank, local, world = dist_env()
     dist = None
+    # Test hook for the N>1 path on a single GPU (tests/test_gpu_bench_ranks.py): every rank on
+    # device 0 and gloo for the host-side barrier/broadcast/reductions. The ranks' kernels never
+    # wait on each other (no per-frame collective), so this only exercises the plumbing.
+    if os.environ.get("SCR_BENCH_ONE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist = dist_init("nccl")
+        dist = dist_init(os.environ.get("SCR_BENCH_BACKEND", "nccl"))
     dev_t = torch.device("cuda", local)
 
     dev = P.Device(local)
