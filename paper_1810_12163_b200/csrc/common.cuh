@@ -484,12 +484,14 @@ SCR_DEV void ray_dir_tab(const float R[9], float dcx, float dcy, float d[3]) {
   for (int i = 0; i < 3; ++i) d[i] = __fmaf_rn(R[3 * i + 0], dcx, __fmaf_rn(R[3 * i + 1], dcy, R[3 * i + 2]));
 }
 
+// Ray casts use __frcp_rn(x) for 1/x: the correctly rounded reciprocal, bit-identical to the
+// IEEE division 1.0f / x of the oracle (including 0 -> inf), with a shorter instruction sequence.
 SCR_DEV Hit raycast(const Prim* prims, int n, const float o[3], const float d[3]) {
   Hit h;
   h.t = __int_as_float(0x7f800000);
   h.prim = -1;
   h.face = -1;
-  const float inv0 = __fdiv_rn(1.0f, d[0]), inv1 = __fdiv_rn(1.0f, d[1]), inv2 = __fdiv_rn(1.0f, d[2]);
+  const float inv0 = __frcp_rn(d[0]), inv1 = __frcp_rn(d[1]), inv2 = __frcp_rn(d[2]);
   const float aa = __fmaf_rn(d[0], d[0], __fmaf_rn(d[1], d[1], __fmul_rn(d[2], d[2])));
   for (int p = 0; p < n; ++p) {
     const Prim& q = prims[p];
@@ -535,7 +537,7 @@ SCR_DEV Hit raycast_list(const Prim* prims, const unsigned char* list, int nl, c
   h.t = __int_as_float(0x7f800000);
   h.prim = -1;
   h.face = -1;
-  const float inv0 = __fdiv_rn(1.0f, d[0]), inv1 = __fdiv_rn(1.0f, d[1]), inv2 = __fdiv_rn(1.0f, d[2]);
+  const float inv0 = __frcp_rn(d[0]), inv1 = __frcp_rn(d[1]), inv2 = __frcp_rn(d[2]);
   const float aa = __fmaf_rn(d[0], d[0], __fmaf_rn(d[1], d[1], __fmul_rn(d[2], d[2])));
   for (int li = 0; li < nl; ++li) {
     const int p = list[li];
@@ -581,7 +583,7 @@ SCR_DEV Hit raycast_mask(const Prim* prims, const unsigned char* list, uint32_t 
   h.t = __int_as_float(0x7f800000);
   h.prim = -1;
   h.face = -1;
-  const float inv0 = __fdiv_rn(1.0f, d[0]), inv1 = __fdiv_rn(1.0f, d[1]), inv2 = __fdiv_rn(1.0f, d[2]);
+  const float inv0 = __frcp_rn(d[0]), inv1 = __frcp_rn(d[1]), inv2 = __frcp_rn(d[2]);
   const float aa = __fmaf_rn(d[0], d[0], __fmaf_rn(d[1], d[1], __fmul_rn(d[2], d[2])));
   while (mask) {
     const int p = list[__ffs(mask) - 1];
@@ -774,7 +776,7 @@ SCR_DEV void hit_normal(const Prim* prims, int prim, int face, const float p[3],
     else n[2] = v;
   } else {
     const Prim& q = prims[prim];
-    const float inv = __fdiv_rn(1.0f, q.b[0]);
+    const float inv = __frcp_rn(q.b[0]);
 #pragma unroll
     for (int i = 0; i < 3; ++i) n[i] = __fmul_rn(__fsub_rn(p[i], q.a[i]), inv);
   }
