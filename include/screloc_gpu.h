@@ -175,6 +175,12 @@ scr_status scr_cascade_frameset(scr_scene s, scr_frameset fs, const int32_t* idx
 size_t scr_predictions_bytes(scr_scene s);
 scr_status scr_predictions_export(scr_scene s, void* device_dst);
 scr_status scr_predictions_import(scr_scene s, const void* device_src);
+/* One host process driving several GPUs: broadcast root's adapted prediction table to the
+ * scenes of the other GPUs with ncclBroadcast (the reference's
+ * single-writer adaptation + concurrent readers). per_gpu[i] must be root scenes
+ * (not lanes) created from the same forest on distinct devices; NCCL is loaded at run time
+ * (libnccl.so.2). ngpu == 1 is a no-op. Receivers publish the table to their lanes. */
+scr_status scr_broadcast_predictions(scr_scene* per_gpu, int ngpu, int root);
 
 /* ---- parity hooks (tests) -------------------------------------------------------------- */
 /* K0+K1: valid 4-px grid (packed x | y << 16) and leaf ids (n_grid x trees) */

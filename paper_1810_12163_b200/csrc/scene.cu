@@ -13,6 +13,8 @@
 //   update_leaves_round_robin SPEC.md:366-374
 //   clear_adaptation
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstring>
@@ -1299,6 +1301,35 @@ scr_status scr_predictions_export(scr_scene s, void* dst) {
   return SCR_OK;
 }
 
+// NCCL, resolved at run time so the library has no link-time dependency on it.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+static const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.comm_init_all = reinterpret_cast<decltype(api.comm_init_all)>(dlsym(h, "ncclCommInitAll"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.bcast = reinterpret_cast<decltype(api.bcast)>(dlsym(h, "ncclBroadcast"));
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.comm_init_all && api.comm_destroy && api.bcast && api.group_start && api.group_end &&
+             api.error_string;
+  });
+  return api;
+}
+
 static scr_status scr_predictions_import_impl(scr_scene s, const void* src) {
   if (!s || !src) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
@@ -1522,6 +1553,91 @@ scr_status scr_load_predictions(scr_scene s, const int32_t* counts, const scr_mo
   scr_status st = scr_load_predictions_impl(s, counts, modes);
   if (st == SCR_OK && s) st = publish(s);
   return st;
+}
+
+scr_status scr_broadcast_predictions(scr_scene* per_gpu, int ngpu, int root) {
+  if (!per_gpu || ngpu < 1 || root < 0 || root >= ngpu) {
+    set_error("scr_broadcast_predictions: need ngpu >= 1 scenes and 0 <= root < ngpu");
+    return SCR_E_ARG;
+  }
+  std::vector<int> devs(ngpu);
+  for (int i = 0; i < ngpu; ++i) {
+    const scr_scene s = per_gpu[i];
+    if (!s || s->parent) {
+      set_error("scr_broadcast_predictions: every entry must be a scene (not a relocalisation lane)");
+      return SCR_E_ARG;
+    }
+    if (s->L != per_gpu[root]->L || s->T != per_gpu[root]->T) {
+      set_error("scr_broadcast_predictions: scenes were created from different forests");
+      return SCR_E_DIMENSION_MISMATCH;
+    }
+    devs[i] = s->dev->ordinal;
+    for (int j = 0; j < i; ++j)
+      if (devs[j] == devs[i]) {
+        set_error("scr_broadcast_predictions: one scene per GPU (two entries share a device)");
+        return SCR_E_ARG;
+      }
+  }
+  if (ngpu == 1) return SCR_OK;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) {
+    set_error("scr_broadcast_predictions: libnccl.so.2 could not be loaded");
+    return SCR_E_CUDA;
+  }
+  // the root's table must be complete before the collective reads it
+  SCR_CUDA(cudaSetDevice(devs[root]));
+  SCR_CUDA(cudaStreamSynchronize(per_gpu[root]->stream));
+  std::vector<ncclComm_t> comms(ngpu);
+  ncclResult_t r = nc.comm_init_all(comms.data(), ngpu, devs.data());
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclCommInitAll: ") + nc.error_string(r));
+    return SCR_E_CUDA;
+  }
+  const size_t M = static_cast<size_t>(per_gpu[root]->L) * kMaxModes;
+  auto run = [&]() -> ncclResult_t {
+    for (int b = 0; b < 4; ++b) {
+      ncclResult_t e = nc.group_start();
+      if (e != ncclSuccess) return e;
+      for (int i = 0; i < ngpu; ++i) {
+        const scr_scene s = per_gpu[i];
+        void* ptr = b == 0 ? static_cast<void*>(s->d_count)
+                    : b == 1 ? static_cast<void*>(s->d_geom)
+                    : b == 2 ? static_cast<void*>(s->d_col)
+                             : static_cast<void*>(s->d_cov);
+        const size_t bytes = b == 0 ? s->L * sizeof(int)
+                             : b == 1 ? M * sizeof(ModeGeom)
+                             : b == 2 ? M * sizeof(float4)
+                                      : M * 6 * sizeof(float);
+        cudaSetDevice(devs[i]);
+        e = nc.bcast(ptr, ptr, bytes, ncclChar, root, comms[i], s->stream);
+        if (e != ncclSuccess) {
+          nc.group_end();
+          return e;
+        }
+      }
+      e = nc.group_end();
+      if (e != ncclSuccess) return e;
+    }
+    return ncclSuccess;
+  };
+  r = run();
+  scr_status st = SCR_OK;
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclBroadcast: ") + nc.error_string(r));
+    st = SCR_E_CUDA;
+  }
+  for (int i = 0; i < ngpu; ++i) {
+    cudaSetDevice(devs[i]);
+    if (cudaStreamSynchronize(per_gpu[i]->stream) != cudaSuccess && st == SCR_OK) {
+      set_error("scr_broadcast_predictions: stream synchronisation failed");
+      st = SCR_E_CUDA;
+    }
+    nc.comm_destroy(comms[i]);
+  }
+  if (st != SCR_OK) return st;
+  for (int i = 0; i < ngpu; ++i)
+    if (i != root) SCR_TRY(publish(per_gpu[i]));
+  return SCR_OK;
 }
 
 scr_status scr_predictions_import(scr_scene s, const void* src) {

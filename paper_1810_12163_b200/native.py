@@ -136,6 +136,7 @@ SIGNATURES = {
     "scr_predictions_bytes": (_sz, [_vp]),
     "scr_predictions_export": (C.c_int, [_vp, _vp]),
     "scr_predictions_import": (C.c_int, [_vp, _vp]),
+    "scr_broadcast_predictions": (C.c_int, [_P(_vp), C.c_int, C.c_int]),
     "scr_debug_leaves": (C.c_int, [_vp, _P(Frame), _P(_i32), _P(_i32), _P(C.c_int)]),
     "scr_debug_features": (C.c_int, [_vp, _P(Frame), _P(_i32), C.c_int, _P(_flt)]),
     "scr_dump_seen": (C.c_int, [_vp, _P(C.c_uint32)]),

@@ -351,6 +351,15 @@ class Scene:
         return out, conv.value, rms.value, inl.value, score.value
 
 
+def broadcast_predictions(scenes: list, root: int = 0) -> None:
+    """One process, several GPUs: ncclBroadcast of root's adapted prediction table to the
+    other scenes (scr_broadcast_predictions; one root scene per GPU, same forest)."""
+    arr = (C.c_void_p * len(scenes))(*[s.handle.value if isinstance(s.handle, C.c_void_p) else s.handle
+                                        for s in scenes])
+    lib = scenes[0].lib if scenes else N.load()
+    N.check(lib.scr_broadcast_predictions(arr, len(scenes), root), "scr_broadcast_predictions")
+
+
 def generate_random_forest(seed: int = 42, height: int = 14, p_depth: float = 0.4, trees: int = 5,
                            radius: int = 130) -> bytes:
     """generate_random_forest (forest.hpp:104-106) -> serialised ForestModel."""
