@@ -64,15 +64,14 @@ SCR_DEV int mode_index(const FrameRefs& fr, const int* pcount, size_t gbase, int
 // Generation slots are independent (slot s draws from Rng::stream(seed, s) and retries up
 // to max_iters; draw order and checks per DESIGN.md A1/A7), so lanes pull
 // slots from a per-frame atomic counter and never idle behind a slower lane.
-// Latency is the cost here (most attempts are rejected), so an attempt is arranged as
-// few dependent memory hops as possible:
-//  * the 7 raw xoshiro outputs an attempt can consume are buffered; assuming no
-//    rejection-sampling retry inside uniform_int (probability ~1e-15, detected exactly and
-//    replayed on the exact sequential path), all three pixel indices are known up front
-//    and their 32-byte records (pixel, depth, colour, |M(u)|, per-tree mode counts, 16-bit
-//    leaf ids, written by K1) are loaded together;
-//  * mode indices come from the records (no slot lookup), so the colour check needs one
-//    more load and the other two modes' world points are fetched only when it passes;
+// Latency is the cost here (most attempts are rejected), so an attempt touches global
+// memory as little as possible:
+//  * each CTA keeps |M(u)| of every grid pixel of its frame in shared memory (a byte per
+//    pixel), so the draws run the exact sequential algorithm and know how many values the
+//    attempt consumes (a pixel without modes ends it) without a global load;
+//  * only the colour-check pixel's 32-byte record (colour, per-tree mode counts, 16-bit leaf
+//    ids, written by K1) and its mode's colour are loaded; the other two modes are resolved
+//    when a warp evaluates its queued colour-check survivors;
 //  * uniform draws use exact Barrett reductions (same values as the 64-bit modulo).
 constexpr int kMaxModeUnion = kMaxTrees * kMaxModes;
 #ifndef SCR_GEN_TPF
@@ -80,20 +79,21 @@ constexpr int kMaxModeUnion = kMaxTrees * kMaxModes;
 #endif
 constexpr int kGenThreadsPerFrame = SCR_GEN_TPF;  // generation threads per frame (slots pulled dynamically)
 
-SCR_DEV uint64_t draw(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
+// uniform_int(n) by rejection (rng.hpp:50-56) with the 32-bit-tail Barrett reduction.
+SCR_DEV uint32_t draw32(Rng& r, uint32_t n, uint64_t m, uint64_t thr) {
   for (;;) {
     const uint64_t v = rng_next(r);
-    if (v >= thr) return mod_barrett(v, n, m);
+    if (v >= thr) return mod_barrett32(v, n, m);
+  }
+}
+// The accepted raw value of uniform_int(n) (reduced mod n later, when needed).
+SCR_DEV uint64_t draw_raw(Rng& r, uint64_t thr) {
+  for (;;) {
+    const uint64_t v = rng_next(r);
+    if (v >= thr) return v;
   }
 }
 
-struct RawBuf {  // the 7 raw outputs one generation attempt can consume
-  uint64_t b0, b1, b2, b3, b4, b5, b6;
-  SCR_DEV void fill(Rng& r) {
-    b0 = rng_next(r); b1 = rng_next(r); b2 = rng_next(r); b3 = rng_next(r);
-    b4 = rng_next(r); b5 = rng_next(r); b6 = rng_next(r);
-  }
-};
 
 // uniform_int by rejection (rng.hpp:50-56) with a precomputed Barrett reciprocal/threshold.
 SCR_DEV uint64_t draw_exact(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
   __shared__ int s_best[kGenWarps][32];  // smallest passing attempt of the lane's slot
   __shared__ int s_pend[kGenWarps][32];  // queued, unevaluated candidates of the lane's slot
   __shared__ int s_cur[kGenWarps][32];   // slot the lane currently owns
+  extern __shared__ uint8_t s_nm[];      // |M(u)| of every grid pixel of the frame (fast path)
   for (int i = threadIdx.x; i <= kMaxModeUnion; i += blockDim.x) {
     const uint64_t n = i ? static_cast<uint64_t>(i) : 1;
     const uint64_t m = barrett_m(n);
@@ -364,6 +365,10 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
   const uint64_t m3 = 0x5555555555555555ull;  // floor((2^64-1)/3)
   const bool fast = gp.fast != 0;
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  if (fast) {  // <= 5 trees x 50 modes: a byte per pixel
+    for (int i = threadIdx.x; i < static_cast<int>(G); i += blockDim.x) s_nm[i] = static_cast<uint8_t>(fr.gnm[fbase + i]);
+    __syncthreads();
+  }
   const float ifx = 1.0f / g.fx, ify = 1.0f / g.fy;  // f32 pre-filter only
   GenCand* q = s_q[wid];
   int qn = 0;  // warp-uniform queue length
@@ -393,55 +398,49 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
     bool push = false;
     GenCand c;
     if (slot >= 0 && it < gp.max_iters) {
-      // The 7 raw values an attempt can consume are generated up front; the stream state
-      // before them is kept, so an attempt that consumes fewer (a pixel without modes) or
-      // must be replayed exactly rewinds instead of carrying values between attempts.
-      const Rng saved = rng;
-      RawBuf buf;
-      buf.fill(rng);
-      // Fast path: none of the 7 raw values can be rejected (every rejection threshold is
-      // < 2^32, so a non-zero high word always passes; otherwise replay the attempt exactly
-      // below). Pixel indices and the colour-check index are then known up front; only the
-      // mode the colour check needs is resolved before the check.
-      const bool spec = fast && (buf.b0 >> 32) != 0 && (buf.b1 >> 32) != 0 && (buf.b2 >> 32) != 0 &&
-                        (buf.b3 >> 32) != 0 && (buf.b4 >> 32) != 0 && (buf.b5 >> 32) != 0 && (buf.b6 >> 32) != 0;
-      if (spec) {
-        const int g0 = static_cast<int>(mod_barrett32(buf.b0, G32, mG));
-        const int g1 = static_cast<int>(mod_barrett32(buf.b2, G32, mG));
-        const int g2 = static_cast<int>(mod_barrett32(buf.b4, G32, mG));
-        const int cc = static_cast<int>(mod_barrett32(buf.b6, 3u, m3));
-        const uint64_t r0 = buf.b1, r1 = buf.b3, r2 = buf.b5;
-        const int gc = cc == 0 ? g0 : (cc == 1 ? g1 : g2);
-        const int4 A0 = fr.grec[2 * (fbase + g0)], A1 = fr.grec[2 * (fbase + g1)], A2 = fr.grec[2 * (fbase + g2)];
-        const uint4 Lc = fr.gleaf[2 * (fbase + gc) + 1];  // issued together with the records
-        const uint32_t nm0 = static_cast<uint32_t>(A0.z) >> 24, nm1 = static_cast<uint32_t>(A1.z) >> 24,
-                       nm2 = static_cast<uint32_t>(A2.z) >> 24;
-        const bool full = nm0 != 0 && nm1 != 0 && nm2 != 0;  // all 7 raw values consumed
-        // the colour check's mode is resolved and its colour load issued before the stream
-        // refill, so the load's latency hides behind the xoshiro work
-        const int4 Ac = cc == 0 ? A0 : (cc == 1 ? A1 : A2);
-        float4 mcol = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (fast) {
+        // The exact sequential attempt (draw order A1/A7, rejection sampling as in
+        // rng.hpp:50-56): each pixel's mode count comes from shared memory, so the stream
+        // consumption (1, 3, 5 or 7 values) is known without touching global memory, and
+        // only the colour-check pixel's record, leaf ids and mode colour are loaded.
+        int g0, g1 = 0, g2 = 0, cc = 0;
+        uint32_t nm1 = 0, nm2 = 0;
+        uint64_t v1 = 0, v3 = 0, v5 = 0;
+        bool full = false;
+        g0 = static_cast<int>(draw32(rng, G32, mG, tG));
+        const uint32_t nm0 = s_nm[g0];
+        if (nm0) {
+          v1 = draw_raw(rng, s_thr[nm0]);
+          g1 = static_cast<int>(draw32(rng, G32, mG, tG));
+          nm1 = s_nm[g1];
+          if (nm1) {
+            v3 = draw_raw(rng, s_thr[nm1]);
+            g2 = static_cast<int>(draw32(rng, G32, mG, tG));
+            nm2 = s_nm[g2];
+            if (nm2) {
+              v5 = draw_raw(rng, s_thr[nm2]);
+              cc = static_cast<int>(draw32(rng, 3u, m3, 1u));  // 2^64 mod 3 = 1
+              full = true;
+            }
+          }
+        }
         if (full) {
-          const uint64_t rc = cc == 0 ? r0 : (cc == 1 ? r1 : r2);
-          const uint32_t nmc = static_cast<uint32_t>(Ac.z) >> 24;
-          const int pc = static_cast<int>(mod_barrett32(rc, nmc, s_m[nmc]));
-          mcol = pv.col[mode_from_record(s_lbase, static_cast<uint32_t>(Ac.w), Lc, pc)];
+          const int gc = cc == 0 ? g0 : (cc == 1 ? g1 : g2);
+          const uint64_t vc = cc == 0 ? v1 : (cc == 1 ? v3 : v5);
+          const uint32_t nmc = cc == 0 ? nm0 : (cc == 1 ? nm1 : nm2);
+          const int4 Ac = fr.grec[2 * (fbase + gc)];
+          const uint4 Lc = fr.gleaf[2 * (fbase + gc) + 1];
+          const uint32_t pc = mod_barrett32(vc, nmc, s_m[nmc]);
+          const float4 mcol = pv.col[mode_from_record(s_lbase, static_cast<uint32_t>(Ac.w), Lc, static_cast<int>(pc))];
+          if (colour_ok(static_cast<uint32_t>(Ac.z), mcol, gp.colour_thresh)) {
+            push = true;
+            c.slot = slot;
+            c.owner_att = lane | (it << 5);
+            c.g0 = g0; c.g1 = g1; c.g2 = g2;
+            c.r0 = u2_of(v1); c.r1 = u2_of(v3); c.r2 = u2_of(v5);
+          }
         }
-        if (!full) {  // consumed 1, 3 or 5 raw values: rewind and advance by that many
-          rng = saved;
-          const int k = nm0 == 0 ? 1 : (nm1 == 0 ? 3 : 5);
-#pragma unroll 1
-          for (int j = 0; j < k; ++j) rng_next(rng);
-        }
-        if (full && colour_ok(static_cast<uint32_t>(Ac.z), mcol, gp.colour_thresh)) {
-          push = true;
-          c.slot = slot;
-          c.owner_att = lane | (it << 5);
-          c.g0 = g0; c.g1 = g1; c.g2 = g2;
-          c.r0 = u2_of(r0); c.r1 = u2_of(r1); c.r2 = u2_of(r2);
-        }
-      } else {  // exact sequential replay of the attempt from the saved stream state
-        rng = saved;
+      } else {  // > 5 trees or 32-bit leaf ids: modes through the slot tables
         int g0, g1, g2, m0, m1, m2;
         if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, s_thr, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2)) {
           push = true;
@@ -1951,7 +1950,8 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   SCR_CUDA(cudaMemsetAsync(w.hctr + w.cap, 0, nA * sizeof(int), s->stream));  // per-frame suspect counts
   const int gen_threads = std::min(p.n_max, kGenThreadsPerFrame);
   SCR_LAUNCH(s, K_HYPGEN,
-             (k_hypgen<<<dim3((gen_threads + kGenWarps * 32 - 1) / (kGenWarps * 32), nA), kGenWarps * 32, 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds,
+             (k_hypgen<<<dim3((gen_threads + kGenWarps * 32 - 1) / (kGenWarps * 32), nA), kGenWarps * 32,
+                         gp.fast ? static_cast<size_t>((w.gmax + 15) & ~15) : 0, s->stream>>>(gp, s->geom, fr, pv, w.seeds,
                                                                                   w.hctr, w.hcand, w.hok, w.hiters,
                                                                                   w.hctr + w.cap, w.sus, wk)));
   SCR_LAUNCH(s, K_HYPFIN,
@@ -2054,6 +2054,8 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
 }  // namespace
 
 scr_status reloc_init() {
+  SCR_CUDA(cudaFuncSetAttribute(k_hypgen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (kMaxImageW / 4) * (kMaxImageH / 4)));
   SCR_CUDA(cudaFuncSetAttribute(k_energy_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kSmallHyps * (kEnergySampleCap + 1) * sizeof(float))));
   SCR_CUDA(cudaFuncSetAttribute(k_energy_grouped<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -758,6 +758,11 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
     set_error("scr_scene_create: null argument");
     return SCR_E_ARG;
   }
+  if (k->width <= 0 || k->height <= 0 || k->width > 1280 || k->height > 960) {
+    // shared-memory tables of ICP (ray directions) and generation (per-pixel mode counts)
+    set_error("scr_scene_create: frames up to 1280 x 960 (the stress configuration)");
+    return SCR_E_ARG;
+  }
   if (!(k->fx > 0 && k->fy > 0 && k->cx >= 0 && k->cx < k->width && k->cy >= 0 && k->cy < k->height)) {
     set_error("scr_scene_create: invalid intrinsics (geometry.hpp:52-54)");
     return SCR_E_ARG;
