@@ -617,11 +617,11 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
       hyp[out] = T;
       hok[out] = 1;
       hiters[out] = res_it;
-    } else if (clear && ns < kMaxSuspects) {  // cannot happen: the recorded Kabsch is clearly regular
-      hok[out] = 0;
     }
   }
-  const bool cont = clear && !ok && ns >= kMaxSuspects;
+  // The recorded triplet can only fail here if the suspect list overflowed (its Kabsch was
+  // not classified); any such slot continues exactly from the next attempt.
+  const bool cont = clear && !ok;
   if (!__syncthreads_or(cont)) return;
   // continuation on the exact path (suspect list overflowed): the tables the draws need
   for (int i = threadIdx.x; i <= kMaxModeUnion; i += blockDim.x) {
