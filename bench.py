@@ -5,8 +5,9 @@ Workload (BASELINE.json configs[1] + configs[2]): one synthetic 7-Scenes-like ro
 primitives), a 5-tree random SCoRe forest (h = 14, p = 0.4) adapted on a 1000-frame
 sequence (integrate + every leaf clustered), then the 3-stage cascade (Fast w/ ICP,
 Intermediate w/ ICP, Slow w/ ranking of 16) on held-out test frames. One step = one
-cascade over a batch of frames already resident in HBM; `e2e` = the same through the
-C ABI with pinned host frames (H2D + result D2H inside the timed region).
+cascade over lanes x batch frames already resident in HBM, each relocalisation lane (own
+stream + host thread) taking one batch of every step; `e2e` = the same through the C ABI
+with pinned host frames (H2D + result D2H inside the timed region).
 
 Multi-GPU (torchrun): weak scaling, frames sharded by rank, the adapted prediction table
 broadcast from rank 0 over NCCL once (no per-frame collective); time = max over ranks.
@@ -269,8 +270,9 @@ def run_ours(args):
     seeds_all = [frame_seed(RUN_SEED, i) for i in mine]
     B = args.batch
 
-    def batch_at(step):
-        i0 = (step * B) % len(poses)
+    def batch_at(sub):
+        """Sub-batch `sub` (B frames); step st is sub-batches st*L .. st*L + L-1, one per lane."""
+        i0 = (sub * B) % len(poses)
         idx = [(i0 + j) % len(poses) for j in range(B)]
         return idx, [seeds_all[i] for i in idx]
 
@@ -280,15 +282,17 @@ def run_ours(args):
     lanes = [scene] + [scene.fork(B) for _ in range(max(1, args.lanes) - 1)]
     lane_streams = [torch.cuda.ExternalStream(l.stream, device=dev_t) for l in lanes]
     clk = ClockSampler(local).__enter__()  # nvidia-smi needs ~1 s to start: launch it before warm-up
+    L = len(lanes)
     for w in range(args.warmup):
-        idx, sd = batch_at(w)
-        for lane in lanes:
+        for li, lane in enumerate(lanes):
+            idx, sd = batch_at(w * L + li)
             fs.cascade(idx, cfg, sd, scene=lane)
     torch.cuda.synchronize()
 
     def run_lanes(step_fn, steps):
-        """Runs steps 0..steps-1 round-robin over the lanes (one host thread per lane) and
-        returns the device time from a common start event to the last lane's end event."""
+        """Runs steps 0..steps-1, each split over the lanes (one host thread per lane: lane li
+        runs its sub-batch of every step), and returns the device time from a common start
+        event to the last lane's end event."""
         torch.cuda.synchronize()
         start = torch.cuda.Event(enable_timing=True)
         ends = [torch.cuda.Event(enable_timing=True) for _ in lanes]
@@ -297,8 +301,8 @@ def run_ours(args):
 
         def work(li):
             try:
-                for st in range(li, steps, len(lanes)):
-                    step_fn(lanes[li], st)
+                for st in range(steps):
+                    step_fn(lanes[li], li, st)
             except Exception as e:  # surfaced after join
                 errs.append(e)
 
@@ -315,16 +319,17 @@ def run_ours(args):
         return max(start.elapsed_time(e) for e in ends)
 
     # ---- timed region: device-resident inputs (no per-kernel instrumentation)
-    results = [None] * args.steps
+    results = [None] * (args.steps * L)
     launches0 = sum(l.kernel_launches for l in lanes)
     if dist is not None:
         dist.barrier()
     if args.profile_window:
         torch.cuda.cudart().cudaProfilerStart()
 
-    def timed_step(lane, st):
-        idx, sd = batch_at(args.warmup + st)
-        results[st] = (idx, fs.cascade(idx, cfg, sd, scene=lane))
+    def timed_step(lane, li, st):
+        sub = st * L + li
+        idx, sd = batch_at(args.warmup * L + sub)
+        results[sub] = (idx, fs.cascade(idx, cfg, sd, scene=lane))
 
     tw0 = time.time()
     elapsed_ms = run_lanes(timed_step, args.steps)
@@ -337,7 +342,7 @@ def run_ours(args):
     clk.__exit__(None, None, None)
     launches = sum(l.kernel_launches for l in lanes) - launches0
     elapsed_max = max_over_ranks(elapsed_ms, dist, dev_t)
-    frames_done = sum_over_ranks(float(args.steps * B), dist, dev_t)
+    frames_done = sum_over_ranks(float(args.steps * B * L), dist, dev_t)
     value = frames_done / (elapsed_max / 1e3)
 
     # ---- second timed pass, same batches, with CUDA events around every launch (roofline)
@@ -346,8 +351,8 @@ def run_ours(args):
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(stream)
-    for st in range(args.steps):
-        idx, sd = batch_at(args.warmup + st)
+    for sub in range(args.steps * L):
+        idx, sd = batch_at(args.warmup * L + sub)
         fs.cascade(idx, cfg, sd)
     p1.record(stream)
     torch.cuda.synchronize()
@@ -380,13 +385,13 @@ def run_ours(args):
         lane.run_cascade_batch([dnp[j] for j in e2e_idx], [cnp[j] for j in e2e_idx], cfg, e2e_seeds)
     if dist is not None:
         dist.barrier()
-    e2e_steps = max(len(lanes), args.steps)
+    e2e_steps = args.steps
     e2e_ms = max_over_ranks(
-        run_lanes(lambda lane, st: lane.run_cascade_batch([dnp[j] for j in e2e_idx], [cnp[j] for j in e2e_idx], cfg,
+        run_lanes(lambda lane, li, st: lane.run_cascade_batch([dnp[j] for j in e2e_idx], [cnp[j] for j in e2e_idx], cfg,
                                                           e2e_seeds), e2e_steps), dist, dev_t)
-    e2e_value = sum_over_ranks(float(e2e_steps * B), dist, dev_t) / (e2e_ms / 1e3)
-    h2d = B * (k.width * k.height * 4 + k.width * k.height * 3)
-    d2h = B * 136
+    e2e_value = sum_over_ranks(float(e2e_steps * B * L), dist, dev_t) / (e2e_ms / 1e3)
+    h2d = B * L * (k.width * k.height * 4 + k.width * k.height * 3)
+    d2h = B * L * 136
 
     # ---- roofline of the dominant kernel (+ the other modelled kernels)
     peaks = measured_peaks()
@@ -427,7 +432,8 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(elapsed_max / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (geometry f64)", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "frames_per_step_per_gpu": B, "test_frames_per_gpu": len(poses),
+        "config": {"workload": WORKLOAD, "frames_per_step_per_gpu": B * L, "frames_per_lane_batch": B,
+                   "test_frames_per_gpu": len(poses),
                    "adapt_frames": args.adapt_frames, "resolution": "640x480", "forest": "random h14 p0.4 x5",
                    "forest_params": "kappa 2048, tau 0.2, min 5", "scene_seed": SCENE_SEED,
                    "l2": "inputs larger than L2 (test frames rotate through %.0f MB of HBM)" % (
@@ -587,7 +593,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=128, help="frames per step per GPU")
+    ap.add_argument("--batch", type=int, default=128, help="frames per lane per step (a step is lanes x batch frames per GPU)")
     ap.add_argument("--test-frames", type=int, default=1024, help="resident test frames per GPU")
     ap.add_argument("--adapt-frames", type=int, default=1000)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
