@@ -140,8 +140,9 @@ IcpResult icp_refine(const Scene& s, const Pose& init, const Frame& fr) {
         for (int i = 0; i < 3; ++i)
           pr[i] = std::fma(Ri[3 * i + 0], pw[0], std::fma(Ri[3 * i + 1], pw[1], std::fma(Ri[3 * i + 2], pw[2], ti[i])));
         if (!(pr[2] > 0.0f)) continue;
-        const float uf = std::fma(fxf, pr[0] / pr[2], cxf);
-        const float vf = std::fma(fyf, pr[1] / pr[2], cyf);
+        const float iz = 1.0f / pr[2];  // one correctly rounded reciprocal, then products
+        const float uf = std::fma(fxf, pr[0] * iz, cxf);
+        const float vf = std::fma(fyf, pr[1] * iz, cyf);
         if (!(uf > -0.5f && vf > -0.5f && uf < W - 0.5f && vf < H - 0.5f)) continue;
         const int ui = static_cast<int>(std::floor(uf + 0.5f)), vi = static_cast<int>(std::floor(vf + 0.5f));
         if (ui < 0 || vi < 0 || ui >= W || vi >= H) continue;

@@ -1501,6 +1501,16 @@ SCR_DEV void divmod_w(int p, int W, float invW, int& x, int& y) {
   y = q;
 }
 
+// (x, y) of pixel p + d where (dx, dy) = (d mod W, d div W), from (x, y) of p: one carry.
+SCR_DEV void xy_advance(int& x, int& y, int dx, int dy, int W) {
+  x += dx;
+  y += dy;
+  if (x >= W) {
+    x -= W;
+    ++y;
+  }
+}
+
 #ifndef SCR_ICP_MINB
 #define SCR_ICP_MINB 4
 #endif
@@ -1581,9 +1591,11 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       unsigned long long tests = 0;
       const int twl = Wl / kTileW;
       const float invWl = __fdiv_rn(1.0f, static_cast<float>(Wl));
-      for (int p = lane_id; p < Wl * Hl; p += kIcpLanes) {
-        int x, y;
-        divmod_w(p, Wl, invWl, x, y);
+      const int sdx = kIcpLanes % Wl, sdy = kIcpLanes / Wl;  // pixel stride of a lane in (x, y)
+      int rx, ry;
+      divmod_w(lane_id, Wl, invWl, rx, ry);
+      for (int p = lane_id; p < Wl * Hl; p += kIcpLanes, xy_advance(rx, ry, sdx, sdy, Wl)) {
+        const int x = rx, y = ry;
         float d[3];
         ray_dir_tab(Rr, s_dcx[x], s_dcy[y], d);
         uint2 v = make_uint2(0u, 0xffffffffu);
@@ -1607,6 +1619,8 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       }
       if (work) work_add(work, W_RAY_PRIMS, static_cast<unsigned>(tests));
       cluster.sync();  // map complete and visible to the whole cluster
+      int rx0, ry0;
+      divmod_w(lane_id, Wl, invWl, rx0, ry0);
       const int iters = level == 2 ? 10 : (level == 1 ? 5 : 4);
       for (int it = 0; it < iters; ++it) {
         const Pose T = Ts;
@@ -1623,12 +1637,15 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
         // lane (p, p + kIcpLanes) are in flight at once: both depth loads, then both model-map
         // loads, then both accumulated in pixel order (same per-lane order as one at a time).
         const int npx = Wl * Hl;
+        int ax = rx0, ay = ry0;  // (x, y) of pixel p
         for (int p = lane_id; p < npx; p += kIcpPix * kIcpLanes) {
           IcpPix px[kIcpPix];
 #pragma unroll
           for (int u = 0; u < kIcpPix; ++u) {
             const int pp = p + u * kIcpLanes;
-            divmod_w(pp, Wl, invWl, px[u].x, px[u].y);
+            px[u].x = ax;
+            px[u].y = ay;
+            xy_advance(ax, ay, sdx, sdy, Wl);
             px[u].dl = pp < npx ? dpl[pp] : 0.0f;
           }
 #pragma unroll
@@ -1646,8 +1663,9 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
               pr[i] = __fmaf_rn(Ri[3 * i + 0], px[u].pw[0],
                                 __fmaf_rn(Ri[3 * i + 1], px[u].pw[1], __fmaf_rn(Ri[3 * i + 2], px[u].pw[2], ti[i])));
             if (!(pr[2] > 0.0f)) continue;
-            const float uf = __fmaf_rn(fxl, __fdiv_rn(pr[0], pr[2]), cxl);
-            const float vf = __fmaf_rn(fyl, __fdiv_rn(pr[1], pr[2]), cyl);
+            const float iz = __frcp_rn(pr[2]);
+            const float uf = __fmaf_rn(fxl, __fmul_rn(pr[0], iz), cxl);
+            const float vf = __fmaf_rn(fyl, __fmul_rn(pr[1], iz), cyl);
             if (!(uf > -0.5f && vf > -0.5f && uf < __fsub_rn(static_cast<float>(Wl), 0.5f) &&
                   vf < __fsub_rn(static_cast<float>(Hl), 0.5f)))
               continue;
@@ -1775,9 +1793,11 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
     unsigned long long tests = 0;
     const int tw0 = g.W / kTileW;
     const float invW = __fdiv_rn(1.0f, static_cast<float>(g.W));
-    for (int p = lane_id; p < g.W * g.H; p += kIcpLanes) {
-      int x, y;
-      divmod_w(p, g.W, invW, x, y);
+    const int fdx = kIcpLanes % g.W, fdy = kIcpLanes / g.W;
+    int fx0, fy0;
+    divmod_w(lane_id, g.W, invW, fx0, fy0);
+    for (int p = lane_id; p < g.W * g.H; p += kIcpLanes, xy_advance(fx0, fy0, fdx, fdy, g.W)) {
+      const int x = fx0, y = fy0;
       float d[3];
       ray_dir_tab(R, s_dcx[x], s_dcy[y], d);
       Hit h;
