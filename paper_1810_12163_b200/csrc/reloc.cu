@@ -762,14 +762,16 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(const Pose* __restr
 SCR_DEV int stage_modes(const PredView& pv, const SampleModes& sm, int T, int nm, int j0, int lane, float4* buf) {
   const int j = j0 + lane;
   if (j >= nm) return -1;
-  int t = 0, before = 0;
+  // tree of mode j and the modes before it; the slot is selected in registers (a runtime
+  // index into sm.slot would put the struct in local memory)
+  int slot = sm.slot[0], before = 0;
 #pragma unroll
   for (int q = 0; q < kMaxTrees - 1; ++q)
     if (q < T - 1 && j >= sm.end[q]) {
-      t = q + 1;
+      slot = sm.slot[q + 1];
       before = sm.end[q];
     }
-  const int mi = sm.slot[t] * kMaxModes + (j - before);
+  const int mi = slot * kMaxModes + (j - before);
   const ModeGeom& g = pv.geom[mi];
   buf[3 * lane + 0] = g.q0;
   buf[3 * lane + 1] = g.q1;
@@ -807,7 +809,10 @@ constexpr int kSmallHyps = 64;
 #endif
 constexpr int kEsThreads = SCR_ES_THREADS;  // warps per frame-tile: more samples in flight per frame
 
-__global__ void __launch_bounds__(kEsThreads) k_energy_small(EnergyArgs ea, FrameRefs fr, PredView pv,
+#ifndef SCR_ES_MINB
+#define SCR_ES_MINB 1
+#endif
+__global__ void __launch_bounds__(kEsThreads, SCR_ES_MINB) k_energy_small(EnergyArgs ea, FrameRefs fr, PredView pv,
                                                       unsigned long long* __restrict__ work) {
   extern __shared__ float es_e[];  // [kSmallHyps][eta + 1]
   __shared__ float s_pose[kSmallHyps][12];
