@@ -1570,12 +1570,11 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       const Pose Tref = Ts;
       Pose Tinv;
       pose_invert(Tref, Tinv);
-      float Rr[9], tr[3], Ri[9], ti[3];
+      // Tinv.R is the exact transpose of Tref.R, so float(Tinv.R[3i+j]) == Rr[3j+i]: the
+      // inverse rotation is read from Rr transposed (9 fewer registers in the pixel loops)
+      float Rr[9], tr[3], ti[3];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) {
-        Rr[i] = static_cast<float>(Tref.R[i]);
-        Ri[i] = static_cast<float>(Tinv.R[i]);
-      }
+      for (int i = 0; i < 9; ++i) Rr[i] = static_cast<float>(Tref.R[i]);
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         tr[i] = static_cast<float>(Tref.t[i]);
@@ -1665,8 +1664,8 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
               px[u].pw[i] = __fmaf_rn(R[3 * i + 0], pc0, __fmaf_rn(R[3 * i + 1], pc1, __fmaf_rn(R[3 * i + 2], px[u].dl, t[i])));
 #pragma unroll
             for (int i = 0; i < 3; ++i)
-              pr[i] = __fmaf_rn(Ri[3 * i + 0], px[u].pw[0],
-                                __fmaf_rn(Ri[3 * i + 1], px[u].pw[1], __fmaf_rn(Ri[3 * i + 2], px[u].pw[2], ti[i])));
+              pr[i] = __fmaf_rn(Rr[0 + i], px[u].pw[0],
+                                __fmaf_rn(Rr[3 + i], px[u].pw[1], __fmaf_rn(Rr[6 + i], px[u].pw[2], ti[i])));
             if (!(pr[2] > 0.0f)) continue;
             const float iz = __frcp_rn(pr[2]);
             const float uf = __fmaf_rn(fxl, __fmul_rn(pr[0], iz), cxl);
