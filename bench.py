@@ -599,7 +599,7 @@ def main(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-batch", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--lanes", type=int, default=4, help="relocalisation lanes (streams + host threads) per GPU")
+    ap.add_argument("--lanes", type=int, default=5, help="relocalisation lanes (streams + host threads) per GPU")
     ap.add_argument("--profile-window", action="store_true",
                     help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
     args = ap.parse_args(argv)
