@@ -190,7 +190,7 @@ inline void eig3_jacobi(const double Ain[9], double evals[3], double Vout[9]) {
 
 // Solves M x = rhs for SPD 6x6 M (row-major, full). Returns false if a pivot <= 0.
 inline bool chol6_solve(const double M[36], const double rhs[6], double x[6]) {
-  double L[36];
+  double L[36], invd[6];
   for (int i = 0; i < 36; ++i) L[i] = 0.0;
   for (int j = 0; j < 6; ++j) {
     double d = M[6 * j + j];
@@ -198,22 +198,24 @@ inline bool chol6_solve(const double M[36], const double rhs[6], double x[6]) {
     if (!(d > 0.0)) return false;
     const double ljj = std::sqrt(d);
     L[6 * j + j] = ljj;
+    const double inv = 1.0 / ljj;  // one division per pivot; every use multiplies by it
+    invd[j] = inv;
     for (int i = j + 1; i < 6; ++i) {
       double s = M[6 * i + j];
       for (int k = 0; k < j; ++k) s = s - L[6 * i + k] * L[6 * j + k];
-      L[6 * i + j] = s / ljj;
+      L[6 * i + j] = s * inv;
     }
   }
   double y[6];
   for (int i = 0; i < 6; ++i) {
     double s = rhs[i];
     for (int k = 0; k < i; ++k) s = s - L[6 * i + k] * y[k];
-    y[i] = s / L[6 * i + i];
+    y[i] = s * invd[i];
   }
   for (int i = 5; i >= 0; --i) {
     double s = y[i];
     for (int k = i + 1; k < 6; ++k) s = s - L[6 * k + i] * x[k];
-    x[i] = s / L[6 * i + i];
+    x[i] = s * invd[i];
   }
   return true;
 }

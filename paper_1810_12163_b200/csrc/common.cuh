@@ -349,7 +349,7 @@ SCR_DEV bool kabsch3(const double cam[9], const double world[9], Pose& T) {
 
 // Cholesky solve of a 6x6 SPD system (oracle chol6_solve restated).
 SCR_DEV bool chol6(const double M[36], const double rhs[6], double x[6]) {
-  double L[36];
+  double L[36], invd[6];
 #pragma unroll
   for (int i = 0; i < 36; ++i) L[i] = 0.0;
 #pragma unroll
@@ -360,12 +360,14 @@ SCR_DEV bool chol6(const double M[36], const double rhs[6], double x[6]) {
     if (!(d > 0.0)) return false;
     const double ljj = sqrt(d);
     L[6 * j + j] = ljj;
+    const double inv = 1.0 / ljj;  // one division per pivot; every use multiplies by it
+    invd[j] = inv;
 #pragma unroll
     for (int i = j + 1; i < 6; ++i) {
       double s = M[6 * i + j];
 #pragma unroll
       for (int k = 0; k < j; ++k) s = s - L[6 * i + k] * L[6 * j + k];
-      L[6 * i + j] = s / ljj;
+      L[6 * i + j] = s * inv;
     }
   }
   double y[6];
@@ -374,14 +376,14 @@ SCR_DEV bool chol6(const double M[36], const double rhs[6], double x[6]) {
     double s = rhs[i];
 #pragma unroll
     for (int k = 0; k < i; ++k) s = s - L[6 * i + k] * y[k];
-    y[i] = s / L[6 * i + i];
+    y[i] = s * invd[i];
   }
 #pragma unroll
   for (int i = 5; i >= 0; --i) {
     double s = y[i];
 #pragma unroll
     for (int k = i + 1; k < 6; ++k) s = s - L[6 * k + i] * x[k];
-    x[i] = s / L[6 * i + i];
+    x[i] = s * invd[i];
   }
   return true;
 }
