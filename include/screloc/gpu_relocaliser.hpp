@@ -269,6 +269,14 @@ class Relocaliser {
   scr_scene s_ = nullptr;
 };
 
+// One host process driving several GPUs: after adapting on per_gpu[root], broadcast its
+// prediction table to the relocalisers of the other GPUs (scr_broadcast_predictions, NCCL).
+inline void broadcast_predictions(const std::vector<Relocaliser*>& per_gpu, int root = 0) {
+  std::vector<scr_scene> h;
+  for (const Relocaliser* r : per_gpu) h.push_back(r ? r->handle() : nullptr);
+  check(scr_broadcast_predictions(h.data(), static_cast<int>(h.size()), root), "broadcast_predictions");
+}
+
 }  // namespace gpu
 }  // namespace screloc
 
