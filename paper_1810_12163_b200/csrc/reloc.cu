@@ -1538,8 +1538,12 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
   __shared__ int stop_level;
   __shared__ unsigned char s_plist[256];
   __shared__ int s_pn;
-  __shared__ float s_dcx[kMaxImageW], s_dcy[kMaxImageH];
-  __shared__ uint32_t s_tmask[kMaxTiles];
+  // ray tables and tile masks sized to the frame (dynamic shared memory): a smaller
+  // shared-memory carve-out leaves more L1 for the depth-plane and model-map gathers
+  extern __shared__ uint32_t s_dyn[];
+  float* s_dcx = reinterpret_cast<float*>(s_dyn);
+  float* s_dcy = s_dcx + g.W;
+  uint32_t* s_tmask = reinterpret_cast<uint32_t*>(s_dcy + g.H);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = static_cast<int>(cluster.block_rank());
   const int lane_id = rank * kIcpThreads + threadIdx.x;
@@ -1855,6 +1859,12 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
   }
 }
 
+// Dynamic shared memory of k_icp_score: ray tables (W + H floats) + level-0 tile masks.
+inline size_t icp_smem(const FrameGeom& g) {
+  const size_t tiles = static_cast<size_t>((g.W + kTileW - 1) / kTileW) * ((g.H + kTileH - 1) / kTileH);
+  return (static_cast<size_t>(g.W) + g.H + tiles) * sizeof(uint32_t);
+}
+
 // ================================ K11: per-frame result =====================================
 __global__ void k_finalize(int nA, int mode, int cand_stride, const Pose* __restrict__ cand,
                            const int* __restrict__ ncand, const Pose* __restrict__ icp_pose,
@@ -2058,12 +2068,12 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
                static_cast<size_t>(s->k.width) * s->k.height};
     if (s->tsdf_model) {
       SCR_LAUNCH(s, K_ICP,
-                 (k_icp_score<true><<<nj * kIcpCtas, kIcpThreads, 0, s->stream>>>(
+                 (k_icp_score<true><<<nj * kIcpCtas, kIcpThreads, icp_smem(s->geom), s->stream>>>(
                      ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand, w.icp_map, w.icp_pose, w.icp_conv,
                      w.icp_rms, w.icp_inl, w.icp_score, wk, tsdf_view(s->tsdf_model))));
     } else {
       SCR_LAUNCH(s, K_ICP,
-                 (k_icp_score<false><<<nj * kIcpCtas, kIcpThreads, 0, s->stream>>>(
+                 (k_icp_score<false><<<nj * kIcpCtas, kIcpThreads, icp_smem(s->geom), s->stream>>>(
                      ia, s->geom, fr, s->d_prims, s->n_prims, w.cand, w.ncand, w.icp_map, w.icp_pose, w.icp_conv,
                      w.icp_rms, w.icp_inl, w.icp_score, wk, TsdfView{})));
     }
@@ -2353,12 +2363,12 @@ scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, 
   SCR_CUDA(cudaMemcpyAsync(s->ws.cand, init, sizeof(Pose), cudaMemcpyHostToDevice, s->stream));
   IcpArgs ia{s->ws.ncull_cap, 1, 1, 0, WH};
   if (s->tsdf_model) {
-    SCR_LAUNCH(s, K_ICP, (k_icp_score<true><<<kIcpCtas, kIcpThreads, 0, s->stream>>>(
+    SCR_LAUNCH(s, K_ICP, (k_icp_score<true><<<kIcpCtas, kIcpThreads, icp_smem(s->geom), s->stream>>>(
                              ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand, s->ws.ncand, s->ws.icp_map,
                              s->ws.icp_pose, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.icp_score, nullptr,
                              tsdf_view(s->tsdf_model))));
   } else {
-    SCR_LAUNCH(s, K_ICP, (k_icp_score<false><<<kIcpCtas, kIcpThreads, 0, s->stream>>>(
+    SCR_LAUNCH(s, K_ICP, (k_icp_score<false><<<kIcpCtas, kIcpThreads, icp_smem(s->geom), s->stream>>>(
                              ia, s->geom, frame_refs(s), s->d_prims, s->n_prims, s->ws.cand, s->ws.ncand, s->ws.icp_map,
                              s->ws.icp_pose, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.icp_score, nullptr,
                              TsdfView{})));
