@@ -2087,7 +2087,19 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
 
 }  // namespace
 
+#ifndef SCR_ICP_CARVE
+#define SCR_ICP_CARVE 25  // 4 CTAs of ~12 KB fit; a larger carve-out costs L1 (100 %: ICP +19 %)
+#endif
+#ifndef SCR_GEN_CARVE
+#define SCR_GEN_CARVE -1
+#endif
 scr_status reloc_init() {
+  if (SCR_ICP_CARVE >= 0) {  // shared-memory carve-out preference (percent): the rest is L1
+    SCR_CUDA(cudaFuncSetAttribute(k_icp_score<false>, cudaFuncAttributePreferredSharedMemoryCarveout, SCR_ICP_CARVE));
+    SCR_CUDA(cudaFuncSetAttribute(k_icp_score<true>, cudaFuncAttributePreferredSharedMemoryCarveout, SCR_ICP_CARVE));
+  }
+  if (SCR_GEN_CARVE >= 0)
+    SCR_CUDA(cudaFuncSetAttribute(k_hypgen, cudaFuncAttributePreferredSharedMemoryCarveout, SCR_GEN_CARVE));
   SCR_CUDA(cudaFuncSetAttribute(k_hypgen, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (kMaxImageW / 4) * (kMaxImageH / 4)));
   SCR_CUDA(cudaFuncSetAttribute(k_energy_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
