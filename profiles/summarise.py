@@ -25,6 +25,7 @@ METRICS = [
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
     ("sm__inst_executed.avg.per_cycle_active", "IPC (warp inst/cycle/SM)"),
     ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue active %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
