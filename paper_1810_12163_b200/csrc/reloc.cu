@@ -86,14 +86,21 @@ SCR_DEV uint32_t draw32(Rng& r, uint32_t n, uint64_t m, uint64_t thr) {
     if (v >= thr) return mod_barrett32(v, n, m);
   }
 }
+// uniform_int(n) for n < 2^32 with the rejection threshold 2^64 mod n (< n) computed only
+// when it can matter: a value with a non-zero high word is always accepted.
+SCR_DEV uint64_t draw_exact_lazy(Rng& r, uint64_t n, uint64_t m) {
+  for (;;) {
+    const uint64_t v = rng_next(r);
+    if ((v >> 32) != 0 || v >= mod_barrett(0 - n, n, m)) return mod_barrett(v, n, m);
+  }
+}
 // The accepted raw value of uniform_int(n) (reduced mod n later, when needed).
-SCR_DEV uint64_t draw_raw(Rng& r, uint64_t thr) {
+SCR_DEV uint64_t draw_raw(Rng& r, uint32_t thr) {
   for (;;) {
     const uint64_t v = rng_next(r);
     if (v >= thr) return v;
   }
 }
-
 
 // uniform_int by rejection (rng.hpp:50-56) with a precomputed Barrett reciprocal/threshold.
 SCR_DEV uint64_t draw_exact(Rng& r, uint64_t n, uint64_t m, uint64_t thr) {
@@ -264,7 +271,7 @@ SCR_DEV bool geometry_exact(double min_sq_dist, double rigidity_tol, const int4*
 // draws pixel, mode, pixel, mode, pixel, mode, colour-pair index from the slot stream with
 // rejection sampling, returns whether the attempt reached the colour check and passed it.
 SCR_DEV bool attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, const PredView& pv,
-                           const int* s_lbase, const uint64_t* s_m, const uint64_t* s_thr, size_t fbase, uint64_t G,
+                           const int* s_lbase, const uint64_t* s_m, size_t fbase, uint64_t G,
                            uint64_t mG, uint64_t tG, bool fast, int& g0, int& g1, int& g2, int& m0, int& m1,
                            int& m2) {
   constexpr uint64_t m3 = 0x5555555555555555ull, t3 = 1;  // floor((2^64-1)/3), 2^64 mod 3
@@ -276,19 +283,19 @@ SCR_DEV bool attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, c
   L0 = fr.gleaf[2 * (fbase + g0) + 1];
   const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
   if (nm0 <= 0) return false;
-  p0 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm0), s_m[nm0], s_thr[nm0]));
+  p0 = static_cast<int>(draw_exact_lazy(rng, static_cast<uint64_t>(nm0), s_m[nm0]));
   g1 = static_cast<int>(draw_exact(rng, G, mG, tG));
   A1 = fr.grec[2 * (fbase + g1)];
   L1 = fr.gleaf[2 * (fbase + g1) + 1];
   const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
   if (nm1 <= 0) return false;
-  p1 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm1), s_m[nm1], s_thr[nm1]));
+  p1 = static_cast<int>(draw_exact_lazy(rng, static_cast<uint64_t>(nm1), s_m[nm1]));
   g2 = static_cast<int>(draw_exact(rng, G, mG, tG));
   A2 = fr.grec[2 * (fbase + g2)];
   L2 = fr.gleaf[2 * (fbase + g2) + 1];
   const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
   if (nm2 <= 0) return false;
-  p2 = static_cast<int>(draw_exact(rng, static_cast<uint64_t>(nm2), s_m[nm2], s_thr[nm2]));
+  p2 = static_cast<int>(draw_exact_lazy(rng, static_cast<uint64_t>(nm2), s_m[nm2]));
   cc = static_cast<int>(draw_exact(rng, 3, m3, t3));
   if (fast) {
     m0 = mode_from_record(s_lbase, static_cast<uint32_t>(A0.w), L0, p0);
@@ -325,8 +332,15 @@ constexpr int kMaxSuspects = 64;  // per frame: triplets whose Kabsch may be deg
 constexpr int kCandResolved = 1 << 30;  // flag in slot: m0..m2 hold mode indices
 struct GenCand {
   int slot, owner_att;  // slot (| kCandResolved), owner lane | attempt << 5
-  int g0, g1, g2;
+  uint32_t gA, gB;      // the three grid pixels (< 2^17 each), packed: g0 | g1 << 17, g1 >> 15 | g2 << 2
   uint2 r0, r1, r2;     // raw 64-bit draws of the three modes, or {m, 0}
+  SCR_DEV void set_pixels(int g0, int g1, int g2) {
+    gA = static_cast<uint32_t>(g0) | (static_cast<uint32_t>(g1) << 17);
+    gB = (static_cast<uint32_t>(g1) >> 15) | (static_cast<uint32_t>(g2) << 2);
+  }
+  SCR_DEV int g0() const { return static_cast<int>(gA & 0x1ffffu); }
+  SCR_DEV int g1() const { return static_cast<int>((gA >> 17) | ((gB & 3u) << 15)); }
+  SCR_DEV int g2() const { return static_cast<int>(gB >> 2); }
 };
 
 SCR_DEV uint64_t u64_of(uint2 v) { return static_cast<uint64_t>(v.x) | (static_cast<uint64_t>(v.y) << 32); }
@@ -338,7 +352,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
                                                    int* __restrict__ hiters, int* __restrict__ sus_cnt,
                                                    int4* __restrict__ sus, unsigned long long* __restrict__ work) {
   __shared__ uint64_t s_m[kMaxModeUnion + 1];    // Barrett reciprocal for mode counts 1..400
-  __shared__ uint64_t s_thr[kMaxModeUnion + 1];  // rejection threshold (2^64 mod n)
+  __shared__ uint32_t s_thr[kMaxModeUnion + 1];  // rejection threshold 2^64 mod n (< n < 2^32)
   __shared__ int s_lbase[kMaxTrees];
   __shared__ GenCand s_q[kGenWarps][kGenQ];
   __shared__ int s_best[kGenWarps][32];  // smallest passing attempt of the lane's slot
@@ -349,7 +363,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
     const uint64_t n = i ? static_cast<uint64_t>(i) : 1;
     const uint64_t m = barrett_m(n);
     s_m[i] = m;
-    s_thr[i] = mod_barrett(0 - n, n, m);
+    s_thr[i] = static_cast<uint32_t>(mod_barrett(0 - n, n, m));
   }
   if (threadIdx.x < kMaxTrees) s_lbase[threadIdx.x] = gp.leaf_base[threadIdx.x];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -436,17 +450,17 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
             push = true;
             c.slot = slot;
             c.owner_att = lane | (it << 5);
-            c.g0 = g0; c.g1 = g1; c.g2 = g2;
+            c.set_pixels(g0, g1, g2);
             c.r0 = u2_of(v1); c.r1 = u2_of(v3); c.r2 = u2_of(v5);
           }
         }
       } else {  // > 5 trees or 32-bit leaf ids: modes through the slot tables
         int g0, g1, g2, m0, m1, m2;
-        if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, s_thr, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2)) {
+        if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2)) {
           push = true;
           c.slot = slot | kCandResolved;
           c.owner_att = lane | (it << 5);
-          c.g0 = g0; c.g1 = g1; c.g2 = g2;
+          c.set_pixels(g0, g1, g2);
           c.r0 = make_uint2(m0, 0); c.r1 = make_uint2(m1, 0); c.r2 = make_uint2(m2, 0);
         }
       }
@@ -472,19 +486,22 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
       // ---- evaluate the oldest <= 32 candidates, one per lane
       const int nproc = qn < 32 ? qn : 32;
       bool pass = false;
-      int owner = 0, att = 0, eslot = -1;
+      int owner = 0, att = 0, eslot = -1, eg0 = 0, eg1 = 0, eg2 = 0;
       GenCand e;
       if (lane < nproc) {
         e = q[lane];
+        eg0 = e.g0();
+        eg1 = e.g1();
+        eg2 = e.g2();
         owner = e.owner_att & 31;
         att = e.owner_att >> 5;
         eslot = e.slot & ~kCandResolved;
         if (s_cur[wid][owner] == eslot) {  // stale if the owner's slot was already resolved
           if (!(e.slot & kCandResolved)) {  // mode indices of the three raw draws (fast path)
             const int4* gr = fr.grec + 2 * fbase;
-            const int4 A0 = gr[2 * e.g0], A1 = gr[2 * e.g1], A2 = gr[2 * e.g2];
-            const uint4 L0 = fr.gleaf[2 * (fbase + e.g0) + 1], L1 = fr.gleaf[2 * (fbase + e.g1) + 1],
-                        L2 = fr.gleaf[2 * (fbase + e.g2) + 1];
+            const int4 A0 = gr[2 * eg0], A1 = gr[2 * eg1], A2 = gr[2 * eg2];
+            const uint4 L0 = fr.gleaf[2 * (fbase + eg0) + 1], L1 = fr.gleaf[2 * (fbase + eg1) + 1],
+                        L2 = fr.gleaf[2 * (fbase + eg2) + 1];
             const uint32_t nm0 = static_cast<uint32_t>(A0.z) >> 24, nm1 = static_cast<uint32_t>(A1.z) >> 24,
                            nm2 = static_cast<uint32_t>(A2.z) >> 24;
             const int p0 = static_cast<int>(mod_barrett32(u64_of(e.r0), nm0, s_m[nm0]));
@@ -497,14 +514,14 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
           const int em0 = static_cast<int>(e.r0.x), em1 = static_cast<int>(e.r1.x), em2 = static_cast<int>(e.r2.x);
           bool regular = true;
           pass = geometry_prefilter(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, ifx, ify, pv.geom,
-                                    e.g0, e.g1, e.g2, em0, em1, em2) &&
-                 distance_checks_f64(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, pv.geom, e.g0, e.g1,
-                                     e.g2, em0, em1, em2, nullptr, nullptr, &regular);
+                                    eg0, eg1, eg2, em0, em1, em2) &&
+                 distance_checks_f64(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, pv.geom, eg0, eg1,
+                                     eg2, em0, em1, em2, nullptr, nullptr, &regular);
           if (pass && (!regular || gp.force_suspect)) {  // Kabsch may be degenerate: k_hypfin decides, the slot goes on
             const int i = atomicAdd(&sus_cnt[a], 1);
             if (i < kMaxSuspects) {
               int4* sp = sus + 2 * (static_cast<size_t>(a) * kMaxSuspects + i);
-              sp[0] = make_int4(att, e.g0, e.g1, e.g2);
+              sp[0] = make_int4(att, eg0, eg1, eg2);
               sp[1] = make_int4(em0, em1, em2, eslot);
               pass = false;
             }  // list full: stop here as usual, k_hypfin continues exactly if Kabsch fails
@@ -516,7 +533,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
       __syncwarp();
       if (pass && s_best[wid][owner] == att) {
         int4* hc = hcand + 2 * (static_cast<size_t>(a) * gp.nmax + eslot);
-        hc[0] = make_int4(att, e.g0, e.g1, e.g2);
+        hc[0] = make_int4(att, eg0, eg1, eg2);
         hc[1] = make_int4(static_cast<int>(e.r0.x), static_cast<int>(e.r1.x), static_cast<int>(e.r2.x), 0);
       }
       // drop the evaluated entries
@@ -566,7 +583,6 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
                                                         const int* __restrict__ sus_cnt, const int4* __restrict__ sus,
                                                         unsigned long long* __restrict__ work) {
   __shared__ uint64_t s_m[kMaxModeUnion + 1];
-  __shared__ uint64_t s_thr[kMaxModeUnion + 1];
   __shared__ int s_lbase[kMaxTrees];
   __shared__ int4 s_sus[kMaxSuspects][2];
   const int a = blockIdx.y;
@@ -628,7 +644,6 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
     const uint64_t n = i ? static_cast<uint64_t>(i) : 1;
     const uint64_t m = barrett_m(n);
     s_m[i] = m;
-    s_thr[i] = mod_barrett(0 - n, n, m);
   }
   if (threadIdx.x < kMaxTrees) s_lbase[threadIdx.x] = gp.leaf_base[threadIdx.x];
   __syncthreads();
@@ -642,9 +657,9 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
   int it = 0;
   int g0, g1, g2, m0, m1, m2;
   for (; it <= att; ++it)  // replay through the recorded attempt
-    attempt_exact(rng, gp, fr, pv, s_lbase, s_m, s_thr, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2);
+    attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2);
   for (; it < gp.max_iters && !ok; ++it) {
-    if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, s_thr, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2) &&
+    if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2) &&
         geometry_prefilter(gp.min_sq_dist, gp.rigidity_tol, grec, g, ifx, ify, pv.geom, g0, g1, g2, m0, m1, m2))
       ok = geometry_exact(gp.min_sq_dist, gp.rigidity_tol, grec, g, pv.geom, g0, g1, g2, m0, m1, m2, &T);
   }
