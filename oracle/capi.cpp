@@ -544,3 +544,56 @@ int or_integrate_batch(void* sp, void* fp, const float* depth, const uint8_t* rg
   });
 }
 }
+
+extern "C" {
+// Generation diagnostics (test/fixture infrastructure): runs generate_hypothesis for every
+// slot of one frame and histograms the outcome of every attempt by rejection tag
+// (tags[6] indexed by Reject: OK, NoModes, ColourCheckFailed, TooClose, NotRigid,
+// DegenerateKabsch). With a ground-truth pose it also reports mode quality: the fraction
+// of (grid pixel, predicted mode) pairs whose mean lies within `radius` of the pixel's
+// true world point, and the fraction of moded grid pixels having at least one such mode.
+int or_generation_stats(void* fp, void* sp, const float* depth, const uint8_t* rgb, const or_intrinsics* k,
+                        const or_ransac_params* rp, uint64_t seed, const or_pose* gt, double radius, int64_t* tags,
+                        int* slots_ok, double* mode_frac, double* pixel_frac) {
+  return guarded([&] {
+    const Frame fr = mk_frame(depth, rgb, *k, 1);
+    const AdaptState& s = *static_cast<AdaptState*>(sp);
+    FrameCtx c;
+    build_frame_ctx(c, *static_cast<Forest*>(fp), s, fr);
+    const RansacParams p = to_rp(*rp);
+    for (int i = 0; i < 6; ++i) tags[i] = 0;
+    *slots_ok = 0;
+    for (int slot = 0; slot < p.n_max; ++slot) {
+      Rng rng = Rng::stream(seed, static_cast<uint64_t>(slot));
+      Pose h;
+      int att = 0;
+      if (generate_hypothesis(c, s, p, rng, &h, &att, tags) == REJ_OK) ++*slots_ok;
+    }
+    *mode_frac = *pixel_frac = 0.0;
+    if (gt) {
+      const Pose T = to_pose(gt->R, gt->t);
+      int64_t good = 0, total = 0, px_good = 0, px_total = 0;
+      for (size_t g = 0; g < c.grid.size(); ++g) {
+        const int nm = c.nmodes[g];
+        if (nm == 0) continue;
+        double w[3];
+        transform_point(T, &c.cam[3 * g], w);
+        bool any = false;
+        for (int m = 0; m < nm; ++m) {
+          const Mode* md = ctx_mode(c, s, static_cast<int>(g), m);
+          const double d0 = w[0] - md->mu[0], d1 = w[1] - md->mu[1], d2 = w[2] - md->mu[2];
+          const bool ok = d0 * d0 + d1 * d1 + d2 * d2 <= radius * radius;
+          good += ok;
+          any = any || ok;
+        }
+        total += nm;
+        px_good += any;
+        ++px_total;
+      }
+      *mode_frac = total ? static_cast<double>(good) / total : 0.0;
+      *pixel_frac = px_total ? static_cast<double>(px_good) / px_total : 0.0;
+    }
+    return 0;
+  });
+}
+}

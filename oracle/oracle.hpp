@@ -205,8 +205,10 @@ struct Hypothesis {
   float energy = 0;
   int iterations = 0;  // generation attempts used
 };
+// tags (optional): per-attempt outcome histogram, indexed by Reject (REJ_OK counts the
+// successful final attempt). Diagnostic only; never changes the draws.
 int generate_hypothesis(const FrameCtx& c, const AdaptState& s, const RansacParams& p, Rng& rng, Pose* out,
-                        int* attempts);
+                        int* attempts, int64_t* tags = nullptr);
 // Eq. 5 accumulated per eta-sample batch: E = sum_b E_b (batches in order), E_b sequential.
 float energy(const FrameCtx& c, const AdaptState& s, const Pose& H, const std::vector<int>& samples, int eta);
 void draw_samples(uint64_t seed, int batch, int n_max, int eta, int G, std::vector<int>& out);

@@ -166,6 +166,8 @@ class Oracle:
             "or_depth_diff_images": (dbl, [P(flt), P(flt), C.c_int, C.c_int]),
             "or_raycast_depth": (None, [vp, P(Pose), P(Intrinsics), P(flt)]),
             "or_stage_seed": (u64, [u64, C.c_int]),
+            "or_generation_stats": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(RansacParams), u64,
+                                              P(Pose), dbl, P(C.c_int64), P(C.c_int), P(dbl), P(dbl)]),
             "or_energy": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(Pose), P(i32), C.c_int, P(flt)]),
             "or_lm": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(Pose), P(i32), C.c_int, C.c_int,
                                 P(dbl)]),

@@ -57,7 +57,7 @@ static inline double d2_3(const double* a, const double* b) {
 // {pixel = uniform_int(G); NoModes if empty; mode = uniform_int(|M|)}, then the
 // colour-check correspondence uniform_int(3) (A7).
 int generate_hypothesis(const FrameCtx& c, const AdaptState& s, const RansacParams& p, Rng& rng, Pose* out,
-                        int* attempts) {
+                        int* attempts, int64_t* tags) {
   const uint64_t G = c.grid.size();
   int last = REJ_NO_MODES;
   *attempts = 0;
@@ -78,6 +78,7 @@ int generate_hypothesis(const FrameCtx& c, const AdaptState& s, const RansacPara
     }
     if (!ok) {
       last = REJ_NO_MODES;
+      if (tags) ++tags[REJ_NO_MODES];
       continue;
     }
     const int cc = static_cast<int>(rng.uniform_int(3));
@@ -89,6 +90,7 @@ int generate_hypothesis(const FrameCtx& c, const AdaptState& s, const RansacPara
         linf = std::fmax(linf, std::fabs(static_cast<float>(c.frame->rgb[3 * idx + ch]) - mm[cc]->colour[ch]));
       if (linf > p.colour_thresh) {
         last = REJ_COLOUR;
+        if (tags) ++tags[REJ_COLOUR];
         continue;
       }
     }
@@ -108,18 +110,22 @@ int generate_hypothesis(const FrameCtx& c, const AdaptState& s, const RansacPara
     }
     if (close) {
       last = REJ_TOO_CLOSE;
+      if (tags) ++tags[REJ_TOO_CLOSE];
       continue;
     }
     for (int q = 0; q < 3; ++q)
       if (std::fabs(std::sqrt(dw2[q]) - std::sqrt(dc2[q])) > p.rigidity_tol) nonrigid = true;
     if (nonrigid) {
       last = REJ_NOT_RIGID;
+      if (tags) ++tags[REJ_NOT_RIGID];
       continue;
     }
     if (!kabsch(cm, w, 3, out)) {
       last = REJ_DEGENERATE;
+      if (tags) ++tags[REJ_DEGENERATE];
       continue;
     }
+    if (tags) ++tags[REJ_OK];
     return REJ_OK;
   }
   return last;

@@ -223,6 +223,17 @@ void render_frame(const Scene& s, const Pose& T, const Intrinsics& k, float* dep
     }
 }
 
+// Uniform direction on the unit sphere from two draws (z = 2u - 1, azimuth 2 pi u').
+static void unit_dir(Rng& r, double v[3]) {
+  const double z = 2.0 * r.uniform() - 1.0, phi = 6.283185307179586 * r.uniform();
+  double sp, cp;
+  det_sincos(phi, &sp, &cp);
+  const double rr = std::sqrt(std::max(0.0, 1.0 - z * z));
+  v[0] = rr * cp;
+  v[1] = rr * sp;
+  v[2] = z;
+}
+
 static Pose look_pose(double px, double py, double pz, double yaw, double pitch, double roll) {
   double sy, cy, sp, cp, sr, cr;
   det_sincos(yaw, &sy, &cy);
@@ -247,7 +258,11 @@ static Pose look_pose(double px, double py, double pz, double yaw, double pitch,
 
 // Smooth loop around the room centre. kind 0 = adaptation
 // sequence; kind 1 = held-out test poses: the same loop sampled half a step
-// off, perturbed by up to +-6 cm / +-6 deg (seeded).
+// off, perturbed by up to +-6 cm / +-6 deg (seeded); kind 2 = the held-out
+// novel-pose set: frame i targets novelty bin b = i mod 11, i.e. a
+// translation offset of 5b..5b+5 cm in a uniformly random direction and a rotation offset
+// of 5b..5b+5 deg (yaw/pitch/roll along a uniformly random direction), so the offsets span
+// every bin up to 55 cm / 55 deg; positions are clamped to the room's free camera volume.
 void generate_trajectory(uint64_t seed, int n, int kind, Pose* out) {
   Rng rng(seed);
   const double twopi = 6.283185307179586;
@@ -255,7 +270,7 @@ void generate_trajectory(uint64_t seed, int n, int kind, Pose* out) {
                ph3 = twopi * rng.uniform();
   Rng pert = Rng::stream(seed, 0x7e57ull);
   for (int i = 0; i < n; ++i) {
-    const double s = (i + (kind == 1 ? 0.5 : 0.0)) / static_cast<double>(n);
+    const double s = (i + (kind != 0 ? 0.5 : 0.0)) / static_cast<double>(n);
     double a, b, c, d;
     det_sincos(twopi * s + ph0, &a, &b);
     det_sincos(2 * twopi * s + ph1, &c, &d);
@@ -271,6 +286,19 @@ void generate_trajectory(uint64_t seed, int n, int kind, Pose* out) {
       yaw += 6 * deg * (2 * pert.uniform() - 1);
       pitch += 6 * deg * (2 * pert.uniform() - 1);
       roll += 3 * deg * (2 * pert.uniform() - 1);
+    } else if (kind == 2) {
+      const double deg = 0.017453292519943295;
+      const int b = i % 11;
+      const double rt = 0.05 * (b + pert.uniform()), ra = 5.0 * deg * (b + pert.uniform());
+      double v[3], q[3];
+      unit_dir(pert, v);
+      unit_dir(pert, q);
+      px = std::min(2.8, std::max(1.2, px + rt * v[0]));
+      py = std::min(1.95, std::max(1.05, py + rt * v[1]));
+      pz = std::min(2.2, std::max(0.5, pz + rt * v[2]));
+      yaw += ra * q[0];
+      pitch += ra * q[1];
+      roll += ra * q[2];
     }
     out[i] = look_pose(px, py, pz, yaw, pitch, roll);
   }

@@ -4,6 +4,7 @@
 //   serialize_forest         proj/include/screloc/forest.hpp:108 (format SPEC.md:300)
 //   generate_synthetic_scene / generate_trajectory   SPEC.md:565-572 (benchmark fixture)
 // They run once per scene, on the host, and produce the inputs the GPU consumes.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -240,7 +241,20 @@ int scr_generate_synthetic_scene(uint64_t seed, int complexity, scr_prim* out, i
 
 // generate_trajectory(seed, n, kind): kind 0 = smooth adaptation loop around the room
 // centre; kind 1 = held-out test poses (same loop half a step off, perturbed by up to
-// +-6 cm / +-6 deg / +-3 deg roll).
+// +-6 cm / +-6 deg / +-3 deg roll); kind 2 = held-out novel-pose set:
+// frame i targets novelty bin b = i mod 11 (offset 5b..5b+5 cm along a uniform random
+// direction, 5b..5b+5 deg of yaw/pitch/roll along another), positions clamped to the
+// free camera volume, so the set spans every bin up to 55 cm / 55 deg.
+static void unit_dir(HostRng& r, double v[3]) {
+  const double z = 2.0 * r.uniform() - 1.0, phi = 6.283185307179586 * r.uniform();
+  double sp, cp;
+  sincos_det(phi, &sp, &cp);
+  const double rr = std::sqrt(std::max(0.0, 1.0 - z * z));
+  v[0] = rr * cp;
+  v[1] = rr * sp;
+  v[2] = z;
+}
+
 void scr_generate_trajectory(uint64_t seed, int n, int kind, scr_pose* out) {
   HostRng rng(seed);
   const double twopi = 6.283185307179586;
@@ -249,7 +263,7 @@ void scr_generate_trajectory(uint64_t seed, int n, int kind, scr_pose* out) {
   HostRng pert = HostRng::stream(seed, 0x7e57ull);
   (void)ph1;
   for (int i = 0; i < n; ++i) {
-    const double s = (i + (kind == 1 ? 0.5 : 0.0)) / static_cast<double>(n);
+    const double s = (i + (kind != 0 ? 0.5 : 0.0)) / static_cast<double>(n);
     double a, b, c, d, e, g;
     sincos_det(twopi * s + ph0, &a, &b);
     sincos_det(2 * twopi * s + ph1, &c, &d);
@@ -264,6 +278,19 @@ void scr_generate_trajectory(uint64_t seed, int n, int kind, scr_pose* out) {
       yaw += 6 * deg * (2 * pert.uniform() - 1);
       pitch += 6 * deg * (2 * pert.uniform() - 1);
       roll += 3 * deg * (2 * pert.uniform() - 1);
+    } else if (kind == 2) {
+      const double deg = 0.017453292519943295;
+      const int bn = i % 11;
+      const double rt = 0.05 * (bn + pert.uniform()), ra = 5.0 * deg * (bn + pert.uniform());
+      double v[3], q[3];
+      unit_dir(pert, v);
+      unit_dir(pert, q);
+      px = std::min(2.8, std::max(1.2, px + rt * v[0]));
+      py = std::min(1.95, std::max(1.05, py + rt * v[1]));
+      pz = std::min(2.2, std::max(0.5, pz + rt * v[2]));
+      yaw += ra * q[0];
+      pitch += ra * q[1];
+      roll += ra * q[2];
     }
     double sy, cy, sp, cp, sr, cr;
     sincos_det(yaw, &sy, &cy);

@@ -149,20 +149,33 @@ def success_curve(outcomes: Sequence[FrameOutcome | None], window: int = 0) -> n
     return np.convolve(s, k, "full")[: s.size] / np.minimum(np.arange(1, s.size + 1), window)
 
 
+def novelty_bin_keys(test_poses, training_poses, step: int = 5, last: int = 55) -> np.ndarray:
+    """Novelty bin of every test pose: the first b in (5, 10, ..., `last`)
+    such that some training pose is within b cm AND b degrees, else `last` + `step`.
+    Vectorised over the training poses (same pose_error arithmetic, geometry.hpp:206-216)."""
+    tr = [pose_arrays(to_pose(p)) for p in training_poses]
+    Rt = np.stack([r for r, _ in tr])            # (n, 3, 3)
+    tt = np.stack([t for _, t in tr])            # (n, 3)
+    edges = np.arange(step, last + step, step, dtype=float)
+    keys = np.empty(len(test_poses), np.int64)
+    for i, tp in enumerate(test_poses):
+        R, t = pose_arrays(to_pose(tp))
+        te = np.linalg.norm(tt - t, axis=1) * 100.0
+        c = (np.einsum("nij,ij->n", Rt, R) - 1.0) / 2.0  # trace(R_t^T R)
+        ae = np.degrees(np.arccos(np.clip(c, -1.0, 1.0)))
+        need = np.maximum(te, ae).min()  # smallest b with te <= b and ae <= b for one pose
+        hit = edges[edges >= need]
+        keys[i] = int(hit[0]) if hit.size else last + step
+    return keys
+
+
 def compute_novelty_bins(test_poses, outcomes: Sequence[FrameOutcome], training_poses, step: int = 5,
                          last: int = 55) -> dict:
     """A test pose belongs to the first bin b (5, 10, ..., `last` cm/deg) such that some
     training pose is within b cm AND b degrees of it; otherwise to the open bin `last`+.
     Returns {bin: (count, success fraction)}; the open bin is keyed by `last` + `step`."""
-    train = [pose_arrays(to_pose(p)) for p in training_poses]
+    keys = novelty_bin_keys(test_poses, training_poses, step, last)
     bins: dict[int, list[bool]] = {b: [] for b in range(step, last + 2 * step, step)}
-    for tp, o in zip(test_poses, outcomes):
-        R, t = pose_arrays(to_pose(tp))
-        errs = [pose_error(R, t, Rt, tt) for Rt, tt in train]
-        key = last + step
-        for b in range(step, last + step, step):
-            if any(te * 100.0 <= b and ae <= b for te, ae in errs):
-                key = b
-                break
-        bins[key].append(bool(o.success))
+    for key, o in zip(keys, outcomes):
+        bins[int(key)].append(bool(o.success))
     return {b: (len(v), (sum(v) / len(v)) if v else math.nan) for b, v in bins.items()}

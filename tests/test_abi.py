@@ -70,7 +70,7 @@ def test_scene_and_trajectory_generators_match_oracle(oracle):
     for seed in (1, 2, 7):
         s = oracle.lib.or_scene_generate(seed, 20)
         assert P.generate_synthetic_scene(seed, 20).tobytes() == oracle.scene_prims(s).tobytes()
-        for kind in (0, 1):
+        for kind in (0, 1, 2):
             a = P.generate_trajectory(seed, 37, kind)
             b = oracle.trajectory(seed, 37, kind)
             assert all(bytes(x) == bytes(y) for x, y in zip(a, b))

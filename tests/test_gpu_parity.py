@@ -201,6 +201,31 @@ def test_cascade_matches_oracle(oracle, gpu_device):
             assert bytes(a.pose) == bytes(b.pose)
 
 
+def test_cascade_novel_poses_resolve_at_every_stage(oracle, gpu_device):
+    """Held-out novel poses (trajectory kind 2, offsets up to 55 cm / 55 deg):
+    frames resolve at the Fast, Intermediate and Slow stages and some end without a pose; the
+    GPU cascade equals the oracle's frame for frame (stage used, pose bytes, score)."""
+    import paper_1810_12163_b200 as P
+
+    w = OracleWorld(oracle, scene_seed=2, n_adapt=30, n_test=22, forest=of.FOREST_CASCADE, test_kind=2)
+    s = gpu_scene(gpu_device, w, max_batch=22)
+    s.integrate_frames(list(w.D), list(w.RGB), w.adapt_poses)
+    s.update_leaves_round_robin(s.total_leaves)
+    cfg = P.CascadeConfig.paper_three_stage()
+    seeds = [77 + i for i in range(len(w.test_poses))]
+    res = s.run_cascade_batch(w.Dt, w.RGBt, cfg, seeds)
+    ref = oracle.cascade_batch(w.forest, w.state, w.scene, w.Dt, w.RGBt, K,
+                               [of.ransac_params(p) for p in ("fast", "intermediate", "slow")],
+                               list(of.CASCADE_MODES), list(of.CASCADE_THRESHOLDS), seeds)
+    stages = [b.stage_used for b in ref]
+    assert {0, 1, 2} <= set(stages) and not all(b.has_pose for b in ref), stages
+    for i, (a, b) in enumerate(zip(res, ref)):
+        assert a.stage_used == b.stage_used and a.has_pose == b.has_pose, i
+        assert a.score == b.score or (np.isinf(a.score) and np.isinf(b.score)), i
+        if a.has_pose:
+            assert bytes(a.pose) == bytes(b.pose), i
+
+
 def test_batch_invariance(world, gscene):
     """Results depend only on (frame, seed): batch composition never changes them."""
     import paper_1810_12163_b200 as P

@@ -12,7 +12,7 @@ class OracleWorld:
     """Scene + random forest + adapted state on the CPU oracle."""
 
     def __init__(self, oracle, scene_seed=1, n_adapt=30, n_test=6, forest=of.FOREST_DEFAULT, cluster=True,
-                 adapt_seed=7, forest_seed=42, k=None):
+                 adapt_seed=7, forest_seed=42, k=None, test_kind=1):
         self.O = O = oracle
         self.k = k = K if k is None else k
         L = O.lib
@@ -21,7 +21,7 @@ class OracleWorld:
         self.scene = L.or_scene_generate(scene_seed, 20)
         self.prims = O.scene_prims(self.scene)
         self.adapt_poses = O.trajectory(scene_seed, n_adapt, 0)
-        self.test_poses = O.trajectory(scene_seed, n_test, 1)
+        self.test_poses = O.trajectory(scene_seed, n_test, test_kind)
         self.D, self.RGB = O.render(self.scene, self.adapt_poses, k)
         self.Dt, self.RGBt = O.render(self.scene, self.test_poses, k)
         self.forest = L.or_forest_random(forest_seed, 14, 0.4, 5, 130)
