@@ -1,28 +1,38 @@
 #!/usr/bin/env python
 """Relocalisations/s of the full F(5 cm) -> I(7.5 cm) -> S cascade at 640x480 on B200.
 
-Workload (BASELINE.json configs[1] + configs[2]): one synthetic 7-Scenes-like room (20
-primitives), a 5-tree random SCoRe forest (h = 14, p = 0.4) adapted on a 1000-frame
+Default workload (BASELINE.json configs[1] + configs[2]): one synthetic 7-Scenes-like room
+(20 primitives), a 5-tree random SCoRe forest (h = 14, p = 0.4) adapted on a 1000-frame
 sequence (integrate + every leaf clustered), then the 3-stage cascade (Fast w/ ICP,
-Intermediate w/ ICP, Slow w/ ranking of 16) on held-out test frames. One step = one
-cascade over lanes x batch frames already resident in HBM, each relocalisation lane (own
-stream + host thread) taking one batch of every step; `e2e` = the same through the C ABI
-with pinned host frames (H2D + result D2H inside the timed region).
+Intermediate w/ ICP, Slow w/ ranking of 16) on the held-out novel-pose set (offsets up to
+55 cm / 55 deg). One step = one cascade over lanes x batch frames already
+resident in HBM, each relocalisation lane (own stream + host thread) taking one batch of
+every step; `e2e` = the same through the C ABI with pinned host frames (H2D + result D2H
+inside the timed region).
 
-Multi-GPU (torchrun): weak scaling, frames sharded by rank, the adapted prediction table
-broadcast from rank 0 over NCCL once (no per-frame collective); time = max over ranks.
-`--impl reference` times the CPU oracle restatement of the reference on all host cores.
+`--workload` selects the other configurations (one JSON line each, same contract):
+default-raw / default-icp / default-ranked (configs 1-2, Default profile + forest), fast /
+intermediate / slow (the cascade's stages alone), stress (config 5: 1280x960, kappa 4096,
+2x N_max), scenes (config 4: 8 scenes, scene s -> rank s mod N, forest replicated) and adapt
+(per-frame training: integrate + update(256) on full reservoirs).
+
+Multi-GPU: `python bench.py --gpus N` launches N ranks itself (torch.distributed.run) unless
+it already runs under torchrun; weak scaling, frames sharded by rank, the adapted prediction
+table broadcast from rank 0 over NCCL once (no per-frame collective); time = max over ranks.
+`--impl reference` times the CPU oracle restatement of the reference on the host cores (the
+reference itself cannot be built); it never loads the B200 library.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import subprocess
 import sys
 import threading
 import time
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -31,15 +41,72 @@ sys.path.insert(0, ROOT)
 
 METRIC = "relocalisations/sec @640×480 (1/2/4/8 B200) + 5cm/5° accuracy vs CPU ref"
 UNIT = "relocalisations/s"
-WORKLOAD = ("cascade F(5cm)->I(7.5cm)->S, forest adapted on 1000 frames, held-out novel poses (offsets up to "
-            "55 cm/55 deg, SPEC.md:567-572), 640x480 synthetic")
-SCENE_SEED, FOREST_SEED, ADAPT_SEED, RUN_SEED = 1, 42, 7, 1234
+FOREST_SEED, ADAPT_SEED, RUN_SEED = 42, 7, 1234
+SCENE_SEED = 1
+MODE_RAW, MODE_ICP, MODE_RANKED = 0, 1, 2
+
+# Table 4 forest profiles — kept here so that the reference arm never
+# imports the B200 package (oracle_ffi holds the same table).
+FOREST_DEFAULT = dict(sigma=0.1, tau=0.05, max_clusters=50, min_cluster_size=20, capacity=1024)
+FOREST_CASCADE = dict(sigma=0.1, tau=0.2, max_clusters=50, min_cluster_size=5, capacity=2048)
+
+
+@dataclass
+class Workload:
+    name: str
+    desc: str
+    forest: dict
+    stages: tuple            # ((profile, mode), ...)
+    thresholds: tuple = ()
+    res: tuple = (640, 480)
+    nmax_scale: int = 1
+    scenes: int = 1
+    batch: int = 128
+    lanes: int = 5
+    scaling: str = "weak"
+    paper_ms: float | None = None
+    paper_ref: str = ""
+    extra: dict = field(default_factory=dict)
+
+
+CASCADE3 = (("fast", MODE_ICP), ("intermediate", MODE_ICP), ("slow", MODE_RANKED))
+WORKLOADS = {
+    "cascade": Workload("cascade", "cascade F(5cm)->I(7.5cm)->S, forest adapted on 1000 frames, held-out novel poses "
+                        "(offsets up to 55 cm/55 deg, SPEC.md:567-572), 640x480 synthetic", FOREST_CASCADE, CASCADE3,
+                        (0.05, 0.075), paper_ms=66.1, paper_ref="PAPER.md:734"),
+    "default-raw": Workload("default-raw", "Default profile, raw RANSAC output (configs 1-2)", FOREST_DEFAULT,
+                            (("default", MODE_RAW),), paper_ms=128.0, paper_ref="PAPER.md:726"),
+    "default-icp": Workload("default-icp", "Default profile + ICP (configs 1-2)", FOREST_DEFAULT,
+                            (("default", MODE_ICP),), paper_ms=132.7, paper_ref="PAPER.md:727"),
+    "default-ranked": Workload("default-ranked", "Default profile + ranking of 16 (configs 1-2)", FOREST_DEFAULT,
+                               (("default", MODE_RANKED),), paper_ms=256.8, paper_ref="PAPER.md:728"),
+    "fast": Workload("fast", "Fast w/ ICP alone (cascade forest)", FOREST_CASCADE, (("fast", MODE_ICP),),
+                     paper_ms=29.91, paper_ref="PAPER.md:1157"),
+    "intermediate": Workload("intermediate", "Intermediate w/ ICP alone (cascade forest)", FOREST_CASCADE,
+                             (("intermediate", MODE_ICP),), paper_ms=77.87, paper_ref="PAPER.md:1159"),
+    "slow": Workload("slow", "Slow w/ ranking of 16 alone (cascade forest)", FOREST_CASCADE,
+                     (("slow", MODE_RANKED),), paper_ms=203.64, paper_ref="PAPER.md:1163"),
+    "stress": Workload("stress", "config 5 stress: 1280x960, kappa 4096, 2x N_max in every stage, F->I->S cascade",
+                       dict(FOREST_CASCADE, capacity=4096), CASCADE3, (0.05, 0.075), res=(1280, 960), nmax_scale=2,
+                       batch=32),
+    "scenes": Workload("scenes", "config 4: 8 synthetic scenes (seeds 1..8), scene s -> rank s mod N, forest "
+                       "replicated, F->I->S cascade on each scene's novel poses", FOREST_CASCADE, CASCADE3,
+                       (0.05, 0.075), scenes=8, scaling="strong"),
+    "adapt": Workload("adapt", "per-frame training on full reservoirs: integrate_frame + update_leaves_round_robin"
+                      "(256) per frame, kappa 2048 (PAPER.md:726-734)", FOREST_CASCADE, (), batch=1,
+                      paper_ms=11.0, paper_ref="PAPER.md:731"),
+}
 
 
 # ------------------------------------------------------------------ host-side plumbing
 def shard(n_total: int, rank: int, world: int) -> list:
     """Frame f goes to rank f mod world."""
     return list(range(rank, n_total, world))
+
+
+def scenes_of_rank(n_scenes: int, rank: int, world: int) -> list:
+    """Scene s (seeds 1..n) goes to rank (s - 1) mod world."""
+    return [s for s in range(1, n_scenes + 1) if (s - 1) % world == rank]
 
 
 def frame_seed(run_seed: int, frame: int) -> int:
@@ -56,9 +123,23 @@ def dist_env():
 def dist_init(backend: str):
     import torch.distributed as dist
 
+    if backend == "nccl":  # communicator creation goes to stderr (comm ... nranks N)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if not dist.is_initialized():
         dist.init_process_group(backend=backend)
     return dist
+
+
+def self_launch(args, argv) -> int:
+    """`bench.py --gpus N` outside torchrun: run N ranks (one process per GPU) under
+    torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 def max_over_ranks(value: float, dist=None, device=None) -> float:
@@ -163,19 +244,21 @@ def measured_peaks() -> dict:
 # primitive tested per ray.
 FLOPS = {"mode_eval": 18, "sample_eval": 24, "lm_term": 170, "icp_term": 110, "ray_prim": 25}
 
+# SURVEY.md §8(d) generation model: Kabsch + checks ~600 flop per attempt (FP32 pipe).
+SURVEY_FLOP_PER_ATTEMPT = 600
 
 # ALU-op model of one hypothesis-generation attempt, 32-bit lane ops:
 # 7 xoshiro256** outputs at ~21 ops each + 7 exact 64-bit Barrett reductions with rejection
 # test at ~23 ops each, 3 mode lookups from the pixel record (~14 each), the colour check
-# (~12) and the 6 record addresses (~12). K4 is issue-bound (integer ALU), not FP or HBM.
+# (~12) and the 6 record addresses (~12) = 374. K4 is issue-bound (integer ALU), not FP or HBM.
 GEN_OPS_PER_ATTEMPT = 7 * 21 + 7 * 23 + 3 * 14 + 12 + 12
 
 
 def kernel_model(name: str, work: dict) -> tuple | None:
-    """(algorithmic work, bound, unit scale) of a kernel from the device work counters."""
+    """(algorithmic work, bound) of a kernel from the device work counters."""
     if name == "k_hypgen":
         return GEN_OPS_PER_ATTEMPT * work["gen_attempts"], "alu"
-    f = kernel_flops(name, work, 0)
+    f = kernel_flops(name, work)
     return (f, "fp32") if f is not None else None
 
 
@@ -188,7 +271,7 @@ def ncu_traffic() -> dict:
         return json.load(f).get("kernels", {})
 
 
-def kernel_flops(name: str, work: dict, n_prims: int) -> float | None:
+def kernel_flops(name: str, work: dict) -> float | None:
     if name == "k_energy":
         return FLOPS["mode_eval"] * work["mode_evals"] + FLOPS["sample_eval"] * work["sample_evals"]
     if name == "k_icp_score":
@@ -206,8 +289,73 @@ def success(pose_R, pose_t, gt) -> tuple:
     return te <= 0.05 and ae <= 5.0, te, ae
 
 
+def intrinsics_of(res):
+    w, h = res
+    s = w / 640.0  # Kinect-like 585 px at 640x480; stress 1170 px at 1280x960
+    return w, h, 585.0 * s, 585.0 * s, w / 2.0, h / 2.0
+
+
 # ------------------------------------------------------------------ our arm (B200)
-def run_ours(args):
+class SceneRun:
+    """One scene on this rank: forest + adapted state + model + resident test frames."""
+
+    def __init__(self, P, dev, wl: Workload, seed: int, args, rank, world, dist, dev_t, k):
+        import torch
+
+        self.seed = seed
+        self.k = k
+        fp = P.forest_params(dict(wl.forest))
+        self.scene = P.Scene(dev, P.generate_random_forest(FOREST_SEED, 14, 0.4, 5, 130), fp, k,
+                             adapt_seed=ADAPT_SEED, max_batch=args.batch)
+        self.prims = P.generate_synthetic_scene(seed, 20)
+        self.scene.set_model(self.prims)
+        t0 = time.perf_counter()
+        self.adapt_poses = P.generate_trajectory(seed, args.adapt_frames, 0)
+        self.bcast_ms = None
+        replicated = wl.scenes == 1 and dist is not None  # one scene, frames sharded: rank 0 adapts
+        if rank == 0 or not replicated:
+            fs_a = P.FrameSet(self.scene, min(args.adapt_frames, 250 if k.width <= 640 else 64))
+            for c0 in range(0, args.adapt_frames, fs_a.capacity):
+                c1 = min(args.adapt_frames, c0 + fs_a.capacity)
+                fs_a.render(self.adapt_poses[c0:c1])
+                fs_a.train(range(c1 - c0), self.adapt_poses[c0:c1])
+            fs_a.close()
+            self.scene.update_leaves_round_robin(self.scene.total_leaves)
+        torch.cuda.synchronize()
+        self.adapt_s = time.perf_counter() - t0
+        if replicated:
+            nbytes = self.scene.lib.scr_predictions_bytes(self.scene.handle)
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=dev_t)
+            if rank == 0:
+                P.native.check(self.scene.lib.scr_predictions_export(self.scene.handle, buf.data_ptr()), "export")
+            torch.cuda.synchronize()
+            dist.barrier()
+            tb = time.perf_counter()
+            dist.broadcast(buf, src=0)
+            torch.cuda.synchronize()
+            self.bcast_ms = (time.perf_counter() - tb) * 1e3
+            if rank != 0:
+                P.native.check(self.scene.lib.scr_predictions_import(self.scene.handle, buf.data_ptr()), "import")
+            del buf
+        # test frames resident in HBM (> L2: batch x 2.15 MB per step, rotating)
+        if replicated:
+            n_total = args.test_frames * world
+            allp = P.generate_trajectory(seed, n_total, args.test_kind)
+            self.ids = shard(n_total, rank, world)
+        else:
+            allp = P.generate_trajectory(seed, args.test_frames, args.test_kind)
+            self.ids = list(range(args.test_frames))
+        self.poses = [allp[i] for i in self.ids]
+        self.fs = P.FrameSet(self.scene, len(self.poses))
+        self.fs.render(self.poses)
+        self.seeds = [frame_seed(RUN_SEED + 1000 * (seed - 1), i) for i in self.ids]
+
+    def close(self):
+        self.fs.close()
+        self.scene.close()
+
+
+def run_ours(args, wl: Workload):
     import torch
 
     import paper_1810_12163_b200 as P
@@ -217,83 +365,60 @@ def run_ours(args):
     # Test hook for the N>1 path on a single GPU (tests/test_gpu_bench_ranks.py): every rank on
     # device 0 and gloo for the host-side barrier/broadcast/reductions. The ranks' kernels never
     # wait on each other (no per-frame collective), so this only exercises the plumbing.
-    if os.environ.get("SCR_BENCH_ONE_GPU") == "1":
+    one_gpu = os.environ.get("SCR_BENCH_ONE_GPU") == "1"
+    if one_gpu:
         local = 0
+    elif world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
-        dist = dist_init(os.environ.get("SCR_BENCH_BACKEND", "nccl"))
+        backend = os.environ.get("SCR_BENCH_BACKEND", "nccl")
+        dist = dist_init(backend)
+        comm = {"backend": backend, "nranks": dist.get_world_size()}
+        print(f"[rank {rank}] process group {backend}: nranks {dist.get_world_size()} rank {dist.get_rank()} "
+              f"device cuda:{local}", file=sys.stderr, flush=True)
     dev_t = torch.device("cuda", local)
 
     dev = P.Device(local)
-    k = P.intrinsics()
-    blob = P.generate_random_forest(FOREST_SEED, 14, 0.4, 5, 130)
-    fparams = P.forest_params("cascade")
-    scene = P.Scene(dev, blob, fparams, k, adapt_seed=ADAPT_SEED, max_batch=args.batch)
-    prims = P.generate_synthetic_scene(SCENE_SEED, 20)
-    scene.set_model(prims)
-    cfg = P.CascadeConfig.paper_three_stage()
+    k = P.intrinsics(*intrinsics_of(wl.res))
+    stages = [P.ransac_params(p, n_max=P.PROFILES[p]["n_max"] * wl.nmax_scale) for p, _ in wl.stages]
+    cfg = P.CascadeConfig(stages, [m for _, m in wl.stages], list(wl.thresholds))
 
-    # ---- adaptation (untimed setup): rank 0 adapts, the table is broadcast over NCCL
-    t0 = time.perf_counter()
-    adapt_poses = P.generate_trajectory(SCENE_SEED, args.adapt_frames, 0)
-    bcast_ms = None
-    if rank == 0 or dist is None:
-        fs_a = P.FrameSet(scene, min(args.adapt_frames, 250))
-        for c0 in range(0, args.adapt_frames, fs_a.capacity):
-            c1 = min(args.adapt_frames, c0 + fs_a.capacity)
-            fs_a.render(adapt_poses[c0:c1])
-            fs_a.train(range(c1 - c0), adapt_poses[c0:c1])
-        fs_a.close()
-        scene.update_leaves_round_robin(scene.total_leaves)
-    torch.cuda.synchronize()
-    adapt_s = time.perf_counter() - t0
-    if dist is not None:
-        nbytes = scene.lib.scr_predictions_bytes(scene.handle)
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev_t)
-        if rank == 0:
-            P.native.check(scene.lib.scr_predictions_export(scene.handle, buf.data_ptr()), "export")
-        torch.cuda.synchronize()
-        tb = time.perf_counter()
-        dist.broadcast(buf, src=0)
-        torch.cuda.synchronize()
-        bcast_ms = (time.perf_counter() - tb) * 1e3
-        if rank != 0:
-            P.native.check(scene.lib.scr_predictions_import(scene.handle, buf.data_ptr()), "import")
-        del buf
-
-    # ---- test frames resident in HBM (> L2: batch * 2.15 MB per step, rotating)
-    n_total = args.test_frames * world
-    test_poses_all = P.generate_trajectory(SCENE_SEED, n_total, args.test_kind)
-    mine = shard(n_total, rank, world)
-    poses = [test_poses_all[i] for i in mine]
-    fs = P.FrameSet(scene, len(poses))
-    fs.render(poses)
-    seeds_all = [frame_seed(RUN_SEED, i) for i in mine]
+    my_scenes = scenes_of_rank(wl.scenes, rank, world) if wl.scenes > 1 else [SCENE_SEED]
+    runs = [SceneRun(P, dev, wl, s, args, rank, world, dist, dev_t, k) for s in my_scenes]
     B = args.batch
 
-    def batch_at(sub):
-        """Sub-batch `sub` (B frames); step st is sub-batches st*L .. st*L + L-1, one per lane."""
-        i0 = (sub * B) % len(poses)
-        idx = [(i0 + j) % len(poses) for j in range(B)]
-        return idx, [seeds_all[i] for i in idx]
-
-    stream = torch.cuda.ExternalStream(scene.stream, device=dev_t)
-    # relocalisation lanes: each host thread drives its own stream + workspace on the shared
+    # relocalisation lanes: each host thread drives its own stream + workspace on a shared
     # scene, so one lane's host work and fallback-stage tail overlap another lane's kernels
-    lanes = [scene] + [scene.fork(B) for _ in range(max(1, args.lanes) - 1)]
-    lane_streams = [torch.cuda.ExternalStream(l.stream, device=dev_t) for l in lanes]
-    clk = ClockSampler(local).__enter__()  # nvidia-smi needs ~1 s to start: launch it before warm-up
+    per_scene = max(1, -(-max(1, args.lanes) // len(runs)))
+    lanes = []  # (run, lane scene)
+    for r in runs:
+        lanes.append((r, r.scene))
+        for _ in range(per_scene - 1):
+            lanes.append((r, r.scene.fork(B)))
+    lane_streams = [torch.cuda.ExternalStream(l.stream, device=dev_t) for _, l in lanes]
     L = len(lanes)
+    lane_no = {li: sum(1 for j in range(li) if lanes[j][0] is lanes[li][0]) for li in range(L)}
+
+    def batch_at(li, sub):
+        """Batch `sub` of lane li: consecutive B-frame windows of the lane's scene, the lanes
+        of one scene interleaved."""
+        r = lanes[li][0]
+        i0 = ((sub * per_scene + lane_no[li]) * B) % len(r.poses)
+        idx = [(i0 + j) % len(r.poses) for j in range(B)]
+        return idx, [r.seeds[i] for i in idx]
+
+    clk = ClockSampler(local).__enter__()  # nvidia-smi needs ~1 s to start: launch it before warm-up
     for w in range(args.warmup):
-        for li, lane in enumerate(lanes):
-            idx, sd = batch_at(w * L + li)
-            fs.cascade(idx, cfg, sd, scene=lane)
+        for li, (r, lane) in enumerate(lanes):
+            idx, sd = batch_at(li, w)
+            r.fs.cascade(idx, cfg, sd, scene=lane)
     torch.cuda.synchronize()
 
     def run_lanes(step_fn, steps):
-        """Runs steps 0..steps-1, each split over the lanes (one host thread per lane: lane li
-        runs its sub-batch of every step), and returns the device time from a common start
-        event to the last lane's end event."""
+        """Runs steps 0..steps-1 on every lane (one host thread per lane) and returns the device
+        time from a common start event to the last lane's end event."""
         torch.cuda.synchronize()
         start = torch.cuda.Event(enable_timing=True)
         ends = [torch.cuda.Event(enable_timing=True) for _ in lanes]
@@ -303,11 +428,11 @@ def run_ours(args):
         def work(li):
             try:
                 for st in range(steps):
-                    step_fn(lanes[li], li, st)
+                    step_fn(li, st)
             except Exception as e:  # surfaced after join
                 errs.append(e)
 
-        ths = [threading.Thread(target=work, args=(li,)) for li in range(len(lanes))]
+        ths = [threading.Thread(target=work, args=(li,)) for li in range(L)]
         for t in ths:
             t.start()
         for t in ths:
@@ -320,17 +445,17 @@ def run_ours(args):
         return max(start.elapsed_time(e) for e in ends)
 
     # ---- timed region: device-resident inputs (no per-kernel instrumentation)
-    results = [None] * (args.steps * L)
-    launches0 = sum(l.kernel_launches for l in lanes)
+    results = {}
+    launches0 = sum(l.kernel_launches for _, l in lanes)
     if dist is not None:
         dist.barrier()
     if args.profile_window:
         torch.cuda.cudart().cudaProfilerStart()
 
-    def timed_step(lane, li, st):
-        sub = st * L + li
-        idx, sd = batch_at(args.warmup * L + sub)
-        results[sub] = (idx, fs.cascade(idx, cfg, sd, scene=lane))
+    def timed_step(li, st):
+        r, lane = lanes[li]
+        idx, sd = batch_at(li, args.warmup + st)
+        results[(li, st)] = (r, idx, r.fs.cascade(idx, cfg, sd, scene=lane))
 
     tw0 = time.time()
     elapsed_ms = run_lanes(timed_step, args.steps)
@@ -341,72 +466,88 @@ def run_ours(args):
         dist.barrier()
     clk.mark(tw0, tw1)
     clk.__exit__(None, None, None)
-    launches = sum(l.kernel_launches for l in lanes) - launches0
+    launches = sum(l.kernel_launches for _, l in lanes) - launches0
     elapsed_max = max_over_ranks(elapsed_ms, dist, dev_t)
     frames_done = sum_over_ranks(float(args.steps * B * L), dist, dev_t)
     value = frames_done / (elapsed_max / 1e3)
 
-    # ---- second timed pass, same batches, with CUDA events around every launch (roofline)
-    scene.profile(True)
+    # ---- second pass, the first scene's batches on its root stream, with CUDA events around
+    # every launch (per-kernel ms for the roofline and the kernel shares)
+    r0 = runs[0]
+    r0.scene.profile(True)
+    stream = torch.cuda.ExternalStream(r0.scene.stream, device=dev_t)
     torch.cuda.synchronize()
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(stream)
-    for sub in range(args.steps * L):
-        idx, sd = batch_at(args.warmup * L + sub)
-        fs.cascade(idx, cfg, sd)
+    prof_batches = 0
+    for st in range(args.steps):
+        for li in range(L):
+            if lanes[li][0] is r0:
+                idx, sd = batch_at(li, args.warmup + st)
+                r0.fs.cascade(idx, cfg, sd)
+                prof_batches += 1
     p1.record(stream)
     torch.cuda.synchronize()
     prof_ms = p0.elapsed_time(p1)
-    prof = scene.profile_read()
-    scene.profile(False)
+    prof = r0.scene.profile_read()
+    r0.scene.profile(False)
+
+    # ---- accuracy: 5 cm / 5 deg, stage mix and per-novelty-bin success
+    from paper_1810_12163_b200.protocols import novelty_bin_keys
 
     ok = 0
     stage_hist = [0, 0, 0]
     stage_ms = [0.0, 0.0, 0.0]
-    from paper_1810_12163_b200.protocols import novelty_bin_keys
-
-    bin_of = dict(zip(range(len(poses)), novelty_bin_keys(poses, adapt_poses)))
-    per_bin = {}
-    for idx, res in results:
-        for i, r in zip(idx, res):
-            stage_hist[min(r.stage_used, 2)] += 1
+    bin_of = {id(r): novelty_bin_keys(r.poses, r.adapt_poses) for r in runs}
+    per_bin, per_scene_ok = {}, {}
+    for (li, st), (r, idx, res) in results.items():
+        for i, x in zip(idx, res):
+            stage_hist[min(x.stage_used, 2)] += 1
             for j in range(3):
-                stage_ms[j] += float(r.stage_ms[j])
+                stage_ms[j] += float(x.stage_ms[j])
             good = False
-            if r.has_pose:
-                R, t = P.pose_arrays(r.pose)
-                good = success(R, t, poses[i])[0]
+            if x.has_pose:
+                R, t = P.pose_arrays(x.pose)
+                good = success(R, t, r.poses[i])[0]
                 ok += good
-            b = per_bin.setdefault(int(bin_of[i]), [0, 0, [0, 0, 0]])
+            b = per_bin.setdefault(int(bin_of[id(r)][i]), [0, 0, [0, 0, 0]])
             b[0] += 1
             b[1] += good
-            b[2][min(r.stage_used, 2)] += 1
-    n_res = sum(len(r) for _, r in results)
+            b[2][min(x.stage_used, 2)] += 1
+            sc = per_scene_ok.setdefault(r.seed, [0, 0])
+            sc[0] += 1
+            sc[1] += good
+    n_res = sum(len(v[2]) for v in results.values())
     succ = sum_over_ranks(float(ok), dist, dev_t) / max(1.0, sum_over_ranks(float(n_res), dist, dev_t))
-    novelty = {f"<={k}cm/deg" if k <= 55 else ">55cm/deg": {"frames": v[0], "success": round(v[1] / v[0], 4),
-                                                            "stage_mix": v[2]}
-               for k, v in sorted(per_bin.items())}
+    novelty = {(f"<={kk}cm/deg" if kk <= 55 else ">55cm/deg"): {"frames": v[0], "success": round(v[1] / v[0], 4),
+                                                                "stage_mix": v[2]}
+               for kk, v in sorted(per_bin.items())}
 
     # ---- e2e: pinned host frames through the C ABI (H2D + result D2H inside)
-    nb = min(len(poses), max(B, 1))
-    hd, hc = fs.download(0, nb)
-    pin_d = torch.empty(hd.shape, dtype=torch.float32, pin_memory=True)
-    pin_c = torch.empty(hc.shape, dtype=torch.uint8, pin_memory=True)
-    pin_d.numpy()[...] = hd
-    pin_c.numpy()[...] = hc
-    dnp, cnp = pin_d.numpy(), pin_c.numpy()
-    e2e_idx = [j % nb for j in range(B)]
-    e2e_seeds = [seeds_all[j] for j in e2e_idx]
-    for lane in lanes:
-        lane.run_cascade_batch([dnp[j] for j in e2e_idx], [cnp[j] for j in e2e_idx], cfg, e2e_seeds)
+    pins = {}
+    for r in runs:
+        nb = min(len(r.poses), max(B, 1))
+        hd, hc = r.fs.download(0, nb)
+        pin_d = torch.empty(hd.shape, dtype=torch.float32, pin_memory=True)
+        pin_c = torch.empty(hc.shape, dtype=torch.uint8, pin_memory=True)
+        pin_d.numpy()[...] = hd
+        pin_c.numpy()[...] = hc
+        e2e_idx = [j % nb for j in range(B)]
+        pins[id(r)] = (pin_d, pin_c, [pin_d.numpy()[j] for j in e2e_idx], [pin_c.numpy()[j] for j in e2e_idx],
+                       [r.seeds[j] for j in e2e_idx])
+
+    def e2e_step(li, st):
+        r, lane = lanes[li]
+        _, _, dl, cl, sd = pins[id(r)]
+        lane.run_cascade_batch(dl, cl, cfg, sd)
+
+    for li in range(L):
+        e2e_step(li, 0)
     if dist is not None:
         dist.barrier()
-    e2e_steps = args.steps
-    e2e_ms = max_over_ranks(
-        run_lanes(lambda lane, li, st: lane.run_cascade_batch([dnp[j] for j in e2e_idx], [cnp[j] for j in e2e_idx], cfg,
-                                                          e2e_seeds), e2e_steps), dist, dev_t)
-    e2e_value = sum_over_ranks(float(e2e_steps * B * L), dist, dev_t) / (e2e_ms / 1e3)
+    e2e_ms = max_over_ranks(run_lanes(e2e_step, args.steps), dist, dev_t)
+    e2e_value = sum_over_ranks(float(args.steps * B * L), dist, dev_t) / (e2e_ms / 1e3)
     h2d = B * L * (k.width * k.height * 4 + k.width * k.height * 3)
     d2h = B * L * 136
 
@@ -415,47 +556,58 @@ def run_ours(args):
     kern = prof["kernels"]
     dom = max(kern, key=lambda n: kern[n]["ms"])
     clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    peak_of = {"fp32": (148 * 128 * 2 * clk_mhz * 1e6 / 1e12, "TFLOP/s",
+    fp32_peak = 148 * 128 * 2 * clk_mhz * 1e6 / 1e12
+    peak_of = {"fp32": (fp32_peak, "TFLOP/s",
                         "nominal FP32 FMA pipe: 148 SM x 128 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS.json)"),
                "alu": (148 * 128 * clk_mhz * 1e6 / 1e12, "Tops/s",
                        "nominal 32-bit ALU issue: 148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)")}
     traffic = ncu_traffic()
 
     def roof(name):
-        k = kern[name]
+        kk = kern[name]
         m = kernel_model(name, prof["work"])
-        tk = traffic.get(name) or next((v for kk, v in traffic.items() if kk.startswith(name + "<")), {})
-        r = {"kernel": name, "kernel_ms": round(k["ms"], 3), "launches": k["launches"],
+        tk = traffic.get(name) or next((v for kx, v in traffic.items() if kx.startswith(name + "<")), {})
+        r = {"kernel": name, "kernel_ms": round(kk["ms"], 3), "launches": kk["launches"],
              "traffic": tk.get("dram_bytes_per_launch")}
-        if m is None or k["ms"] <= 0:
+        if m is None or kk["ms"] <= 0:
             r.update({"bound": None, "achieved": None, "peak": None, "unit": None, "frac": None})
             return r
         work_units, bound = m
         pk, unit, src = peak_of[bound]
-        ach = work_units / (k["ms"] / 1e3) / 1e12
+        ach = work_units / (kk["ms"] / 1e3) / 1e12
         r.update({"bound": bound, "achieved": round(ach, 3), "peak": round(pk, 2), "unit": unit,
                   "frac": round(ach / pk, 4), "peak_source": src,
-                  "work_per_launch": work_units / max(1, k["launches"])})
+                  "work_per_launch": work_units / max(1, kk["launches"])})
+        if name == "k_hypgen":  # the SURVEY.md §8(d) model: 600 flop per attempt on the FP32 pipe
+            sv = SURVEY_FLOP_PER_ATTEMPT * prof["work"]["gen_attempts"] / (kk["ms"] / 1e3) / 1e12
+            r["survey_model"] = {"achieved": round(sv, 3), "peak": round(fp32_peak, 2), "unit": "TFLOP/s",
+                                 "frac": round(sv / fp32_peak, 4), "flop_per_attempt": SURVEY_FLOP_PER_ATTEMPT}
         if r["traffic"] is not None:
             r["traffic_source"] = "profiles/ncu_kernels.json (ncu --set full, dram__bytes_read+write per launch)"
         return r
 
     roofline = roof(dom)
-    rooflines = {n: roof(n) for n in sorted(kern, key=lambda n: -kern[n]["ms"])[:5]
+    rooflines = {n: roof(n) for n in sorted(kern, key=lambda n: -kern[n]["ms"])[:6]
                  if n != dom and kernel_model(n, prof["work"]) is not None}
-    share = {n: round(v["ms"] / max(1e-9, sum(x["ms"] for x in kern.values())), 4) for n, v in kern.items() if v["ms"] > 0}
+    tot_ms = sum(x["ms"] for x in kern.values())
+    share = {n: round(v["ms"] / max(1e-9, tot_ms), 4) for n, v in kern.items() if v["ms"] > 0}
 
+    per_gpu = value / max(1, world)
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(elapsed_max / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (geometry f64)", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "frames_per_step_per_gpu": B * L, "frames_per_lane_batch": B,
-                   "test_frames_per_gpu": len(poses),
-                   "adapt_frames": args.adapt_frames, "resolution": "640x480", "forest": "random h14 p0.4 x5",
-                   "forest_params": "kappa 2048, tau 0.2, min 5", "scene_seed": SCENE_SEED,
-                   "l2": "inputs larger than L2 (test frames rotate through %.0f MB of HBM)" % (
-                       len(poses) * 2.15), "parallelism": f"replicas x{world} (frames sharded)",
-                   "lanes_per_gpu": len(lanes)},
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32 (geometry f64)", "data": "synthetic",
+        "config": {"workload": wl.desc, "workload_key": wl.name, "frames_per_step_per_gpu": B * L,
+                   "frames_per_lane_batch": B, "test_frames_per_scene": len(runs[0].poses),
+                   "scenes_on_rank0": [r.seed for r in runs], "adapt_frames": args.adapt_frames,
+                   "resolution": f"{wl.res[0]}x{wl.res[1]}", "forest": "random h14 p0.4 x5",
+                   "forest_params": wl.forest, "stages": [f"{p}/{['raw', 'icp', 'ranked'][m]}" for p, m in wl.stages],
+                   "n_max_scale": wl.nmax_scale, "test_poses": "novel (kind 2)" if args.test_kind == 2 else "near-loop",
+                   "l2": "inputs larger than L2 (test frames rotate through %.0f MB of HBM per scene)" % (
+                       len(runs[0].poses) * wl.res[0] * wl.res[1] * 7 / 1e6),
+                   "parallelism": (f"replicas x{world} (frames sharded)" if wl.scenes == 1 else
+                                   f"{wl.scenes} scenes sharded over {world} ranks"),
+                   "lanes_per_gpu": L},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(sum_over_ranks(float(launches), dist, dev_t)),
         "roofline": roofline,
@@ -463,84 +615,186 @@ def run_ours(args):
         "clocks": clk.summary(),
         "accuracy": {"success_5cm_5deg": round(succ, 4), "frames": n_res, "stage_mix": stage_hist,
                      "stage_share": [round(x / max(1, n_res), 4) for x in stage_hist],
-                     "per_novelty_bin": novelty},
-        "stage_ms_per_step": [round(x / args.steps / L, 3) for x in stage_ms],
+                     "per_novelty_bin": novelty,
+                     "per_scene": {s: round(v[1] / v[0], 4) for s, v in sorted(per_scene_ok.items())}},
+        "stage_ms_per_step": [round(x / args.steps, 3) for x in stage_ms],
         "kernel_share": share,
-        "instrumented_pass_ms_per_step": round(prof_ms / args.steps, 3),
+        "instrumented_pass": {"ms_per_batch": round(prof_ms / max(1, prof_batches), 3), "batches": prof_batches},
         "work": prof["work"],
-        "adapt": {"frames": args.adapt_frames, "seconds": round(adapt_s, 2), "broadcast_ms": bcast_ms},
+        "adapt": {"frames": args.adapt_frames, "seconds": round(runs[0].adapt_s, 2),
+                  "broadcast_ms": runs[0].bcast_ms},
     }
+    if comm:
+        out["comm"] = comm
+    if wl.paper_ms:
+        out["paper"] = {"ms_per_frame": wl.paper_ms, "frames_per_s": round(1e3 / wl.paper_ms, 2),
+                        "ref": wl.paper_ref, "hardware": "GTX 1080Ti / Titan X (paper)",
+                        "b200_per_gpu_speedup": round(per_gpu * wl.paper_ms / 1e3, 1)}
     if rank == 0 and world == 1 and not args.no_cpu:
-        out["cpu_baseline"], out["parity"] = cpu_baseline(scene, fs, poses, seeds_all, prims, results, args)
+        res0 = [(idx, res) for (li, st), (r, idx, res) in sorted(results.items(), key=lambda x: x[0]) if r is r0]
+        out["cpu_baseline"], out["parity"] = cpu_baseline(wl, r0, res0, args)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    fs.close()
-    scene.close()
+    for r in runs:
+        r.close()
     if dist is not None:
         dist.destroy_process_group()
 
 
-def _oracle_world(prims, adapt_frames, threads, gpu_scene=None):
+def run_adapt(args, wl: Workload):
+    """Per-frame training as the paper times it: after the 1000-frame
+    adaptation has filled the reservoirs, every step integrates one new frame and refreshes
+    256 leaves (update_leaves_round_robin). Frames are resident; poses continue the loop."""
+    import torch
+
+    import paper_1810_12163_b200 as P
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    dev_t = torch.device("cuda", local)
+    dev = P.Device(local)
+    k = P.intrinsics(*intrinsics_of(wl.res))
+    scene = P.Scene(dev, P.generate_random_forest(FOREST_SEED, 14, 0.4, 5, 130), P.forest_params(dict(wl.forest)), k,
+                    adapt_seed=ADAPT_SEED, max_batch=64)
+    scene.set_model(P.generate_synthetic_scene(SCENE_SEED, 20))
+    n_pre = args.adapt_frames
+    total = n_pre + args.warmup + args.steps
+    poses = P.generate_trajectory(SCENE_SEED + 100 * rank, total, 0)
+    fs = P.FrameSet(scene, 250)
+    for c0 in range(0, n_pre, 250):
+        c1 = min(n_pre, c0 + 250)
+        fs.render(poses[c0:c1])
+        fs.train(range(c1 - c0), poses[c0:c1])
+    scene.update_leaves_round_robin(scene.total_leaves)
+    n_run = args.warmup + args.steps
+    fs_t = P.FrameSet(scene, n_run)
+    fs_t.render(poses[n_pre:total])
+    stream = torch.cuda.ExternalStream(scene.stream, device=dev_t)
+    for w in range(args.warmup):
+        fs_t.train([w], [poses[n_pre + w]])
+        scene.update_leaves_round_robin(256)
+    clk = ClockSampler(local).__enter__()
+    time.sleep(1.0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = scene.kernel_launches
+    tw0 = time.time()
+    e0.record(stream)
+    for s in range(args.steps):
+        i = args.warmup + s
+        fs_t.train([i], [poses[n_pre + i]])
+        scene.update_leaves_round_robin(256)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    clk.mark(tw0, tw1)
+    clk.__exit__(None, None, None)
+    ms = e0.elapsed_time(e1)
+    launches = scene.kernel_launches - launches0
+    scene.profile(True)
+    for s in range(args.steps):
+        i = args.warmup + s
+        fs_t.train([i], [poses[n_pre + i]])
+        scene.update_leaves_round_robin(256)
+    torch.cuda.synchronize()
+    prof = scene.profile_read()
+    scene.profile(False)
+    kern = prof["kernels"]
+    tot = sum(v["ms"] for v in kern.values())
+    out = {"metric": "adapted frames/s (integrate + update(256) per frame)", "value": round(args.steps / (ms / 1e3), 2),
+           "unit": "frames/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32 (positions f64)", "data": "synthetic",
+           "config": {"workload": wl.desc, "workload_key": wl.name, "prefill_frames": n_pre,
+                      "forest_params": wl.forest, "resolution": f"{wl.res[0]}x{wl.res[1]}"},
+           "gpu_launches": launches, "clocks": clk.summary(),
+           "kernel_ms_per_frame": {n: round(v["ms"] / args.steps, 4)
+                                   for n, v in sorted(kern.items(), key=lambda x: -x[1]["ms"])},
+           "kernel_share": {n: round(v["ms"] / max(1e-9, tot), 4) for n, v in kern.items()},
+           "paper": {"ms_per_frame": wl.paper_ms, "ref": wl.paper_ref, "hardware": "GTX 1080Ti / Titan X (paper)"}}
+    print(json.dumps(out), flush=True)
+    fs_t.close()
+    fs.close()
+    scene.close()
+
+
+# ------------------------------------------------------------------ CPU oracle (checker only)
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle_ffi as of
 
-    O = of.get()
+    return of.get(), of
+
+
+def _oracle_world(wl: Workload, scene_seed: int, adapt_frames: int, threads: int):
+    """The oracle adapts its own state on the same seeded sequence (no GPU data)."""
+    import ctypes as C
+
+    O, of = _oracle()
     forest = O.lib.or_forest_random(FOREST_SEED, 14, 0.4, 5, 130)
-    state = O.state_create(forest, of.FOREST_CASCADE, ADAPT_SEED)
-    pr = np.ascontiguousarray(prims)
-    scene = O.lib.or_scene_from_prims(pr.ctypes.data, pr.size)
+    state = O.state_create(forest, dict(wl.forest), ADAPT_SEED)
+    scene = O.lib.or_scene_generate(scene_seed, 20)
     total = O.lib.or_forest_total_leaves(forest)
-    if gpu_scene is not None:  # the adapted table (bit-exact with the oracle's, see tests) -> oracle
-        cnt, modes = gpu_scene.predictions()
-        O.load_predictions(state, cnt, modes.view(of.MODE_DTYPE))
-    else:
-        k = of.intrinsics()
-        poses = O.trajectory(SCENE_SEED, adapt_frames, 0)
-        import ctypes as C
-
-        for c0 in range(0, adapt_frames, 100):
-            chunk = poses[c0:c0 + 100]
-            D, RGB = O.render(scene, chunk, k, threads)
-            arr = (of.Pose * len(chunk))(*chunk)
-            rc = O.lib.or_integrate_batch(state, forest, of._ptr(D, C.c_float), of._ptr(RGB, C.c_uint8),
-                                          C.byref(k), arr, len(chunk), threads)
-            assert rc == 0, O.err()
-        O.lib.or_update_all_parallel(state, threads)
-    return O, of, forest, state, scene, total
+    k = of.intrinsics(*intrinsics_of(wl.res))
+    poses = O.trajectory(scene_seed, adapt_frames, 0)
+    chunk = 100 if wl.res[0] <= 640 else 25
+    for c0 in range(0, adapt_frames, chunk):
+        part = poses[c0:c0 + chunk]
+        D, RGB = O.render(scene, part, k, threads)
+        arr = (of.Pose * len(part))(*part)
+        rc = O.lib.or_integrate_batch(state, forest, of._ptr(D, C.c_float), of._ptr(RGB, C.c_uint8),
+                                      C.byref(k), arr, len(part), threads)
+        assert rc == 0, O.err()
+    O.lib.or_update_all_parallel(state, threads)
+    return O, of, forest, state, scene, total, k
 
 
-def cpu_baseline(gscene, fs, poses, seeds, prims, gpu_results, args):
-    """Oracle (CPU restatement) on a bounded sample of the same frames, all host threads."""
+def _oracle_stages(of, wl: Workload):
+    return [of.ransac_params(p, n_max=of.PROFILES[p]["n_max"] * wl.nmax_scale) for p, _ in wl.stages]
+
+
+def cpu_baseline(wl: Workload, r0, gpu_results, args):
+    """Oracle (CPU restatement) on a bounded sample of the same frames, all host threads;
+    the oracle adapts on its own, and its adapted table is compared with the GPU's."""
     threads = os.cpu_count() or 1
-    O, of, forest, state, scene, _ = _oracle_world(prims, args.adapt_frames, threads, gpu_scene=gscene)
+    t0 = time.perf_counter()
+    O, of, forest, state, scene, total, k = _oracle_world(wl, r0.seed, args.adapt_frames, threads)
+    adapt_s = time.perf_counter() - t0
+    cnt_o, modes_o = O.predictions(state, total)
+    cnt_g, modes_g = r0.scene.predictions()
+    valid = (np.arange(50)[None, :] < cnt_o[:, None]).reshape(-1)
+    table_equal = bool(np.array_equal(cnt_o, cnt_g) and
+                       np.array_equal(modes_o.view(np.uint8).reshape(-1, 100)[valid],
+                                      modes_g.view(np.uint8).reshape(-1, 100)[valid]))
+    del modes_o, modes_g
     gpu_by_frame = {}
     for idx, res in gpu_results:
         for i, r in zip(idx, res):
             gpu_by_frame.setdefault(i, r)
     sample = sorted(gpu_by_frame)[:256]
-    D, RGB = fs.download(0, max(sample) + 1)
-    st = [of.ransac_params(p) for p in ("fast", "intermediate", "slow")]
-    done, t0, ok, exact, n = [], time.perf_counter(), 0, 0, 0
+    D, RGB = r0.fs.download(0, max(sample) + 1)
+    st = _oracle_stages(of, wl)
+    modes = [m for _, m in wl.stages]
+    done, ok, exact, n = [], 0, 0, 0
     max_te = max_ae = 0.0
-    chunk = threads
+    t0 = time.perf_counter()
     while True:
-        part = [sample[(len(done) + j) % len(sample)] for j in range(chunk)]
-        res = O.cascade_batch(forest, state, scene, D[part], RGB[part], of.intrinsics(), st,
-                              list(of.CASCADE_MODES), list(of.CASCADE_THRESHOLDS), [seeds[i] for i in part],
-                              threads=threads)
+        part = [sample[(len(done) + j) % len(sample)] for j in range(threads)]
+        res = O.cascade_batch(forest, state, scene, D[part], RGB[part], k, st, modes, list(wl.thresholds),
+                              [r0.seeds[i] for i in part], threads=threads)
         for i, r in zip(part, res):
             n += 1
             g = gpu_by_frame[i]
             if r.has_pose:
                 R, t = of.pose_np(r.pose)
-                ok += success(R, t, poses[i])[0]
+                ok += success(R, t, r0.poses[i])[0]
             if r.has_pose and g.has_pose:
-                exact += bytes(r.pose) == bytes(g.pose)
+                exact += bytes(r.pose) == bytes(g.pose) and r.stage_used == g.stage_used
                 Rg_, tg_ = np.array(g.pose.R[:]).reshape(3, 3), np.array(g.pose.t[:])
                 max_te = max(max_te, float(np.linalg.norm(t - tg_)))
                 max_ae = max(max_ae, float(np.degrees(np.arccos(np.clip((np.trace(Rg_.T @ R) - 1) / 2, -1, 1)))))
             elif r.has_pose == g.has_pose:
-                exact += 1
+                exact += r.stage_used == g.stage_used
         done.extend(part)
         el = time.perf_counter() - t0
         if el > args.cpu_seconds or len(done) >= len(sample):
@@ -550,48 +804,49 @@ def cpu_baseline(gscene, fs, poses, seeds, prims, gpu_results, args):
         g = gpu_by_frame[i]
         if g.has_pose:
             R, t = of.pose_np(g.pose)
-            gpu_ok += success(R, t, poses[i])[0]
+            gpu_ok += success(R, t, r0.poses[i])[0]
     base = {"value": round(len(done) / el, 3), "unit": UNIT, "cores": threads, "kind": "port",
+            "success_5cm_5deg": round(ok / max(1, n), 4),
             "gpu_success_same_frames": round(gpu_ok / max(1, len(done)), 4),
-            "sample": f"{len(done)} test frames ({len(set(done))} distinct) through the same cascade, "
-                      f"oracle/ C++ restatement, {threads} threads, {el:.1f} s",
-            "success_5cm_5deg": round(ok / max(1, n), 4)}
-    parity = {"frames_compared": n, "bit_exact_results": exact, "max_t_diff_m": max_te, "max_rot_diff_deg": max_ae}
+            "sample": f"{len(done)} test frames ({len(set(done))} distinct) of scene {r0.seed} through the same "
+                      f"stages, oracle/ C++ restatement, {threads} threads, {el:.1f} s"}
+    parity = {"frames_compared": n, "bit_exact_results": exact, "max_t_diff_m": max_te, "max_rot_diff_deg": max_ae,
+              "adapted_table_bit_exact": table_equal, "oracle_adapt_seconds": round(adapt_s, 1),
+              "adapted_table": f"oracle's own {args.adapt_frames}-frame adaptation vs the GPU's (counts + modes)"}
     return base, parity
 
 
 # ------------------------------------------------------------------ reference arm (CPU)
-def run_reference(args):
+def run_reference(args, wl: Workload):
+    """The reference's CPU path (restated in oracle/) on the host cores. Never
+    imports the B200 package: scene, trajectories and forest come from the oracle."""
     rank, local, world = dist_env()
     if rank != 0:
         return
-    import paper_1810_12163_b200 as P  # host-side generators only (no GPU calls)
-
     threads = os.cpu_count() or 1
-    prims = P.generate_synthetic_scene(SCENE_SEED, 20)
     t0 = time.perf_counter()
-    O, of, forest, state, scene, _ = _oracle_world(prims, args.adapt_frames, threads)
+    O, of, forest, state, scene, _, k = _oracle_world(wl, SCENE_SEED, args.adapt_frames, threads)
     setup_s = time.perf_counter() - t0
-    k = of.intrinsics()
     n_total = max(args.test_frames, threads)
     poses = O.trajectory(SCENE_SEED, n_total * world, args.test_kind)[:n_total]
     B = min(args.ref_batch or threads, n_total)
-    st = [of.ransac_params(p) for p in ("fast", "intermediate", "slow")]
+    st = _oracle_stages(of, wl)
+    modes = [m for _, m in wl.stages]
     pidx = list(range(min(n_total, B * (args.steps + args.warmup))))
     D, RGB = O.render(scene, [poses[i] for i in pidx], k, threads)
 
-    def step(s):
-        part = [(s * B + j) % len(pidx) for j in range(B)]
+    def step(s, nthreads, b):
+        part = [(s * b + j) % len(pidx) for j in range(b)]
         t = time.perf_counter()
-        res = O.cascade_batch(forest, state, scene, D[part], RGB[part], k, st, list(of.CASCADE_MODES),
-                              list(of.CASCADE_THRESHOLDS), [frame_seed(RUN_SEED, i) for i in part], threads=threads)
+        res = O.cascade_batch(forest, state, scene, D[part], RGB[part], k, st, modes, list(wl.thresholds),
+                              [frame_seed(RUN_SEED, i) for i in part], threads=nthreads)
         return time.perf_counter() - t, part, res
 
     for w in range(args.warmup):
-        step(w)
+        step(w, threads, B)
     tot, ok, n = 0.0, 0, 0
     for s in range(args.steps):
-        dt, part, res = step(args.warmup + s)
+        dt, part, res = step(args.warmup + s, threads, B)
         tot += dt
         for i, r in zip(part, res):
             n += 1
@@ -599,15 +854,24 @@ def run_reference(args):
                 R, t = of.pose_np(r.pose)
                 ok += success(R, t, poses[i])[0]
     value = n / tot
+    # 1-thread number: a bounded sample of the same frames on one core
+    one_t, one_n, s = 0.0, 0, 0
+    while one_t < args.cpu_seconds and one_n < len(pidx):
+        dt, _, _ = step(s, 1, 1)
+        one_t += dt
+        one_n += 1
+        s += 1
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 2),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (geometry f64)",
+           "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32 (geometry f64)",
            "data": "synthetic",
-           "config": {"workload": WORKLOAD, "frames_per_step": B, "adapt_frames": args.adapt_frames,
-                      "resolution": "640x480"},
+           "config": {"workload": wl.desc, "workload_key": wl.name, "frames_per_step": B,
+                      "adapt_frames": args.adapt_frames, "resolution": f"{wl.res[0]}x{wl.res[1]}"},
            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port",
                             "sample": f"{B} frames per step x {args.steps} steps; reference unbuildable here "
-                                      "(Eigen/libpng absent, 11/13 sources missing) -> oracle/ C++ port"},
+                                      "(Eigen/libpng absent, 11/13 sources missing) -> oracle/ C++ port",
+                            "one_thread": {"value": round(one_n / max(one_t, 1e-9), 4), "cores": 1,
+                                           "sample": f"{one_n} frames, {one_t:.1f} s"}},
            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "accuracy": {"success_5cm_5deg": round(ok / max(1, n), 4), "frames": n},
            "setup_seconds": round(setup_s, 1)}
@@ -615,29 +879,38 @@ def run_reference(args):
 
 
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=128, help="frames per lane per step (a step is lanes x batch frames per GPU)")
-    ap.add_argument("--test-frames", type=int, default=1024, help="resident test frames per GPU")
+    ap.add_argument("--workload", default="cascade", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="frames per lane per step (default: the workload's)")
+    ap.add_argument("--test-frames", type=int, default=1024, help="resident test frames per GPU (per scene)")
     ap.add_argument("--adapt-frames", type=int, default=1000)
     ap.add_argument("--test-kind", type=int, default=2,
                     help="test trajectory: 2 = held-out novel poses up to 55 cm/55 deg (default), 1 = near-loop poses")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-batch", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--lanes", type=int, default=5, help="relocalisation lanes (streams + host threads) per GPU")
+    ap.add_argument("--lanes", type=int, default=0, help="relocalisation lanes (streams + host threads) per GPU")
     ap.add_argument("--profile-window", action="store_true",
                     help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
     args = ap.parse_args(argv)
+    wl = WORKLOADS[args.workload]
+    args.batch = args.batch or wl.batch
+    args.lanes = args.lanes or wl.lanes
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args, argv))
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args, wl)
+    elif wl.name == "adapt":
+        run_adapt(args, wl)
     else:
-        run_ours(args)
+        run_ours(args, wl)
 
 
 if __name__ == "__main__":
