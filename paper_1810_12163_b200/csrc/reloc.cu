@@ -1156,7 +1156,233 @@ SCR_DEV void lm_accum(const Pose& H, const double x[3], const ModeGeom& mg, bool
   for (int a = 0; a < 6; ++a) acc[21 + a] = acc[21 + a] + ((J[0][a] * r[0] + J[1][a] * r[1]) + J[2][a] * r[2]);
 }
 
-// One LM iteration's damped 6x6 solve, all lanes in lockstep.
+// LM state per (frame, candidate) lives in global memory so that each LM iteration can be
+// split into two well-shaped kernels:
+//  k_lm_assoc — warp per sample, lanes over hypotheses: nearest mode of H x (f32 metric of
+//               Eq. 5, or Euclidean without covariance) for every hypothesis that needs a
+//               fresh association; each mode is loaded once per warp (uniform load);
+//  k_lm_step  — warp per hypothesis, lanes over samples in the canonical 32-lane order:
+//               normal equations with the frozen association, damped solve, trial
+//               energy, accept/reject (identical on every lane).
+struct LmState {
+  double lambda;
+  int need_assoc, done;
+};
+
+__global__ void k_lm_init(const int* __restrict__ ncand, int n_out, int cand_stride, LmState* __restrict__ st) {
+  const int a = blockIdx.x, h = threadIdx.x;
+  if (h >= cand_stride) return;
+  LmState s;
+  s.lambda = 1e-3;
+  s.need_assoc = 1;
+  s.done = (ncand[a] <= n_out || h >= ncand[a]) ? 1 : 0;
+  st[static_cast<size_t>(a) * cand_stride + h] = s;
+}
+
+__global__ void __launch_bounds__(256) k_lm_assoc(FrameRefs fr, PredView pv, LmArgs la,
+                                                  const int* __restrict__ samples, const Pose* __restrict__ cand,
+                                                  const int* __restrict__ ncand, const LmState* __restrict__ st,
+                                                  int* __restrict__ assoc, unsigned long long* __restrict__ work) {
+  __shared__ float s_pose[kSmallHyps][12];
+  __shared__ int s_need[kSmallHyps];
+  __shared__ int s_any;
+  __shared__ float4 s_modes[8 * 96];
+  __shared__ int s_mi[8 * 32];
+  const int a = blockIdx.y;
+  const int n = ncand[a];
+  if (n <= la.n_out) return;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  for (int h = threadIdx.x; h < n; h += blockDim.x) {
+    const LmState ls = st[static_cast<size_t>(a) * la.cand_stride + h];
+    const int need = (!ls.done && ls.need_assoc) ? 1 : 0;
+    s_need[h] = need;
+    if (need) {
+      s_any = 1;
+      const Pose& P = cand[static_cast<size_t>(a) * la.cand_stride + h];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) s_pose[h][i] = static_cast<float>(P.R[i]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s_pose[h][9 + i] = static_cast<float>(P.t[i]);
+    }
+  }
+  __syncthreads();
+  if (!s_any) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (s >= la.ns) return;
+  const int h0 = lane, h1 = lane + 32;
+  const bool v0 = h0 < n && s_need[h0], v1 = h1 < n && s_need[h1];
+  const int f = fr.fidx[a];
+  const size_t gb = static_cast<size_t>(f) * fr.gmax + samples[static_cast<size_t>(a) * la.scap + s];
+  int best0 = -1, best1 = -1;
+  if (fr.gnm[gb] > 0 && __any_sync(0xffffffffu, v0 || v1)) {  // warp-uniform: lanes cooperate below
+    float R0[9], t0[3], R1[9], t1[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      R0[i] = v0 ? s_pose[h0][i] : 0.0f;
+      R1[i] = v1 ? s_pose[h1][i] : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      t0[i] = v0 ? s_pose[h0][9 + i] : 0.0f;
+      t1[i] = v1 ? s_pose[h1][9 + i] : 0.0f;
+    }
+    const float4 c = fr.gcam[gb];
+    float y0[3], y1[3];
+    xform_f32(R0, t0, c.x, c.y, c.z, y0);
+    xform_f32(R1, t1, c.x, c.y, c.z, y1);
+    float q0b = 0.0f, q1b = 0.0f;
+    const int nm = fr.gnm[gb];
+    SampleModes sm;
+    sample_modes(fr, pv.count, gb, lane, sm);
+    float4* wbuf = s_modes + wid * 96;
+    int* wmi = s_mi + wid * 32;
+    for (int j0 = 0; j0 < nm; j0 += 32) {
+      wmi[lane] = stage_modes(pv, sm, fr.T, nm, j0, lane, wbuf);
+      __syncwarp();
+      const int cnt = min(32, nm - j0);
+      for (int m = 0; m < cnt; ++m) {
+        const float4 g0 = wbuf[3 * m];
+        const int mi = wmi[m];
+        float qa, qb;
+        const float a0 = __fsub_rn(y0[0], g0.x), a1 = __fsub_rn(y0[1], g0.y), a2 = __fsub_rn(y0[2], g0.z);
+        const float b0 = __fsub_rn(y1[0], g0.x), b1 = __fsub_rn(y1[1], g0.y), b2 = __fsub_rn(y1[2], g0.z);
+        if (la.use_cov) {
+          const float4 g1 = wbuf[3 * m + 1], g2 = wbuf[3 * m + 2];
+          qa = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, a0, a1, a2);
+          qb = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, b0, b1, b2);
+        } else {
+          qa = quad_eucl(a0, a1, a2);
+          qb = quad_eucl(b0, b1, b2);
+        }
+        if (best0 < 0 || qa < q0b) {  // first minimum wins ties
+          q0b = qa;
+          best0 = mi;
+        }
+        if (best1 < 0 || qb < q1b) {
+          q1b = qb;
+          best1 = mi;
+        }
+      }
+      __syncwarp();
+    }
+    if (work && lane == 0)
+      atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(fr.gnm[gb]) * static_cast<unsigned long long>(n));
+  }
+  if (v0) assoc[(static_cast<size_t>(a) * la.cand_stride + h0) * la.scap + s] = best0;
+  if (v1) assoc[(static_cast<size_t>(a) * la.cand_stride + h1) * la.scap + s] = best1;
+}
+
+// Global mode index of union position j of a sample's predicted modes (trees in order).
+SCR_DEV int union_mode(const SampleModes& sm, int T, int j) {
+  int slot = sm.slot[0], before = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxTrees - 1; ++q)
+    if (q < T - 1 && j >= sm.end[q]) {
+      slot = sm.slot[q + 1];
+      before = sm.end[q];
+    }
+  return slot * kMaxModes + (j - before);
+}
+
+// k_lm_assoc for <= 32 / G candidates per frame (the later preemption steps): warp per
+// sample, a group of G lanes per candidate, the group's lanes stride the sample's modes and
+// the group min-reduces (quadratic form, union position) — the same mode as the sequential
+// first-minimum scan. Keeps every lane busy when only a few candidates remain (with lanes
+// over candidates, 2 candidates would leave 30 of 32 lanes idle).
+template <int G>
+__global__ void __launch_bounds__(256) k_lm_assoc_g(FrameRefs fr, PredView pv, LmArgs la,
+                                                    const int* __restrict__ samples, const Pose* __restrict__ cand,
+                                                    const int* __restrict__ ncand, const LmState* __restrict__ st,
+                                                    int* __restrict__ assoc, unsigned long long* __restrict__ work) {
+  constexpr int NH = 32 / G;
+  __shared__ float s_pose[NH][12];
+  __shared__ int s_need[NH];
+  __shared__ int s_any;
+  const int a = blockIdx.y;
+  const int n = ncand[a];
+  if (n <= la.n_out) return;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  for (int h = threadIdx.x; h < NH; h += blockDim.x) {
+    int need = 0;
+    if (h < n) {
+      const LmState ls = st[static_cast<size_t>(a) * la.cand_stride + h];
+      need = (!ls.done && ls.need_assoc) ? 1 : 0;
+    }
+    s_need[h] = need;
+    if (need) {
+      s_any = 1;
+      const Pose& P = cand[static_cast<size_t>(a) * la.cand_stride + h];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) s_pose[h][i] = static_cast<float>(P.R[i]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s_pose[h][9 + i] = static_cast<float>(P.t[i]);
+    }
+  }
+  __syncthreads();
+  if (!s_any) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (s >= la.ns) return;
+  const int h = lane / G, sub = lane % G;
+  const bool v = s_need[h] != 0;
+  const int f = fr.fidx[a];
+  const size_t gb = static_cast<size_t>(f) * fr.gmax + samples[static_cast<size_t>(a) * la.scap + s];
+  const int nm = fr.gnm[gb];
+  int bj = 0x7fffffff, bmi = -1;
+  if (nm > 0 && __any_sync(0xffffffffu, v)) {  // warp-uniform
+    SampleModes sm;
+    sample_modes(fr, pv.count, gb, lane, sm);
+    float bq = 0.0f;
+    if (v) {
+      float R[9], t[3], y[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) R[i] = s_pose[h][i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) t[i] = s_pose[h][9 + i];
+      const float4 c = fr.gcam[gb];
+      xform_f32(R, t, c.x, c.y, c.z, y);
+      for (int j = sub; j < nm; j += G) {
+        const int mi = union_mode(sm, fr.T, j);
+        const float4 g0 = pv.geom[mi].q0;
+        const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
+        float q;
+        if (la.use_cov) {
+          const float4 g1 = pv.geom[mi].q1;
+          q = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, pv.geom[mi].q2.x, d0, d1, d2);
+        } else {
+          q = quad_eucl(d0, d1, d2);
+        }
+        if (bj == 0x7fffffff || q < bq) {  // first minimum of this lane's (increasing) positions
+          bq = q;
+          bj = j;
+          bmi = mi;
+        }
+      }
+    }
+#pragma unroll
+    for (int off = G / 2; off >= 1; off >>= 1) {  // stays inside the aligned G-lane group
+      const float oq = __shfl_xor_sync(0xffffffffu, bq, off);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+      const int om = __shfl_xor_sync(0xffffffffu, bmi, off);
+      if (oj != 0x7fffffff && (bj == 0x7fffffff || oq < bq || (oq == bq && oj < bj))) {
+        bq = oq;
+        bj = oj;
+        bmi = om;
+      }
+    }
+    if (work && lane == 0) {
+      int nv = 0;
+      for (int hh = 0; hh < NH; ++hh) nv += s_need[hh];
+      atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(nm) * static_cast<unsigned long long>(nv));
+    }
+  }
+  if (v && sub == 0) assoc[(static_cast<size_t>(a) * la.cand_stride + h) * la.scap + s] = bmi;
+}
+
+// One LM iteration of one hypothesis, all lanes in lockstep.
 __device__ __noinline__ bool lm_solve(const double* acc, double lambda, double delta[6]) {
   double M[36], rhs[6];
   int k = 0;
@@ -1175,135 +1401,105 @@ __device__ __noinline__ bool lm_solve(const double* acc, double lambda, double d
   return chol6(M, rhs, delta);
 }
 
-// k_lm — all (<= 10) LM iterations of one preemption step in one launch: warp per (frame,
-// candidate), 8 candidates of a frame per CTA (their warps read the same samples' modes,
-// so those loads hit L1). Lane l owns samples l, l + 32, ... (the canonical 32-lane order):
-// it associates each of its samples with the nearest predicted mode of H x (the f32 metric
-// of Eq. 5, or Euclidean without covariance; ties to the first mode in union order), then
-// accumulates the f64 normal equations over them; the 28 sums are xor-butterflied, so every
-// lane takes the same accept/reject path and the warp leaves the loop as soon as its
-// candidate converges. The association is recomputed only after an accepted step.
-constexpr int kLmWarps = 8;
-#ifndef SCR_LM_MINB
-#define SCR_LM_MINB 2  // 128 registers (80 B of spills) instead of 182 at one CTA per SM
-#endif
-
-__global__ void __launch_bounds__(kLmWarps * 32, SCR_LM_MINB) k_lm(FrameRefs fr, PredView pv, LmArgs la,
-                                                       const int* __restrict__ samples, Pose* __restrict__ cand,
-                                                       const int* __restrict__ ncand, int* __restrict__ assoc,
-                                                       unsigned long long* __restrict__ work) {
+__global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmArgs la,
+                                                 const int* __restrict__ samples, Pose* __restrict__ cand,
+                                                 const int* __restrict__ ncand, LmState* __restrict__ st,
+                                                 const int* __restrict__ assoc, unsigned long long* __restrict__ work) {
   const int a = blockIdx.y;
-  const int n = ncand[a];
-  const int h = blockIdx.x * kLmWarps + (threadIdx.x >> 5);
+  const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
+  const int n = ncand[a];
   if (n <= la.n_out || h >= n) return;
   const size_t hi = static_cast<size_t>(a) * la.cand_stride + h;
+  LmState ls = st[hi];
+  if (ls.done) return;
   const int f = fr.fidx[a];
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
   const int* smp = samples + static_cast<size_t>(a) * la.scap;
-  int* as = assoc + hi * la.scap;
-  const bool use_cov = la.use_cov != 0;
+  const int* as = assoc + hi * la.scap;
   Pose H = cand[hi];
-  double lambda = 1e-3;
-  bool need_assoc = true;
-  unsigned terms = 0, evals = 0;
-#pragma unroll 1
-  for (int it = 0; it < 10; ++it) {
-    if (need_assoc) {
-      float R[9], t[3];
+  double acc[28];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) R[i] = static_cast<float>(H.R[i]);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(H.t[i]);
-#pragma unroll 1
-      for (int i = lane; i < la.ns; i += 32) {
-        const size_t gb = fbase + smp[i];
-        int best = -1;
-        if (fr.gnm[gb] > 0) {
-          const float4 c = fr.gcam[gb];
-          float y[3];
-          xform_f32(R, t, c.x, c.y, c.z, y);
-          float qb = 0.0f;
-#pragma unroll 1
-          for (int tr = 0; tr < fr.T; ++tr) {
-            const int slot = fr.gslot[gb * fr.T + tr];
-            const int cnt = pv.count[slot];
-            evals += static_cast<unsigned>(cnt);
-#pragma unroll 1
-            for (int m = 0; m < cnt; ++m) {
-              const int mi = slot * kMaxModes + m;
-              const float4 g0 = pv.geom[mi].q0;
-              const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
-              float q;
-              if (use_cov) {
-                const float4 g1 = pv.geom[mi].q1;
-                const float g2x = pv.geom[mi].q2.x;
-                q = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2x, d0, d1, d2);
-              } else {
-                q = quad_eucl(d0, d1, d2);
-              }
-              if (best < 0 || q < qb) {  // first minimum wins ties
-                qb = q;
-                best = mi;
-              }
-            }
-          }
-        }
-        as[i] = best;
-      }
-      need_assoc = false;
+  for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+  int terms = 0;
+  // lane l accumulates samples l, l + 32, l + 64, ... in order; two of them are loaded
+  // before either is accumulated, so two gathers are in flight per lane
+  for (int i = lane; i < la.ns; i += 64) {
+    const int i2 = i + 32;
+    const int mi0 = as[i], mi1 = i2 < la.ns ? as[i2] : -1;
+    float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
+    ModeGeom g0{}, g1{};
+    if (mi0 >= 0) {
+      c0 = fr.gcam[fbase + smp[i]];
+      g0 = pv.geom[mi0];
     }
-    double acc[28];
-#pragma unroll
-    for (int k = 0; k < 28; ++k) acc[k] = 0.0;
-#pragma unroll 1
-    for (int i = lane; i < la.ns; i += 32) {
-      const int mi = as[i];
-      if (mi < 0) continue;
-      const float4 c = fr.gcam[fbase + smp[i]];
-      const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
-      lm_accum(H, x, pv.geom[mi], use_cov, acc, true);
+    if (mi1 >= 0) {
+      c1 = fr.gcam[fbase + smp[i2]];
+      g1 = pv.geom[mi1];
+    }
+    if (mi0 >= 0) {
+      const double x[3] = {static_cast<double>(c0.x), static_cast<double>(c0.y), static_cast<double>(c0.z)};
+      lm_accum(H, x, g0, la.use_cov != 0, acc, true);
       ++terms;
     }
+    if (mi1 >= 0) {
+      const double x[3] = {static_cast<double>(c1.x), static_cast<double>(c1.y), static_cast<double>(c1.z)};
+      lm_accum(H, x, g1, la.use_cov != 0, acc, true);
+      ++terms;
+    }
+  }
+  if (work) work_add(work, W_LM_TERMS, static_cast<unsigned>(terms));
 #pragma unroll
-    for (int k = 0; k < 28; ++k) acc[k] = warp_sum_xor(acc[k]);
-    const double E = acc[27];
-    if (!(E > 0.0)) break;
+  for (int k = 0; k < 28; ++k) acc[k] = warp_sum_xor(acc[k]);
+  ls.need_assoc = 0;
+  const double E = acc[27];
+  if (!(E > 0.0)) {
+    ls.done = 1;
+  } else {
     double delta[6];
-    if (!lm_solve(acc, lambda, delta)) {
-      lambda = lambda * 10.0;
-      continue;
-    }
-    Pose D, Hn;
-    exp_se3(delta, D);
-    pose_compose(D, H, Hn);
-    double en = 0.0;
-#pragma unroll 1
-    for (int i = lane; i < la.ns; i += 32) {
-      const int mi = as[i];
-      if (mi < 0) continue;
-      const float4 c = fr.gcam[fbase + smp[i]];
-      const double x[3] = {static_cast<double>(c.x), static_cast<double>(c.y), static_cast<double>(c.z)};
-      double accn[28];
-      accn[27] = en;
-      lm_accum(Hn, x, pv.geom[mi], use_cov, accn, false);
-      en = accn[27];
-    }
-    const double En = warp_sum_xor(en);
-    if (En < E) {
-      H = Hn;
-      lambda = lambda * 0.1;
-      need_assoc = true;
-      if ((E - En) / E < 1e-6) break;
+    if (!lm_solve(acc, ls.lambda, delta)) {
+      ls.lambda = ls.lambda * 10.0;
     } else {
-      lambda = lambda * 10.0;
+      Pose D, Hn;
+      exp_se3(delta, D);
+      pose_compose(D, H, Hn);
+      double accn[28];
+      accn[27] = 0.0;
+      for (int i = lane; i < la.ns; i += 64) {
+        const int i2 = i + 32;
+        const int mi0 = as[i], mi1 = i2 < la.ns ? as[i2] : -1;
+        float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
+        ModeGeom g0{}, g1{};
+        if (mi0 >= 0) {
+          c0 = fr.gcam[fbase + smp[i]];
+          g0 = pv.geom[mi0];
+        }
+        if (mi1 >= 0) {
+          c1 = fr.gcam[fbase + smp[i2]];
+          g1 = pv.geom[mi1];
+        }
+        if (mi0 >= 0) {
+          const double x[3] = {static_cast<double>(c0.x), static_cast<double>(c0.y), static_cast<double>(c0.z)};
+          lm_accum(Hn, x, g0, la.use_cov != 0, accn, false);
+        }
+        if (mi1 >= 0) {
+          const double x[3] = {static_cast<double>(c1.x), static_cast<double>(c1.y), static_cast<double>(c1.z)};
+          lm_accum(Hn, x, g1, la.use_cov != 0, accn, false);
+        }
+      }
+      const double En = warp_sum_xor(accn[27]);
+      if (En < E) {
+        H = Hn;
+        ls.lambda = ls.lambda * 0.1;
+        ls.need_assoc = 1;
+        if ((E - En) / E < 1e-6) ls.done = 1;
+        if (lane == 0) cand[hi] = H;
+      } else {
+        ls.lambda = ls.lambda * 10.0;
+      }
     }
   }
-  if (lane == 0) cand[hi] = H;
-  if (work) {
-    work_add(work, W_LM_TERMS, terms);
-    work_add(work, W_LM_ASSOC, evals);
-  }
+  if (lane == 0) st[hi] = ls;
 }
 
 // ================================ K8-K10: ICP + raycast + depth-difference score ============
@@ -1973,10 +2169,34 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
     const int ns = p.eta * (k + 1);
     if (p.pose_update) {
       la.ns = ns;
+      LmState* lmst = static_cast<LmState*>(w.lmst);
+      SCR_LAUNCH(s, K_LM, (k_lm_init<<<nA, w.ncull_cap, 0, s->stream>>>(w.ncand, p.n_out, w.ncull_cap, lmst)));
       // candidates still in play at step k: at most ceil(n_cull / 2^(k-1))
       const int nk = (p.n_cull + (1 << (k - 1)) - 1) >> (k - 1);
-      SCR_LAUNCH(s, K_LM, (k_lm<<<dim3((nk + kLmWarps - 1) / kLmWarps, nA), kLmWarps * 32, 0, s->stream>>>(
-                              fr, pv, la, w.samples, w.cand, w.ncand, w.assoc, wk)));
+      for (int it = 0; it < 10; ++it) {
+        const dim3 ag((ns + 7) / 8, nA);
+        if (nk > 16) {
+          SCR_LAUNCH(s, K_LM, (k_lm_assoc<<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
+                                                                     w.assoc, wk)));
+        } else if (nk > 8) {
+          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<2><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
+                                                                          w.assoc, wk)));
+        } else if (nk > 4) {
+          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<4><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
+                                                                          w.assoc, wk)));
+        } else if (nk > 2) {
+          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<8><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
+                                                                          w.assoc, wk)));
+        } else if (nk > 1) {
+          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<16><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand,
+                                                                           lmst, w.assoc, wk)));
+        } else {
+          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<32><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand,
+                                                                           lmst, w.assoc, wk)));
+        }
+        SCR_LAUNCH(s, K_LM, (k_lm_step<<<dim3((p.n_cull + 3) / 4, nA), 128, 0, s->stream>>>(
+                                fr, pv, la, w.samples, w.cand, w.ncand, lmst, w.assoc, wk)));
+      }
     }
     // rescore (only frames still above n_out take part): per-batch partial energies, then
     // E(I_k) = E(I_{k-1}) + E_k without LM (poses unchanged), or the full batch sum with LM
@@ -2094,6 +2314,7 @@ scr_status ensure_ransac_ws(scr_scene s, int nmax, int ncull, int scap) {
     SCR_TRY(grow(&w.icp_rms, B * nc));
     SCR_TRY(grow(&w.icp_inl, B * nc));
     SCR_TRY(grow(&w.epart, B * nc * kEnergyBatches));
+    SCR_TRY(grow(reinterpret_cast<LmState**>(&w.lmst), B * nc));
     w.ncull_cap = nc;
     w.samples_cap = sc;
     if (w.henergy && static_cast<size_t>(w.nmax_cap) < static_cast<size_t>(nc)) {
