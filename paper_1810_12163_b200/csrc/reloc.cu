@@ -1300,6 +1300,8 @@ __global__ void __launch_bounds__(256) k_lm_assoc_g(FrameRefs fr, PredView pv, L
   __shared__ float s_pose[NH][12];
   __shared__ int s_need[NH];
   __shared__ int s_any;
+  __shared__ float4 s_modes[8 * 64];  // per warp: 32 staged modes x {mu + c00, c11 c22 2c01 2c02}
+  __shared__ float s_c12[8 * 32];     // ... and 2c12
   const int a = blockIdx.y;
   const int n = ncand[a];
   if (n <= la.n_out) return;
@@ -1336,43 +1338,57 @@ __global__ void __launch_bounds__(256) k_lm_assoc_g(FrameRefs fr, PredView pv, L
     SampleModes sm;
     sample_modes(fr, pv.count, gb, lane, sm);
     float bq = 0.0f;
-    if (v) {
-      float R[9], t[3], y[3];
+    float R[9], t[3], y[3];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) R[i] = s_pose[h][i];
+    for (int i = 0; i < 9; ++i) R[i] = s_pose[h][i];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) t[i] = s_pose[h][9 + i];
-      const float4 c = fr.gcam[gb];
-      xform_f32(R, t, c.x, c.y, c.z, y);
-      for (int j = sub; j < nm; j += G) {
-        const int mi = union_mode(sm, fr.T, j);
-        const float4 g0 = pv.geom[mi].q0;
-        const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
-        float q;
+    for (int i = 0; i < 3; ++i) t[i] = s_pose[h][9 + i];
+    const float4 c = fr.gcam[gb];
+    xform_f32(R, t, c.x, c.y, c.z, y);
+    float4* wbuf = s_modes + wid * 64;
+    float* wc12 = s_c12 + wid * 32;
+    for (int j0 = 0; j0 < nm; j0 += 32) {
+      // lane l stages mode j0 + l (one coalesced round trip per 32 modes)
+      const int jl = j0 + lane;
+      if (jl < nm) {
+        const int mi = union_mode(sm, fr.T, jl);
+        wbuf[2 * lane] = pv.geom[mi].q0;
         if (la.use_cov) {
-          const float4 g1 = pv.geom[mi].q1;
-          q = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, pv.geom[mi].q2.x, d0, d1, d2);
-        } else {
-          q = quad_eucl(d0, d1, d2);
-        }
-        if (bj == 0x7fffffff || q < bq) {  // first minimum of this lane's (increasing) positions
-          bq = q;
-          bj = j;
-          bmi = mi;
+          wbuf[2 * lane + 1] = pv.geom[mi].q1;
+          wc12[lane] = pv.geom[mi].q2.x;
         }
       }
+      __syncwarp();
+      const int cnt = min(32, nm - j0);
+      if (v) {
+        for (int jj = sub; jj < cnt; jj += G) {
+          const float4 g0 = wbuf[2 * jj];
+          const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
+          float q;
+          if (la.use_cov) {
+            const float4 g1 = wbuf[2 * jj + 1];
+            q = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, wc12[jj], d0, d1, d2);
+          } else {
+            q = quad_eucl(d0, d1, d2);
+          }
+          if (bj == 0x7fffffff || q < bq) {  // first minimum of this lane's (increasing) positions
+            bq = q;
+            bj = j0 + jj;
+          }
+        }
+      }
+      __syncwarp();
     }
 #pragma unroll
     for (int off = G / 2; off >= 1; off >>= 1) {  // stays inside the aligned G-lane group
       const float oq = __shfl_xor_sync(0xffffffffu, bq, off);
       const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
-      const int om = __shfl_xor_sync(0xffffffffu, bmi, off);
       if (oj != 0x7fffffff && (bj == 0x7fffffff || oq < bq || (oq == bq && oj < bj))) {
         bq = oq;
         bj = oj;
-        bmi = om;
       }
     }
+    if (bj != 0x7fffffff) bmi = union_mode(sm, fr.T, bj);
     if (work && lane == 0) {
       int nv = 0;
       for (int hh = 0; hh < NH; ++hh) nv += s_need[hh];
@@ -1401,6 +1417,11 @@ __device__ __noinline__ bool lm_solve(const double* acc, double lambda, double d
   return chol6(M, rhs, delta);
 }
 
+#ifndef SCR_LM_INFLIGHT
+#define SCR_LM_INFLIGHT 4
+#endif
+constexpr int kLmInFlight = SCR_LM_INFLIGHT;  // sample gathers in flight per lane
+
 __global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmArgs la,
                                                  const int* __restrict__ samples, Pose* __restrict__ cand,
                                                  const int* __restrict__ ncand, LmState* __restrict__ st,
@@ -1422,31 +1443,28 @@ __global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmAr
 #pragma unroll
   for (int k = 0; k < 28; ++k) acc[k] = 0.0;
   int terms = 0;
-  // lane l accumulates samples l, l + 32, l + 64, ... in order; two of them are loaded
-  // before either is accumulated, so two gathers are in flight per lane
-  for (int i = lane; i < la.ns; i += 64) {
-    const int i2 = i + 32;
-    const int mi0 = as[i], mi1 = i2 < la.ns ? as[i2] : -1;
-    float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
-    ModeGeom g0{}, g1{};
-    if (mi0 >= 0) {
-      c0 = fr.gcam[fbase + smp[i]];
-      g0 = pv.geom[mi0];
+  // lane l accumulates samples l, l + 32, l + 64, ... in order; kLmInFlight of them are
+  // gathered before any is accumulated (the loads are independent, the sums are not)
+  for (int i0 = lane; i0 < la.ns; i0 += 32 * kLmInFlight) {
+    int mi[kLmInFlight];
+    float4 c[kLmInFlight];
+    ModeGeom gm[kLmInFlight];
+#pragma unroll
+    for (int u = 0; u < kLmInFlight; ++u) {
+      const int i = i0 + 32 * u;
+      mi[u] = i < la.ns ? as[i] : -1;
+      if (mi[u] >= 0) {
+        c[u] = fr.gcam[fbase + smp[i]];
+        gm[u] = pv.geom[mi[u]];
+      }
     }
-    if (mi1 >= 0) {
-      c1 = fr.gcam[fbase + smp[i2]];
-      g1 = pv.geom[mi1];
-    }
-    if (mi0 >= 0) {
-      const double x[3] = {static_cast<double>(c0.x), static_cast<double>(c0.y), static_cast<double>(c0.z)};
-      lm_accum(H, x, g0, la.use_cov != 0, acc, true);
-      ++terms;
-    }
-    if (mi1 >= 0) {
-      const double x[3] = {static_cast<double>(c1.x), static_cast<double>(c1.y), static_cast<double>(c1.z)};
-      lm_accum(H, x, g1, la.use_cov != 0, acc, true);
-      ++terms;
-    }
+#pragma unroll
+    for (int u = 0; u < kLmInFlight; ++u)
+      if (mi[u] >= 0) {
+        const double x[3] = {static_cast<double>(c[u].x), static_cast<double>(c[u].y), static_cast<double>(c[u].z)};
+        lm_accum(H, x, gm[u], la.use_cov != 0, acc, true);
+        ++terms;
+      }
   }
   if (work) work_add(work, W_LM_TERMS, static_cast<unsigned>(terms));
 #pragma unroll
@@ -1465,27 +1483,26 @@ __global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmAr
       pose_compose(D, H, Hn);
       double accn[28];
       accn[27] = 0.0;
-      for (int i = lane; i < la.ns; i += 64) {
-        const int i2 = i + 32;
-        const int mi0 = as[i], mi1 = i2 < la.ns ? as[i2] : -1;
-        float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
-        ModeGeom g0{}, g1{};
-        if (mi0 >= 0) {
-          c0 = fr.gcam[fbase + smp[i]];
-          g0 = pv.geom[mi0];
+      for (int i0 = lane; i0 < la.ns; i0 += 32 * kLmInFlight) {
+        int mi[kLmInFlight];
+        float4 c[kLmInFlight];
+        ModeGeom gm[kLmInFlight];
+#pragma unroll
+        for (int u = 0; u < kLmInFlight; ++u) {
+          const int i = i0 + 32 * u;
+          mi[u] = i < la.ns ? as[i] : -1;
+          if (mi[u] >= 0) {
+            c[u] = fr.gcam[fbase + smp[i]];
+            gm[u] = pv.geom[mi[u]];
+          }
         }
-        if (mi1 >= 0) {
-          c1 = fr.gcam[fbase + smp[i2]];
-          g1 = pv.geom[mi1];
-        }
-        if (mi0 >= 0) {
-          const double x[3] = {static_cast<double>(c0.x), static_cast<double>(c0.y), static_cast<double>(c0.z)};
-          lm_accum(Hn, x, g0, la.use_cov != 0, accn, false);
-        }
-        if (mi1 >= 0) {
-          const double x[3] = {static_cast<double>(c1.x), static_cast<double>(c1.y), static_cast<double>(c1.z)};
-          lm_accum(Hn, x, g1, la.use_cov != 0, accn, false);
-        }
+#pragma unroll
+        for (int u = 0; u < kLmInFlight; ++u)
+          if (mi[u] >= 0) {
+            const double x[3] = {static_cast<double>(c[u].x), static_cast<double>(c[u].y),
+                                 static_cast<double>(c[u].z)};
+            lm_accum(Hn, x, gm[u], la.use_cov != 0, accn, false);
+          }
       }
       const double En = warp_sum_xor(accn[27]);
       if (En < E) {
