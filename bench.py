@@ -617,7 +617,7 @@ def run_ours(args, wl: Workload):
                      "stage_share": [round(x / max(1, n_res), 4) for x in stage_hist],
                      "per_novelty_bin": novelty,
                      "per_scene": {s: round(v[1] / v[0], 4) for s, v in sorted(per_scene_ok.items())}},
-        "stage_ms_per_step": [round(x / args.steps, 3) for x in stage_ms],
+        "stage_ms_per_step_summed_over_lanes": [round(x / args.steps, 3) for x in stage_ms],
         "kernel_share": share,
         "instrumented_pass": {"ms_per_batch": round(prof_ms / max(1, prof_batches), 3), "batches": prof_batches},
         "work": prof["work"],
@@ -712,10 +712,36 @@ def run_adapt(args, wl: Workload):
                                    for n, v in sorted(kern.items(), key=lambda x: -x[1]["ms"])},
            "kernel_share": {n: round(v["ms"] / max(1e-9, tot), 4) for n, v in kern.items()},
            "paper": {"ms_per_frame": wl.paper_ms, "ref": wl.paper_ref, "hardware": "GTX 1080Ti / Titan X (paper)"}}
+    if not args.no_cpu:
+        out["cpu_baseline"] = cpu_adapt_baseline(wl, args)
     print(json.dumps(out), flush=True)
     fs_t.close()
     fs.close()
     scene.close()
+
+
+def cpu_adapt_baseline(wl: Workload, args, threads: int | None = None) -> dict:
+    """The oracle's per-frame training (integrate_frame + update_leaves_round_robin(256)) on
+    full reservoirs, one frame after another on `threads` host threads for the prefill and
+    one thread for the timed frames (the reference's training is single-writer)."""
+    import ctypes as C
+
+    threads = threads or os.cpu_count() or 1
+    O, of, forest, state, scene, total, k = _oracle_world(wl, SCENE_SEED, args.adapt_frames, threads)
+    n_pre = args.adapt_frames
+    poses = O.trajectory(SCENE_SEED, n_pre + 64, 0)[n_pre:]
+    D, RGB = O.render(scene, poses, k, threads)
+    n, t = 0, 0.0
+    while t < args.cpu_seconds and n < len(poses):
+        t0 = time.perf_counter()
+        rc = O.integrate(state, forest, D[n], RGB[n], k, poses[n])
+        O.lib.or_update(state, C.c_int64(256))
+        t += time.perf_counter() - t0
+        assert rc == 0, O.err()
+        n += 1
+    return {"value": round(n / t, 3), "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": f"{n} frames of integrate_frame + update_leaves_round_robin(256) after a {n_pre}-frame "
+                      f"prefill, oracle/ C++ restatement, 1 thread, {t:.1f} s"}
 
 
 # ------------------------------------------------------------------ CPU oracle (checker only)
@@ -726,8 +752,10 @@ def _oracle():
     return of.get(), of
 
 
-def _oracle_world(wl: Workload, scene_seed: int, adapt_frames: int, threads: int):
-    """The oracle adapts its own state on the same seeded sequence (no GPU data)."""
+def _oracle_world(wl: Workload, scene_seed: int, adapt_frames: int, threads: int, gpu_table=None):
+    """The oracle adapts its own state on the same seeded sequence (no GPU data), unless
+    `gpu_table` (counts, modes) is given: then the GPU's adapted table is loaded (used only
+    for the 1280x960 kappa-4096 stress world, whose CPU adaptation would take hours)."""
     import ctypes as C
 
     O, of = _oracle()
@@ -736,6 +764,9 @@ def _oracle_world(wl: Workload, scene_seed: int, adapt_frames: int, threads: int
     scene = O.lib.or_scene_generate(scene_seed, 20)
     total = O.lib.or_forest_total_leaves(forest)
     k = of.intrinsics(*intrinsics_of(wl.res))
+    if gpu_table is not None:
+        O.load_predictions(state, gpu_table[0], gpu_table[1].view(of.MODE_DTYPE))
+        return O, of, forest, state, scene, total, k
     poses = O.trajectory(scene_seed, adapt_frames, 0)
     chunk = 100 if wl.res[0] <= 640 else 25
     for c0 in range(0, adapt_frames, chunk):
@@ -758,15 +789,20 @@ def cpu_baseline(wl: Workload, r0, gpu_results, args):
     the oracle adapts on its own, and its adapted table is compared with the GPU's."""
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    O, of, forest, state, scene, total, k = _oracle_world(wl, r0.seed, args.adapt_frames, threads)
+    own = wl.res[0] <= 640  # the stress world's table is loaded from the GPU (see _oracle_world)
+    gpu_table = None if own else r0.scene.predictions()
+    O, of, forest, state, scene, total, k = _oracle_world(wl, r0.seed, args.adapt_frames, threads, gpu_table)
     adapt_s = time.perf_counter() - t0
-    cnt_o, modes_o = O.predictions(state, total)
-    cnt_g, modes_g = r0.scene.predictions()
-    valid = (np.arange(50)[None, :] < cnt_o[:, None]).reshape(-1)
-    table_equal = bool(np.array_equal(cnt_o, cnt_g) and
-                       np.array_equal(modes_o.view(np.uint8).reshape(-1, 100)[valid],
-                                      modes_g.view(np.uint8).reshape(-1, 100)[valid]))
-    del modes_o, modes_g
+    table_equal = None
+    if own:
+        cnt_o, modes_o = O.predictions(state, total)
+        cnt_g, modes_g = r0.scene.predictions()
+        valid = (np.arange(50)[None, :] < cnt_o[:, None]).reshape(-1)
+        table_equal = bool(np.array_equal(cnt_o, cnt_g) and
+                           np.array_equal(modes_o.view(np.uint8).reshape(-1, 100)[valid],
+                                          modes_g.view(np.uint8).reshape(-1, 100)[valid]))
+        del modes_o, modes_g
+    del gpu_table
     gpu_by_frame = {}
     for idx, res in gpu_results:
         for i, r in zip(idx, res):
@@ -812,7 +848,9 @@ def cpu_baseline(wl: Workload, r0, gpu_results, args):
                       f"stages, oracle/ C++ restatement, {threads} threads, {el:.1f} s"}
     parity = {"frames_compared": n, "bit_exact_results": exact, "max_t_diff_m": max_te, "max_rot_diff_deg": max_ae,
               "adapted_table_bit_exact": table_equal, "oracle_adapt_seconds": round(adapt_s, 1),
-              "adapted_table": f"oracle's own {args.adapt_frames}-frame adaptation vs the GPU's (counts + modes)"}
+              "adapted_table": (f"oracle's own {args.adapt_frames}-frame adaptation vs the GPU's (counts + modes)" if own
+                                else "GPU-adapted table loaded into the oracle (stress world; adaptation parity is "
+                                     "held by tests/test_gpu_stress.py)")}
     return base, parity
 
 
@@ -824,6 +862,16 @@ def run_reference(args, wl: Workload):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    if wl.name == "adapt":
+        base = cpu_adapt_baseline(wl, args, threads)
+        print(json.dumps({"impl": "reference", "metric": "adapted frames/s (integrate + update(256) per frame)",
+                          "value": base["value"], "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "higher_is_better": True, "scaling": wl.scaling,
+                          "vs_baseline": None, "dtype": "f32 (positions f64)", "data": "synthetic",
+                          "config": {"workload": wl.desc, "workload_key": wl.name}, "cpu_baseline": base,
+                          "e2e": {"value": base["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
     t0 = time.perf_counter()
     O, of, forest, state, scene, _, k = _oracle_world(wl, SCENE_SEED, args.adapt_frames, threads)
     setup_s = time.perf_counter() - t0
