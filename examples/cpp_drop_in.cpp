@@ -42,7 +42,7 @@ int main() {
   std::vector<sg::RgbdFrame> frames;
   std::vector<uint64_t> seeds;
   for (int i = 0; i < n_test; ++i) {
-    frames.push_back({&depth[(n_adapt + i) * px], &rgb[(n_adapt + i) * px * 3], true});
+    frames.push_back({&depth[(n_adapt + i) * px], &rgb[(n_adapt + i) * px * 3], k.width, k.height, true});
     seeds.push_back(100 + i);
   }
   const auto res = reloc.run_cascade_batch(sg::CascadeConfig::paper_three_stage(), frames, seeds);
@@ -56,10 +56,16 @@ int main() {
   }
   std::printf("cpp drop-in: %d/%d frames within 5 cm (stage of frame 0: %d)\n", ok, n_test, res[0].stage_used);
   try {
-    reloc.integrate_frame({&depth[0], &rgb[0], false}, adapt[0]);
+    reloc.integrate_frame({&depth[0], &rgb[0], k.width, k.height, false}, adapt[0]);
     return 2;
-  } catch (const sg::UnreliablePose&) {
+  } catch (const screloc::UnreliablePose&) {  // the reference's class (core.hpp:53)
     std::printf("UnreliablePose raised as in the reference\n");
+  }
+  try {  // a frame whose size is not the scene's: screloc::DimensionMismatch (core.hpp:57)
+    reloc.relocalise(sg::profile("fast"), {&depth[0], &rgb[0], k.width / 2, k.height, true}, sg::Mode::Icp, 1);
+    return 3;
+  } catch (const screloc::DimensionMismatch&) {
+    std::printf("DimensionMismatch raised as in the reference\n");
   }
   {  // a second relocalisation lane on another thread gives the same poses
     sg::Relocaliser lane = reloc.fork_lane(n_test);

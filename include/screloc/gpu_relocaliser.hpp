@@ -23,9 +23,12 @@
 #include "../screloc_gpu.h"
 
 namespace screloc {
-namespace gpu {
 
-// ---- exceptions (core.hpp:24-72) --------------------------------------------------------
+// ---- exceptions: the reference's classes by name (core.hpp:24-72) ------------------------
+// A caller's `catch (screloc::InvalidDepth&)` fires for the B200 path exactly as for the CPU
+// reference. If the reference's core.hpp is included first, its classes are used as they
+// are; otherwise the same hierarchy (same names, same bases) is declared here.
+#ifndef SCRELOC_CORE_HPP
 class Error : public std::runtime_error {
  public:
   explicit Error(const std::string& w) : std::runtime_error(w) {}
@@ -35,15 +38,38 @@ class Error : public std::runtime_error {
    public:                      \
     using Error::Error;         \
   };
-SCRELOC_GPU_ERROR(InvalidDepth)
-SCRELOC_GPU_ERROR(InvalidCentrePixel)
-SCRELOC_GPU_ERROR(UnreliablePose)
-SCRELOC_GPU_ERROR(NoHypotheses)
-SCRELOC_GPU_ERROR(AllCandidatesFailed)
-SCRELOC_GPU_ERROR(DimensionMismatch)
-SCRELOC_GPU_ERROR(MalformedData)
-SCRELOC_GPU_ERROR(CudaError)
+SCRELOC_GPU_ERROR(InvalidDepth)        // core.hpp:29
+SCRELOC_GPU_ERROR(InvalidCentrePixel)  // core.hpp:33
+SCRELOC_GPU_ERROR(MalformedData)       // core.hpp:49
+SCRELOC_GPU_ERROR(UnreliablePose)      // core.hpp:53
+SCRELOC_GPU_ERROR(DimensionMismatch)   // core.hpp:57
 #undef SCRELOC_GPU_ERROR
+#endif
+// SPEC-level outcomes without a core.hpp class ("no pose") and device errors
+class NoHypotheses : public Error {
+ public:
+  using Error::Error;
+};
+class AllCandidatesFailed : public Error {
+ public:
+  using Error::Error;
+};
+class CudaError : public Error {
+ public:
+  using Error::Error;
+};
+
+namespace gpu {
+
+using screloc::AllCandidatesFailed;
+using screloc::CudaError;
+using screloc::DimensionMismatch;
+using screloc::Error;
+using screloc::InvalidCentrePixel;
+using screloc::InvalidDepth;
+using screloc::MalformedData;
+using screloc::NoHypotheses;
+using screloc::UnreliablePose;
 
 inline void check(scr_status s, const char* what) {
   if (s == SCR_OK) return;
@@ -79,8 +105,9 @@ inline RigidTransform identity_transform() {
 struct RgbdFrame {
   const float* depth = nullptr;
   const uint8_t* colour = nullptr;
+  int width = 0, height = 0;  // must match the relocaliser's intrinsics (else DimensionMismatch)
   bool pose_reliable = true;
-  scr_frame c() const { return scr_frame{depth, colour, pose_reliable ? 1 : 0, 0}; }
+  scr_frame c() const { return scr_frame{depth, colour, width, height, pose_reliable ? 1 : 0, 0}; }
 };
 
 enum class Mode : int { Raw = SCR_MODE_RAW, Icp = SCR_MODE_ICP, Ranked = SCR_MODE_RANKED };

@@ -48,8 +48,16 @@ typedef enum {
 typedef struct { int32_t width, height; double fx, fy, cx, cy; } scr_intrinsics;
 /* RigidTransform camera->world (geometry.hpp:14-42), row-major R */
 typedef struct { double R[9]; double t[3]; } scr_pose;
-/* RgbdFrame (features.hpp:31-44): depth metres (0/NaN invalid), colour RGB8 interleaved */
-typedef struct { const float* depth; const uint8_t* rgb; int32_t pose_reliable; int32_t pad; } scr_frame;
+/* RgbdFrame (features.hpp:31-44): depth metres (0/NaN invalid), colour RGB8 interleaved, both
+ * width x height row-major. width/height must equal the scene's intrinsics, else
+ * SCR_E_DIMENSION_MISMATCH (screloc::DimensionMismatch, core.hpp:57). */
+typedef struct {
+  const float* depth;
+  const uint8_t* rgb;
+  int32_t width, height;
+  int32_t pose_reliable;
+  int32_t pad;
+} scr_frame;
 /* forest-side profile parameters (Table 4) */
 typedef struct { float sigma, tau; int32_t max_clusters, min_cluster_size, capacity; } scr_forest_params;
 /* RansacParams (Table 4) */
@@ -202,6 +210,12 @@ scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_pa
    Kabsch ("suspect", decided by the exact finisher; overflows the per-frame list and exercises the
    exact continuation), 0 restores the normal classification. Results are identical either way. */
 scr_status scr_debug_generation_mode(scr_scene s, int mode);
+/* Generation diagnostics for one frame (not on the hot path): runs generate_hypothesis for
+ * every slot and histograms every attempt's outcome by rejection tag,
+ * tags[0..5] = {successful final attempts, NoModes, ColourCheckFailed, TooClose, NotRigid,
+ * DegenerateKabsch}; *slots_ok = slots that generated a hypothesis. */
+scr_status scr_debug_generation_stats(scr_scene s, const scr_frame* f, const scr_ransac_params* p, uint64_t seed,
+                                      int64_t* tags, int* slots_ok);
 scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, scr_pose* out, int* converged,
                          double* rms, double* inlier_frac, double* score);
 /* number of kernel launches issued by this scene so far (bench accounting) */

@@ -597,3 +597,26 @@ int or_generation_stats(void* fp, void* sp, const float* depth, const uint8_t* r
   });
 }
 }
+
+extern "C" {
+// KAT hooks (test infrastructure): checks 2-3 + Kabsch of one explicit triplet, and the LM
+// residual/Jacobian of one sample.
+int or_check_triplet(const double* cm, const double* w, const or_ransac_params* rp, or_pose* out) {
+  Pose T;
+  const int tag = check_triplet(cm, w, to_rp(*rp), &T);
+  if (tag == REJ_OK && out) {
+    std::memcpy(out->R, T.R, sizeof(T.R));
+    std::memcpy(out->t, T.t, sizeof(T.t));
+  }
+  return tag;
+}
+void or_lm_residual_jacobian(const or_pose* H, const double* x, const or_mode* m, int use_cov, double* r,
+                             double* J) {
+  double y[3], Jm[3][6];
+  lm_residual_jacobian(to_pose(H->R, H->t), x, *reinterpret_cast<const Mode*>(m), use_cov != 0, r, J ? Jm : nullptr,
+                       y);
+  if (J)
+    for (int i = 0; i < 3; ++i)
+      for (int a = 0; a < 6; ++a) J[6 * i + a] = Jm[i][a];
+}
+}

@@ -209,6 +209,11 @@ struct Hypothesis {
 // successful final attempt). Diagnostic only; never changes the draws.
 int generate_hypothesis(const FrameCtx& c, const AdaptState& s, const RansacParams& p, Rng& rng, Pose* out,
                         int* attempts, int64_t* tags = nullptr);
+// Checks 2-3 + Kabsch of one triplet: REJ_OK (transform in *out) or the tag.
+int check_triplet(const double cm[9], const double w[9], const RansacParams& p, Pose* out);
+// LM residual S (H x - mu) and Jacobian w.r.t. the left twist (omega, rho); J may be null.
+void lm_residual_jacobian(const Pose& H, const double x[3], const Mode& m, bool use_cov, double r[3],
+                          double J[3][6], double y[3]);
 // Eq. 5 accumulated per eta-sample batch: E = sum_b E_b (batches in order), E_b sequential.
 float energy(const FrameCtx& c, const AdaptState& s, const Pose& H, const std::vector<int>& samples, int eta);
 void draw_samples(uint64_t seed, int batch, int n_max, int eta, int G, std::vector<int>& out);

@@ -166,6 +166,8 @@ class Oracle:
             "or_depth_diff_images": (dbl, [P(flt), P(flt), C.c_int, C.c_int]),
             "or_raycast_depth": (None, [vp, P(Pose), P(Intrinsics), P(flt)]),
             "or_stage_seed": (u64, [u64, C.c_int]),
+            "or_check_triplet": (C.c_int, [P(dbl), P(dbl), P(RansacParams), P(Pose)]),
+            "or_lm_residual_jacobian": (None, [P(Pose), P(dbl), vp, C.c_int, P(dbl), P(dbl)]),
             "or_generation_stats": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(RansacParams), u64,
                                               P(Pose), dbl, P(C.c_int64), P(C.c_int), P(dbl), P(dbl)]),
             "or_energy": (C.c_int, [vp, vp, P(flt), P(C.c_uint8), P(Intrinsics), P(Pose), P(i32), C.c_int, P(flt)]),
@@ -304,6 +306,40 @@ class Oracle:
         if rc:
             raise RuntimeError(self.err())
         return list(out)
+
+    REJECTION_TAGS = ("OK", "NoModes", "ColourCheckFailed", "TooClose", "NotRigid", "DegenerateKabsch")
+
+    def generation_stats(self, forest, state, depth, rgb, k, params, seed, gt=None, radius=0.05):
+        """Per-attempt rejection-tag histogram of generate_hypothesis over all slots of one frame
+        ({tag: attempts}, slots ok, fraction of modes within `radius` of the true point, fraction
+        of moded grid pixels with such a mode)."""
+        tags = (C.c_int64 * 6)()
+        ok = C.c_int()
+        mf, pf = C.c_double(), C.c_double()
+        d = np.ascontiguousarray(depth, np.float32)
+        c = np.ascontiguousarray(rgb, np.uint8)
+        rc = self.lib.or_generation_stats(forest, state, _ptr(d, C.c_float), _ptr(c, C.c_uint8), C.byref(k),
+                                          C.byref(params), seed, C.byref(gt) if gt is not None else None, radius,
+                                          tags, C.byref(ok), C.byref(mf), C.byref(pf))
+        if rc:
+            raise RuntimeError(self.err())
+        return dict(zip(self.REJECTION_TAGS, list(tags))), ok.value, mf.value, pf.value
+
+    def check_triplet(self, cam, world, params):
+        cm = np.ascontiguousarray(cam, np.float64).reshape(9)
+        w = np.ascontiguousarray(world, np.float64).reshape(9)
+        out = Pose()
+        tag = self.lib.or_check_triplet(_ptr(cm, C.c_double), _ptr(w, C.c_double), C.byref(params), C.byref(out))
+        return self.REJECTION_TAGS[tag], out
+
+    def lm_residual_jacobian(self, H, x, mode, use_cov):
+        xx = np.ascontiguousarray(x, np.float64)
+        m = np.ascontiguousarray(mode, MODE_DTYPE)
+        r = np.zeros(3)
+        J = np.zeros(18)
+        self.lib.or_lm_residual_jacobian(C.byref(H), _ptr(xx, C.c_double), m.ctypes.data, int(use_cov),
+                                         _ptr(r, C.c_double), _ptr(J, C.c_double))
+        return r, J.reshape(3, 6)
 
     # ---- TSDF model ----
     def tsdf_create(self, origin, voxel, dims, trunc=None):

@@ -100,35 +100,29 @@ int generate_hypothesis(const FrameCtx& c, const AdaptState& s, const RansacPara
         w[3 * k + q] = static_cast<double>(mm[k]->mu[q]);
         cm[3 * k + q] = c.cam[3 * static_cast<size_t>(gi[k]) + q];
       }
-    static const int PA[3] = {0, 0, 1}, PB[3] = {1, 2, 2};
-    bool close = false, nonrigid = false;
-    double dw2[3], dc2[3];
-    for (int q = 0; q < 3; ++q) {
-      dw2[q] = d2_3(&w[3 * PA[q]], &w[3 * PB[q]]);
-      dc2[q] = d2_3(&cm[3 * PA[q]], &cm[3 * PB[q]]);
-      if (dw2[q] < p.min_sq_dist) close = true;
-    }
-    if (close) {
-      last = REJ_TOO_CLOSE;
-      if (tags) ++tags[REJ_TOO_CLOSE];
-      continue;
-    }
-    for (int q = 0; q < 3; ++q)
-      if (std::fabs(std::sqrt(dw2[q]) - std::sqrt(dc2[q])) > p.rigidity_tol) nonrigid = true;
-    if (nonrigid) {
-      last = REJ_NOT_RIGID;
-      if (tags) ++tags[REJ_NOT_RIGID];
-      continue;
-    }
-    if (!kabsch(cm, w, 3, out)) {
-      last = REJ_DEGENERATE;
-      if (tags) ++tags[REJ_DEGENERATE];
-      continue;
-    }
-    if (tags) ++tags[REJ_OK];
-    return REJ_OK;
+    last = check_triplet(cm, w, p, out);
+    if (tags) ++tags[last];
+    if (last == REJ_OK) return REJ_OK;
   }
   return last;
+}
+
+// Checks 2-3 and Kabsch of one colour-checked triplet: camera points cm
+// and world points w (3 x 3, row per point) -> REJ_OK with the transform, or the tag.
+int check_triplet(const double cm[9], const double w[9], const RansacParams& p, Pose* out) {
+  static const int PA[3] = {0, 0, 1}, PB[3] = {1, 2, 2};
+  bool close = false;
+  double dw2[3], dc2[3];
+  for (int q = 0; q < 3; ++q) {
+    dw2[q] = d2_3(&w[3 * PA[q]], &w[3 * PB[q]]);
+    dc2[q] = d2_3(&cm[3 * PA[q]], &cm[3 * PB[q]]);
+    if (dw2[q] < p.min_sq_dist) close = true;
+  }
+  if (close) return REJ_TOO_CLOSE;
+  for (int q = 0; q < 3; ++q)
+    if (std::fabs(std::sqrt(dw2[q]) - std::sqrt(dc2[q])) > p.rigidity_tol) return REJ_NOT_RIGID;
+  if (!kabsch(cm, w, 3, out)) return REJ_DEGENERATE;
+  return REJ_OK;
 }
 
 void draw_samples(uint64_t seed, int batch, int n_max, int eta, int G, std::vector<int>& out) {
@@ -192,25 +186,25 @@ struct LmSample {
   double x[3];
 };
 
-// Residual and Jacobian for one sample at pose H (left perturbation, twist = (omega, rho)).
-inline void lm_term(const Pose& H, const LmSample& s, bool use_cov, double acc[kAcc], bool with_jac) {
-  double y[3];
-  transform_point(H, s.x, y);
-  const double d[3] = {y[0] - s.m->mu[0], y[1] - s.m->mu[1], y[2] - s.m->mu[2]};
+}  // namespace
+
+// Residual r = S (H x - mu) and its Jacobian J = dr/d(delta) for H <- exp(delta) H (left
+// perturbation, twist = (omega, rho)); S = Sigma^-1/2 or I. Returns y = H x.
+void lm_residual_jacobian(const Pose& H, const double x[3], const Mode& m, bool use_cov, double r[3],
+                          double J[3][6], double y[3]) {
+  transform_point(H, x, y);
+  const double d[3] = {y[0] - m.mu[0], y[1] - m.mu[1], y[2] - m.mu[2]};
   double S[9];
   if (use_cov) {
-    const float* q = s.m->isqrt;
+    const float* q = m.isqrt;
     S[0] = q[0]; S[1] = q[1]; S[2] = q[2];
     S[3] = q[1]; S[4] = q[3]; S[5] = q[4];
     S[6] = q[2]; S[7] = q[4]; S[8] = q[5];
   } else {
     for (int i = 0; i < 9; ++i) S[i] = (i % 4 == 0) ? 1.0 : 0.0;
   }
-  double r[3];
   for (int i = 0; i < 3; ++i) r[i] = (S[3 * i + 0] * d[0] + S[3 * i + 1] * d[1]) + S[3 * i + 2] * d[2];
-  acc[27] = acc[27] + ((r[0] * r[0] + r[1] * r[1]) + r[2] * r[2]);
-  if (!with_jac) return;
-  double J[3][6];
+  if (!J) return;
   for (int i = 0; i < 3; ++i) {
     J[i][0] = S[3 * i + 1] * (-y[2]) + S[3 * i + 2] * y[1];
     J[i][1] = S[3 * i + 0] * y[2] + S[3 * i + 2] * (-y[0]);
@@ -219,6 +213,15 @@ inline void lm_term(const Pose& H, const LmSample& s, bool use_cov, double acc[k
     J[i][4] = S[3 * i + 1];
     J[i][5] = S[3 * i + 2];
   }
+}
+
+namespace {
+// One sample's contribution to the normal equations (or only to sum r^2).
+inline void lm_term(const Pose& H, const LmSample& s, bool use_cov, double acc[kAcc], bool with_jac) {
+  double y[3], r[3], J[3][6];
+  lm_residual_jacobian(H, s.x, *s.m, use_cov, r, with_jac ? J : nullptr, y);
+  acc[27] = acc[27] + ((r[0] * r[0] + r[1] * r[1]) + r[2] * r[2]);
+  if (!with_jac) return;
   int k = 0;
   for (int a = 0; a < 6; ++a)
     for (int b = a; b < 6; ++b, ++k) acc[k] = acc[k] + ((J[0][a] * J[0][b] + J[1][a] * J[1][b]) + J[2][a] * J[2][b]);

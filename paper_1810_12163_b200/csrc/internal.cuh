@@ -220,4 +220,8 @@ scr_status run_ransac_debug(scr_scene s, const scr_ransac_params* p, uint64_t se
                             float* surv_energy, int* n_surv);
 scr_status run_icp_debug(scr_scene s, const scr_pose* init, scr_pose* out, int* conv, double* rms, double* inl,
                          double* score);
+// Frames handed to the ABI: non-null planes (SCR_E_ARG) whose width x height equal the
+// scene's intrinsics (SCR_E_DIMENSION_MISMATCH, core.hpp:57).
+scr_status check_frames(const scr_scene_s* s, const scr_frame* frames, int n);
+
 }  // namespace scr

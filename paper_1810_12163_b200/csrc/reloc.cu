@@ -36,6 +36,9 @@ struct GenParams {
   int leaf_base[kMaxTrees];
 };
 
+// Outcome of one generation attempt: pass, or its rejection tag.
+enum { kAttPass = 0, kAttNoModes = 1, kAttColour = 2, kAttTooClose = 3, kAttNotRigid = 4, kAttDegenerate = 5 };
+
 struct FrameRefs {  // per-batch views of the packed frames
   const int* fidx;       // active index -> workspace slot
   const int* gcount;
@@ -226,7 +229,7 @@ SCR_DEV bool kabsch_clearly_regular(const double cm[9], const double w[9]) {
 
 SCR_DEV bool distance_checks_f64(double min_sq_dist, double rigidity_tol, const int4* grec, const FrameGeom& g,
                                  const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1, int m2,
-                                 double* cm_out, double* w_out, bool* regular = nullptr) {
+                                 double* cm_out, double* w_out, bool* regular = nullptr, int* why = nullptr) {
   const float4 w0 = geom[m0].q0, w1 = geom[m1].q0, w2 = geom[m2].q0;
   const int4 r0 = grec[2 * g0], r1 = grec[2 * g1], r2 = grec[2 * g2];
   double w[9] = {w0.x, w0.y, w0.z, w1.x, w1.y, w1.z, w2.x, w2.y, w2.z};
@@ -245,10 +248,16 @@ SCR_DEV bool distance_checks_f64(double min_sq_dist, double rigidity_tol, const 
     dc2[q] = (bx * bx + by * by) + bz * bz;
     if (dw2[q] < min_sq_dist) close = true;
   }
-  if (close) return false;
+  if (close) {
+    if (why) *why = kAttTooClose;
+    return false;
+  }
 #pragma unroll
   for (int q = 0; q < 3; ++q)
-    if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > rigidity_tol) return false;
+    if (fabs(sqrt(dw2[q]) - sqrt(dc2[q])) > rigidity_tol) {
+      if (why) *why = kAttNotRigid;
+      return false;
+    }
   if (cm_out) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
@@ -269,8 +278,9 @@ SCR_DEV bool geometry_exact(double min_sq_dist, double rigidity_tol, const int4*
 
 // One generation attempt on the exact sequential path (draw order A1/A7):
 // draws pixel, mode, pixel, mode, pixel, mode, colour-pair index from the slot stream with
-// rejection sampling, returns whether the attempt reached the colour check and passed it.
-SCR_DEV bool attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, const PredView& pv,
+// rejection sampling; returns kAttPass if the attempt reached the colour check and passed it,
+// else its rejection tag (kAttNoModes, kAttColour).
+SCR_DEV int attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, const PredView& pv,
                            const int* s_lbase, const uint64_t* s_m, size_t fbase, uint64_t G,
                            uint64_t mG, uint64_t tG, bool fast, int& g0, int& g1, int& g2, int& m0, int& m1,
                            int& m2) {
@@ -282,19 +292,19 @@ SCR_DEV bool attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, c
   A0 = fr.grec[2 * (fbase + g0)];
   L0 = fr.gleaf[2 * (fbase + g0) + 1];
   const int nm0 = fast ? (static_cast<uint32_t>(A0.z) >> 24) : fr.gnm[fbase + g0];
-  if (nm0 <= 0) return false;
+  if (nm0 <= 0) return kAttNoModes;
   p0 = static_cast<int>(draw_exact_lazy(rng, static_cast<uint64_t>(nm0), s_m[nm0]));
   g1 = static_cast<int>(draw_exact(rng, G, mG, tG));
   A1 = fr.grec[2 * (fbase + g1)];
   L1 = fr.gleaf[2 * (fbase + g1) + 1];
   const int nm1 = fast ? (static_cast<uint32_t>(A1.z) >> 24) : fr.gnm[fbase + g1];
-  if (nm1 <= 0) return false;
+  if (nm1 <= 0) return kAttNoModes;
   p1 = static_cast<int>(draw_exact_lazy(rng, static_cast<uint64_t>(nm1), s_m[nm1]));
   g2 = static_cast<int>(draw_exact(rng, G, mG, tG));
   A2 = fr.grec[2 * (fbase + g2)];
   L2 = fr.gleaf[2 * (fbase + g2) + 1];
   const int nm2 = fast ? (static_cast<uint32_t>(A2.z) >> 24) : fr.gnm[fbase + g2];
-  if (nm2 <= 0) return false;
+  if (nm2 <= 0) return kAttNoModes;
   p2 = static_cast<int>(draw_exact_lazy(rng, static_cast<uint64_t>(nm2), s_m[nm2]));
   cc = static_cast<int>(draw_exact(rng, 3, m3, t3));
   if (fast) {
@@ -307,7 +317,7 @@ SCR_DEV bool attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, c
     m2 = mode_index(fr, pv.count, fbase + g2, p2);
   }
   const uint32_t col = static_cast<uint32_t>(cc == 0 ? A0.z : (cc == 1 ? A1.z : A2.z));
-  return colour_ok(col, pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)], gp.colour_thresh);
+  return colour_ok(col, pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)], gp.colour_thresh) ? kAttPass : kAttColour;
 }
 
 // Per-warp queue of colour-check survivors, evaluated 32 at a time at full SIMD width.
@@ -456,7 +466,7 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
         }
       } else {  // > 5 trees or 32-bit leaf ids: modes through the slot tables
         int g0, g1, g2, m0, m1, m2;
-        if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2)) {
+        if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2) == kAttPass) {
           push = true;
           c.slot = slot | kCandResolved;
           c.owner_att = lane | (it << 5);
@@ -659,7 +669,7 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
   for (; it <= att; ++it)  // replay through the recorded attempt
     attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2);
   for (; it < gp.max_iters && !ok; ++it) {
-    if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2) &&
+    if (attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, fast, g0, g1, g2, m0, m1, m2) == kAttPass &&
         geometry_prefilter(gp.min_sq_dist, gp.rigidity_tol, grec, g, ifx, ify, pv.geom, g0, g1, g2, m0, m1, m2))
       ok = geometry_exact(gp.min_sq_dist, gp.rigidity_tol, grec, g, pv.geom, g0, g1, g2, m0, m1, m2, &T);
   }
@@ -670,6 +680,60 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
   hok[out] = ok ? 1 : 0;
   hiters[out] = it;  // ok: the passing attempt + 1; otherwise max_iters
   if (work) atomicAdd(&work[W_GEN_ATTEMPTS], static_cast<unsigned long long>(it - (att + 1)));
+}
+
+// Generation diagnostics (scr_debug_generation_stats): thread per slot of one frame runs
+// generate_hypothesis on the exact sequential path and histograms the outcome of every
+// attempt by rejection tag (NoModes, ColourCheckFailed, TooClose, NotRigid,
+// DegenerateKabsch; tag 0 counts the successful final attempts). Not on the hot path.
+__global__ void k_gen_stats(GenParams gp, FrameGeom g, FrameRefs fr, PredView pv, uint64_t seed,
+                            unsigned long long* __restrict__ tags, int* __restrict__ slots_ok) {
+  __shared__ uint64_t s_m[kMaxModeUnion + 1];
+  __shared__ int s_lbase[kMaxTrees];
+  __shared__ unsigned long long s_tag[6];
+  for (int i = threadIdx.x; i <= kMaxModeUnion; i += blockDim.x) s_m[i] = barrett_m(i ? static_cast<uint64_t>(i) : 1);
+  if (threadIdx.x < kMaxTrees) s_lbase[threadIdx.x] = gp.leaf_base[threadIdx.x];
+  if (threadIdx.x < 6) s_tag[threadIdx.x] = 0;
+  __syncthreads();
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = fr.fidx[0];
+  const size_t fbase = static_cast<size_t>(f) * fr.gmax;
+  const uint64_t G = static_cast<uint64_t>(fr.gcount[f]);
+  unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
+  bool ok = false;
+  if (slot < gp.nmax && G > 0) {
+    const uint64_t mG = barrett_m(G), tG = mod_barrett(0 - G, G, mG);
+    const int4* grec = fr.grec + 2 * fbase;
+    Rng rng = rng_stream(seed, static_cast<uint64_t>(slot));
+    for (int it = 0; it < gp.max_iters && !ok; ++it) {
+      int g0, g1, g2, m0, m1, m2;
+      const int r = attempt_exact(rng, gp, fr, pv, s_lbase, s_m, fbase, G, mG, tG, gp.fast != 0, g0, g1, g2, m0, m1,
+                                  m2);
+      if (r != kAttPass) {
+        ++cnt[r];
+        continue;
+      }
+      double cm[9], w[9];
+      int why = 0;
+      if (!distance_checks_f64(gp.min_sq_dist, gp.rigidity_tol, grec, g, pv.geom, g0, g1, g2, m0, m1, m2, cm, w,
+                               nullptr, &why)) {
+        ++cnt[why];
+        continue;
+      }
+      Pose T;
+      if (!kabsch3_cold(cm, w, &T)) {
+        ++cnt[kAttDegenerate];
+        continue;
+      }
+      ++cnt[kAttPass];
+      ok = true;
+    }
+  }
+  for (int i = 0; i < 6; ++i)
+    if (cnt[i]) atomicAdd(&s_tag[i], cnt[i]);
+  if (ok) atomicAdd(slots_ok, 1);
+  __syncthreads();
+  if (threadIdx.x < 6 && s_tag[threadIdx.x]) atomicAdd(&tags[threadIdx.x], s_tag[threadIdx.x]);
 }
 
 // Sample batch k of frame a: eta draws of uniform_int(G) from Rng::stream(seed, nmax + k).
@@ -2431,10 +2495,9 @@ scr_status scr_cascade_batch(scr_scene s, const scr_frame* frames, int n, const 
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  SCR_TRY(check_frames(s, frames, n));
   for (int b0 = 0; b0 < n; b0 += s->ws.cap) {
     const int nb = std::min(s->ws.cap, n - b0);
-    for (int i = 0; i < nb; ++i)
-      if (!frames[b0 + i].depth || !frames[b0 + i].rgb) return SCR_E_ARG;
     {  // this call's frames, contiguous on the device's copy stream (staging is free: the
        // previous call on this lane synchronised its stream)
       std::lock_guard<std::mutex> lk(s->dev->copy_mu);
@@ -2469,6 +2532,10 @@ scr_status scr_cascade_frameset(scr_scene s, scr_frameset fs, const int32_t* idx
     set_error("relocalise: no scene model set (scr_scene_set_analytic_model)");
     return SCR_E_ARG;
   }
+  if (fs->scene != s && fs->scene != s->parent) {
+    set_error("scr_cascade_frameset: the frame set belongs to another scene");
+    return SCR_E_ARG;
+  }
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   for (int i = 0; i < n; ++i)
@@ -2488,6 +2555,7 @@ scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_pa
                             int32_t* gen_slots, scr_pose* gen_poses, int* n_gen, int32_t* surv_slots,
                             scr_pose* surv_poses, float* surv_energy, int* n_surv) {
   if (!s || !f || !p || !n_gen || !n_surv) return SCR_E_ARG;
+  SCR_TRY(check_frames(s, f, 1));
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
@@ -2551,9 +2619,46 @@ scr_status scr_debug_generation_mode(scr_scene s, int mode) {
   return SCR_OK;
 }
 
+scr_status scr_debug_generation_stats(scr_scene s, const scr_frame* f, const scr_ransac_params* p, uint64_t seed,
+                                      int64_t* tags, int* slots_ok) {
+  if (!s || !f || !f->depth || !f->rgb || !p || !tags || !slots_ok || p->n_max <= 0 || p->n_max > 4096 ||
+      p->max_gen_iters <= 0) {
+    set_error("scr_debug_generation_stats: bad argument");
+    return SCR_E_ARG;
+  }
+  SCR_TRY(check_frames(s, f, 1));
+  SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  SCR_TRY(refresh_lane(s));
+  const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
+  SCR_CUDA(cudaMemcpyAsync(s->ws.depth, f->depth, WH * sizeof(float), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->ws.rgb, f->rgb, WH * 3, cudaMemcpyHostToDevice, s->stream));
+  SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
+  const int zero = 0;
+  SCR_CUDA(cudaMemcpyAsync(s->ws.fidx, &zero, sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  GenParams gp{p->max_gen_iters, p->n_max, p->min_sq_dist, p->colour_thresh, p->rigidity_tol,
+               (s->T <= 5 && s->leaves16) ? 1 : 0, 0, {0}};
+  for (int t = 0; t < s->T && t < kMaxTrees; ++t) gp.leaf_base[t] = s->leaf_base[t];
+  unsigned long long* d_tags = nullptr;
+  SCR_CUDA(cudaMalloc(&d_tags, 6 * sizeof(unsigned long long) + sizeof(int)));
+  int* d_ok = reinterpret_cast<int*>(d_tags + 6);
+  SCR_CUDA(cudaMemsetAsync(d_tags, 0, 6 * sizeof(unsigned long long) + sizeof(int), s->stream));
+  k_gen_stats<<<(p->n_max + 127) / 128, 128, 0, s->stream>>>(gp, s->geom, frame_refs(s), s->pred_view(), seed,
+                                                              d_tags, d_ok);
+  unsigned long long h[6];
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, d_tags, sizeof(h), cudaMemcpyDeviceToHost, s->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(slots_ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, s->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  cudaFree(d_tags);
+  SCR_CUDA(e);
+  for (int i = 0; i < 6; ++i) tags[i] = static_cast<int64_t>(h[i]);
+  return SCR_OK;
+}
+
 scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, scr_pose* out, int* converged,
                          double* rms, double* inlier_frac, double* score) {
   if (!s || !f || !init || !(s->d_prims || s->tsdf_model)) return SCR_E_ARG;
+  SCR_TRY(check_frames(s, f, 1));
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;

@@ -1049,10 +1049,31 @@ scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_
   return SCR_OK;
 }
 
+scr_status check_frames(const scr_scene_s* s, const scr_frame* frames, int n) {
+  if (n > 0 && !frames) {
+    set_error("null frame array");
+    return SCR_E_ARG;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (!frames[i].depth || !frames[i].rgb) {
+      set_error("frame without depth or colour plane");
+      return SCR_E_ARG;
+    }
+    if (frames[i].width != s->k.width || frames[i].height != s->k.height) {
+      set_error("frame " + std::to_string(i) + " is " + std::to_string(frames[i].width) + "x" +
+                std::to_string(frames[i].height) + ", the scene's intrinsics are " + std::to_string(s->k.width) + "x" +
+                std::to_string(s->k.height));
+      return SCR_E_DIMENSION_MISMATCH;
+    }
+  }
+  return SCR_OK;
+}
+
 }  // namespace scr
 
 namespace {
 scr_status upload_frames(scr_scene s, const scr_frame* frames, int n) {
+  SCR_TRY(check_frames(s, frames, n));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
   for (int i = 0; i < n; ++i) {
     if (!frames[i].depth || !frames[i].rgb) {
@@ -1353,6 +1374,7 @@ static scr_status scr_predictions_import_impl(scr_scene s, const void* src) {
 
 scr_status scr_debug_leaves(scr_scene s, const scr_frame* f, int32_t* grid_px, int32_t* leaves, int* n_grid) {
   if (!s || !f || !n_grid) return SCR_E_ARG;
+  SCR_TRY(check_frames(s, f, 1));
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   SCR_TRY(upload_frames(s, f, 1));
@@ -1373,6 +1395,7 @@ scr_status scr_debug_leaves(scr_scene s, const scr_frame* f, int32_t* grid_px, i
 
 scr_status scr_debug_features(scr_scene s, const scr_frame* f, const int32_t* px, int n, float* out) {
   if (!s || !f || !px || !out || n < 0) return SCR_E_ARG;
+  SCR_TRY(check_frames(s, f, 1));
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   SCR_TRY(upload_frames(s, f, 1));
@@ -1433,6 +1456,7 @@ void scr_frameset_destroy(scr_frameset fs) {
 scr_status scr_frameset_upload(scr_frameset fs, int first, const scr_frame* frames, int n) {
   if (!fs || first < 0 || n < 0 || first + n > fs->cap) return SCR_E_ARG;
   scr_scene s = fs->scene;
+  SCR_TRY(check_frames(s, frames, n));
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
   for (int i = 0; i < n; ++i) {

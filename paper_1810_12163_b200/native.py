@@ -25,7 +25,8 @@ class Pose(C.Structure):
 
 
 class Frame(C.Structure):
-    _fields_ = [("depth", C.c_void_p), ("rgb", C.c_void_p), ("pose_reliable", C.c_int32), ("pad", C.c_int32)]
+    _fields_ = [("depth", C.c_void_p), ("rgb", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32),
+                ("pose_reliable", C.c_int32), ("pad", C.c_int32)]
 
 
 class ForestParams(C.Structure):
@@ -148,6 +149,7 @@ SIGNATURES = {
     "scr_debug_ransac": (C.c_int, [_vp, _P(Frame), _P(RansacParams), _u64, _P(_i32), _P(Pose), _P(C.c_int),
                                    _P(_i32), _P(Pose), _P(_flt), _P(C.c_int)]),
     "scr_debug_generation_mode": (C.c_int, [_vp, C.c_int]),
+    "scr_debug_generation_stats": (C.c_int, [_vp, _P(Frame), _P(RansacParams), _u64, _P(_i64), _P(C.c_int)]),
     "scr_debug_icp": (C.c_int, [_vp, _P(Frame), _P(Pose), _P(Pose), _P(C.c_int), _P(_dbl), _P(_dbl), _P(_dbl)]),
     "scr_kernel_launches": (_i64, [_vp]),
     "scr_profile_enable": (C.c_int, [_vp, C.c_int]),

@@ -125,15 +125,33 @@ class Device:
             self.handle = None
 
 
-def _frames(depths, rgbs, reliable=1):
+def _frames(depths, rgbs, reliable=1, k: N.Intrinsics | None = None):
+    """C frame views of (H, W) depth and (H, W, 3) colour arrays. Shapes that disagree with each
+    other or with the scene's intrinsics raise DimensionMismatch (core.hpp:57) before any
+    native call reads them."""
+    if len(depths) != len(rgbs):
+        raise N.DimensionMismatch(f"{len(depths)} depth images but {len(rgbs)} colour images")
     depths = [np.ascontiguousarray(d, np.float32) for d in depths]
     rgbs = [np.ascontiguousarray(c, np.uint8) for c in rgbs]
     arr = (N.Frame * len(depths))()
     for i, (d, c) in enumerate(zip(depths, rgbs)):
+        if d.ndim != 2 or c.shape != d.shape + (3,):
+            raise N.DimensionMismatch(f"frame {i}: depth {d.shape} and colour {c.shape} are not (H, W) / (H, W, 3)")
+        if k is not None and d.shape != (k.height, k.width):
+            raise N.DimensionMismatch(f"frame {i} is {d.shape[1]}x{d.shape[0]}, the scene's intrinsics are "
+                                      f"{k.width}x{k.height}")
         arr[i].depth = d.ctypes.data
         arr[i].rgb = c.ctypes.data
+        arr[i].height, arr[i].width = d.shape
         arr[i].pose_reliable = reliable
     return arr, (depths, rgbs)  # keep buffers alive
+
+
+def _seeds(seeds, n: int) -> np.ndarray:
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    if sd.ndim != 1 or sd.size != n:
+        raise N.DimensionMismatch(f"{sd.size} seeds for {n} frames")
+    return sd
 
 
 class Scene:
@@ -219,12 +237,14 @@ class Scene:
 
     # ---- adaptation -------------------------------------------------------------------
     def integrate_frame(self, depth, rgb, pose, pose_reliable: bool = True):
-        arr, keep = _frames([depth], [rgb], 1 if pose_reliable else 0)
+        arr, keep = _frames([depth], [rgb], 1 if pose_reliable else 0, self.k)
         p = to_pose(pose)
         N.check(self.lib.scr_train(self.handle, arr, C.byref(p)), "integrate_frame")
 
     def integrate_frames(self, depths, rgbs, poses):
-        arr, keep = _frames(depths, rgbs)
+        if len(poses) != len(depths):
+            raise N.DimensionMismatch(f"{len(poses)} poses for {len(depths)} frames")
+        arr, keep = _frames(depths, rgbs, 1, self.k)
         ps = (N.Pose * len(poses))(*[to_pose(p) for p in poses])
         N.check(self.lib.scr_train_batch(self.handle, arr, ps, len(poses)), "integrate_frame")
 
@@ -240,10 +260,10 @@ class Scene:
 
     # ---- relocalisation -----------------------------------------------------------------
     def relocalise_batch(self, depths, rgbs, profile, mode, seeds) -> list[N.Result]:
-        arr, keep = _frames(depths, rgbs)
+        arr, keep = _frames(depths, rgbs, 1, self.k)
         n = len(depths)
         p = profile if isinstance(profile, N.RansacParams) else ransac_params(profile)
-        sd = np.ascontiguousarray(seeds, np.uint64)
+        sd = _seeds(seeds, n)
         out = (N.Result * n)()
         m = MODES[mode] if isinstance(mode, str) else int(mode)
         N.check(self.lib.scr_relocalise_batch(self.handle, arr, n, C.byref(p), m, N.ptr(sd, C.c_uint64), out),
@@ -254,12 +274,12 @@ class Scene:
         return RelocalisationResult.from_c(self.relocalise_batch([depth], [rgb], profile, mode, [seed])[0])
 
     def run_cascade_batch(self, depths, rgbs, config: CascadeConfig, seeds) -> list[N.Result]:
-        arr, keep = _frames(depths, rgbs)
+        arr, keep = _frames(depths, rgbs, 1, self.k)
         n = len(depths)
         st = (N.RansacParams * len(config.stages))(*config.stages)
         md = np.asarray(config.modes, np.int32)
         th = np.asarray(list(config.thresholds) + [0.0], np.float64)
-        sd = np.ascontiguousarray(seeds, np.uint64)
+        sd = _seeds(seeds, n)
         out = (N.Result * n)()
         N.check(self.lib.scr_cascade_batch(self.handle, arr, n, st, N.ptr(md, C.c_int32), N.ptr(th, C.c_double),
                                            len(config.stages), N.ptr(sd, C.c_uint64), out), "run_cascade")
@@ -270,7 +290,7 @@ class Scene:
 
     # ---- parity hooks -----------------------------------------------------------------
     def debug_leaves(self, depth, rgb):
-        arr, keep = _frames([depth], [rgb])
+        arr, keep = _frames([depth], [rgb], 1, self.k)
         h, w = np.asarray(depth).shape
         gmax = ((w + 3) // 4) * ((h + 3) // 4)
         T = 8
@@ -283,7 +303,7 @@ class Scene:
         return px[:g], leaves[: g * self.trees].reshape(g, self.trees)
 
     def debug_features(self, depth, rgb, px):
-        arr, keep = _frames([depth], [rgb])
+        arr, keep = _frames([depth], [rgb], 1, self.k)
         px = np.ascontiguousarray(px, np.int32)
         out = np.zeros((px.size, 256), np.float32)
         N.check(self.lib.scr_debug_features(self.handle, arr, N.ptr(px, C.c_int32), px.size, N.ptr(out, C.c_float)),
@@ -323,7 +343,7 @@ class Scene:
         return out[: n.value], labels[: e.size]
 
     def debug_ransac(self, depth, rgb, params: N.RansacParams, seed: int):
-        arr, keep = _frames([depth], [rgb])
+        arr, keep = _frames([depth], [rgb], 1, self.k)
         nmax = params.n_max
         gs = np.zeros(nmax, np.int32)
         gp = (N.Pose * nmax)()
@@ -340,8 +360,20 @@ class Scene:
         """Test hook: 1 = every passing triplet goes through the exact suspect/continuation path."""
         N.check(self.lib.scr_debug_generation_mode(self.handle, int(mode)), "debug_generation_mode")
 
+    REJECTION_TAGS = ("OK", "NoModes", "ColourCheckFailed", "TooClose", "NotRigid", "DegenerateKabsch")
+
+    def debug_generation_stats(self, depth, rgb, params: N.RansacParams, seed: int):
+        """Per-attempt outcome histogram of hypothesis generation on one frame:
+        ({tag: attempts}, slots that generated a hypothesis)."""
+        arr, keep = _frames([depth], [rgb], 1, self.k)
+        tags = np.zeros(6, np.int64)
+        ok = C.c_int()
+        N.check(self.lib.scr_debug_generation_stats(self.handle, arr, C.byref(params), seed, N.ptr(tags, C.c_int64),
+                                                    C.byref(ok)), "generation_stats")
+        return dict(zip(self.REJECTION_TAGS, (int(v) for v in tags))), ok.value
+
     def debug_icp(self, depth, rgb, init):
-        arr, keep = _frames([depth], [rgb])
+        arr, keep = _frames([depth], [rgb], 1, self.k)
         p = to_pose(init)
         out = N.Pose()
         conv = C.c_int()
@@ -457,7 +489,7 @@ class FrameSet:
         N.check(self.lib.scr_frameset_render(self.handle, first, ps, len(poses)), "render_frame")
 
     def upload(self, depths, rgbs, first: int = 0):
-        arr, keep = _frames(depths, rgbs)
+        arr, keep = _frames(depths, rgbs, 1, self.scene.k)
         N.check(self.lib.scr_frameset_upload(self.handle, first, arr, len(depths)), "frameset_upload")
 
     def download(self, first: int, n: int):
@@ -469,6 +501,8 @@ class FrameSet:
 
     def train(self, idx: Iterable[int], poses):
         idx = np.ascontiguousarray(list(idx), np.int32)
+        if len(poses) != idx.size:
+            raise N.DimensionMismatch(f"{len(poses)} poses for {idx.size} frames")
         ps = (N.Pose * len(poses))(*[to_pose(p) for p in poses])
         N.check(self.lib.scr_train_frameset(self.scene.handle, self.handle, N.ptr(idx, C.c_int32), ps, idx.size),
                 "integrate_frame")
@@ -480,7 +514,7 @@ class FrameSet:
         st = (N.RansacParams * len(config.stages))(*config.stages)
         md = np.asarray(config.modes, np.int32)
         th = np.asarray(list(config.thresholds) + [0.0], np.float64)
-        sd = np.ascontiguousarray(seeds, np.uint64)
+        sd = _seeds(seeds, n)
         out = (N.Result * n)()
         N.check(self.lib.scr_cascade_frameset((scene or self.scene).handle, self.handle, N.ptr(idx, C.c_int32), n, st,
                                               N.ptr(md, C.c_int32), N.ptr(th, C.c_double), len(config.stages),

@@ -84,3 +84,27 @@ def test_malformed_forest_rejected_before_gpu(lib):
 
     blob = P.generate_random_forest(1, 3, 0.4, 1, 130)
     assert blob[:4] == b"SCRF" and len(blob) == 4 + 12 + 256 * 6 + 8 + 15 * 20
+
+
+def test_python_mirror_rejects_mismatched_frames_before_native_calls():
+    """wrong-sized frames and seed/pose counts raise DimensionMismatch in the
+    mirror (the C ABI also checks width/height against the scene, core.hpp:57)."""
+    import numpy as np
+    import pytest
+
+    import paper_1810_12163_b200 as P
+    from paper_1810_12163_b200 import native as N
+    from paper_1810_12163_b200.relocaliser import _frames, _seeds
+
+    k = P.intrinsics(64, 48)
+    d, c = np.zeros((48, 64), np.float32), np.zeros((48, 64, 3), np.uint8)
+    arr, _ = _frames([d], [c], 1, k)
+    assert (arr[0].width, arr[0].height) == (64, 48)
+    with pytest.raises(N.DimensionMismatch):
+        _frames([np.zeros((48, 32), np.float32)], [np.zeros((48, 32, 3), np.uint8)], 1, k)
+    with pytest.raises(N.DimensionMismatch):
+        _frames([d], [np.zeros((48, 64), np.uint8)], 1, k)
+    with pytest.raises(N.DimensionMismatch):
+        _frames([d, d], [c], 1, k)
+    with pytest.raises(N.DimensionMismatch):
+        _seeds([1, 2, 3], 2)
