@@ -279,13 +279,16 @@ RelocResult relocalise(const RansacParams& p, int mode, const Frame& fr, const F
     r.pose = hyps[0].pose;
     r.score = depth_diff_score(model, r.pose, fr);
   } else if (mode == MODE_ICP) {
+    // "If this fails, we discard the pose" (§3.2.4): a non-converged ICP gives no
+    // pose, exactly as ranked mode with one candidate (A11)
     const IcpResult ir = icp_refine(model, hyps[0].pose, fr);
-    r.has_pose = 1;
     if (ir.converged) {
+      r.has_pose = 1;
       r.pose = ir.pose;
       r.score = depth_diff_score(model, ir.pose, fr);
     } else {
-      r.pose = hyps[0].pose;
+      r.status = E_ALL_CANDIDATES_FAILED;
+      r.has_pose = 0;
       r.score = kInf;
     }
   } else {

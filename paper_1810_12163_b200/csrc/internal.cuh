@@ -4,6 +4,7 @@
 
 #include <string>
 #include <mutex>
+#include <shared_mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -117,13 +118,19 @@ struct Workspace {
   int* status = nullptr;      // [cap] frame-set indices for pack_frames
   int* hctr = nullptr;        // [2 * cap] per-frame generation slot counters, then suspect counts
   // reservoir insertion scratch (one frame)
-  unsigned* ins_cnt = nullptr;  // [L]
-  unsigned* ins_off = nullptr;  // [L + 1]
-  unsigned* ins_cur = nullptr;  // [L]
-  int* ins_item = nullptr;      // [gmax * T] packed g * T + t
-  int* ins_tgt = nullptr;       // [gmax * T]
-  int* ins_rank = nullptr;      // [gmax * T]
-  unsigned* ins_total = nullptr;
+  // reservoir insertion (K2): two stable radix sorts over the frame's gmax * T items
+  int* ins_start = nullptr;        // [L] first sorted position of a leaf's insertions
+  uint32_t* ins_key = nullptr;     // [items] leaf slot (padding: L)
+  uint32_t* ins_key_s = nullptr;   // sorted
+  int* ins_val = nullptr;          // [items] item = g * T + t
+  int* ins_item = nullptr;         // sorted items
+  int* ins_tgt = nullptr;          // [items] target entry per sorted position (-1: none)
+  uint64_t* ins_key2 = nullptr;    // [items] slot * kappa + target (padding: L * kappa)
+  uint64_t* ins_key2_s = nullptr;  // sorted
+  int* ins_val2 = nullptr;         // [items] sorted position
+  int* ins_pos2 = nullptr;         // positions in (slot, target) order
+  void* ins_tmp = nullptr;         // radix-sort scratch
+  size_t ins_tmp_bytes = 0;
 };
 
 }  // namespace scr
@@ -167,6 +174,11 @@ struct scr_scene_s {
   scr_scene_s* parent = nullptr;
   int lanes = 0;                      // live lanes forked from this scene
   cudaEvent_t published = nullptr;    // recorded after every update of shared state
+  // Readers (relocalisation on the scene or any of its lanes) hold this shared for a whole
+  // call, which returns only after its kernels finished; updates of what they read (RQS
+  // refresh, reset, loaded/imported/broadcast predictions, scene model) hold it exclusively,
+  // so no reader ever sees a half-written table or a freed model.
+  std::shared_mutex state_mu;
   int64_t launches = 0;
   scr::Profiler prof;
   scr::ForestView forest_view() const;
@@ -223,5 +235,31 @@ scr_status run_icp_debug(scr_scene s, const scr_pose* init, scr_pose* out, int* 
 // Frames handed to the ABI: non-null planes (SCR_E_ARG) whose width x height equal the
 // scene's intrinsics (SCR_E_DIMENSION_MISMATCH, core.hpp:57).
 scr_status check_frames(const scr_scene_s* s, const scr_frame* frames, int n);
+
+// RAII locks on the root scene's state (lanes lock their parent's).
+struct StateReadLock {
+  std::shared_mutex* m = nullptr;
+  explicit StateReadLock(scr_scene_s* s) {
+    if (s) {
+      m = &(s->parent ? s->parent : s)->state_mu;
+      m->lock_shared();
+    }
+  }
+  ~StateReadLock() {
+    if (m) m->unlock_shared();
+  }
+};
+struct StateWriteLock {
+  std::shared_mutex* m = nullptr;
+  explicit StateWriteLock(scr_scene_s* s) {
+    if (s) {
+      m = &s->state_mu;
+      m->lock();
+    }
+  }
+  ~StateWriteLock() {
+    if (m) m->unlock();
+  }
+};
 
 }  // namespace scr

@@ -2121,13 +2121,13 @@ __global__ void k_finalize(int nA, int mode, int cand_stride, const Pose* __rest
     r.has_pose = 1;
     memcpy(&r.pose, &cand[b], sizeof(scr_pose));
     r.score = icp_score[b];
-  } else if (mode == SCR_MODE_ICP) {
-    r.has_pose = 1;
+  } else if (mode == SCR_MODE_ICP) {  // a non-converged ICP discards the pose (§3.2.4)
     if (icp_conv[b]) {
+      r.has_pose = 1;
       memcpy(&r.pose, &icp_pose[b], sizeof(scr_pose));
       r.score = icp_score[b];
     } else {
-      memcpy(&r.pose, &cand[b], sizeof(scr_pose));
+      r.status = SCR_E_ALL_CANDIDATES_FAILED;
     }
   } else {
     int bi = -1;
@@ -2492,6 +2492,7 @@ scr_status scr_cascade_batch(scr_scene s, const scr_frame* frames, int n, const 
     set_error("relocalise: no scene model set (scr_scene_set_analytic_model)");
     return SCR_E_ARG;
   }
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
@@ -2536,6 +2537,7 @@ scr_status scr_cascade_frameset(scr_scene s, scr_frameset fs, const int32_t* idx
     set_error("scr_cascade_frameset: the frame set belongs to another scene");
     return SCR_E_ARG;
   }
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   for (int i = 0; i < n; ++i)
@@ -2556,6 +2558,7 @@ scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_pa
                             scr_pose* surv_poses, float* surv_energy, int* n_surv) {
   if (!s || !f || !p || !n_gen || !n_surv) return SCR_E_ARG;
   SCR_TRY(check_frames(s, f, 1));
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
@@ -2627,6 +2630,7 @@ scr_status scr_debug_generation_stats(scr_scene s, const scr_frame* f, const scr
     return SCR_E_ARG;
   }
   SCR_TRY(check_frames(s, f, 1));
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
@@ -2659,6 +2663,7 @@ scr_status scr_debug_icp(scr_scene s, const scr_frame* f, const scr_pose* init, 
                          double* rms, double* inlier_frac, double* score) {
   if (!s || !f || !init || !(s->d_prims || s->tsdf_model)) return SCR_E_ARG;
   SCR_TRY(check_frames(s, f, 1));
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;

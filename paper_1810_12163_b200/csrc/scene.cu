@@ -12,12 +12,14 @@
 //   cluster_reservoir (RQS)
 //   update_leaves_round_robin SPEC.md:366-374
 //   clear_adaptation
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -262,64 +264,48 @@ __global__ void k_features(ForestView fv, FrameGeom g, const uint2* __restrict__
 }
 
 // =============================== K2: reservoir insertion ================================
-// Sequential Algorithm R made parallel and bit-exact: insertions of
-// one frame are grouped per leaf (count / scan / place), each insertion's rank inside its
-// leaf is its row-major pixel order, n = seen + rank, and the counter-based draw
-// j = uniform_int(n + 1) from Rng::stream(adapt_seed, slot << 32 | n) picks the target.
-// Among insertions of one frame hitting the same target slot the highest rank wins,
-// exactly as the sequential loop would overwrite it.
-__global__ void k_ins_count(const int* __restrict__ gslot, int items, unsigned* __restrict__ cnt) {
+// Sequential Algorithm R made parallel and bit-exact. An insertion is an
+// item i = g * T + t (grid pixel g, tree t) aimed at leaf slot = gslot[i]; its rank inside
+// the leaf is its row-major pixel order among the frame's insertions into that leaf, n =
+// seen + rank, and the counter-based draw j = uniform_int(n + 1) from
+// Rng::stream(adapt_seed, slot << 32 | n) picks the target. Among insertions of one frame
+// hitting the same target the highest rank wins, exactly as the sequential loop would
+// overwrite it. Both orderings come from stable radix sorts (O(items) per frame, no scan of
+// a leaf's other insertions, no host round trip for the item count):
+//  1. sort (slot, item): inside a leaf, items stay in item = pixel order -> rank = position
+//     minus the leaf's first position;
+//  2. sort (slot * kappa + target, position): inside a run of one target the last entry has
+//     the highest rank -> it is the one written.
+__global__ void k_ins_keys(const int* __restrict__ gslot, const int* __restrict__ gcount, int T, int items_max,
+                           uint32_t pad_key, uint32_t* __restrict__ key, int* __restrict__ val) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < items) atomicAdd(&cnt[gslot[i]], 1u);
+  if (i >= items_max) return;
+  const int items = gcount[0] * T;
+  key[i] = i < items ? static_cast<uint32_t>(gslot[i]) : pad_key;
+  val[i] = i;
 }
 
-__global__ void __launch_bounds__(1024) k_scan(const unsigned* __restrict__ in, unsigned* __restrict__ out, int n,
-                                               unsigned* __restrict__ total) {
-  __shared__ unsigned s[1024];
-  const int per = (n + 1023) / 1024;
-  const int beg = threadIdx.x * per, end = min(n, beg + per);
-  unsigned acc = 0;
-  for (int i = beg; i < end; ++i) acc += in[i];
-  s[threadIdx.x] = acc;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    const unsigned v = threadIdx.x >= off ? s[threadIdx.x - off] : 0u;
-    __syncthreads();
-    s[threadIdx.x] += v;
-    __syncthreads();
-  }
-  unsigned run = threadIdx.x ? s[threadIdx.x - 1] : 0u;
-  for (int i = beg; i < end; ++i) {
-    out[i] = run;
-    run += in[i];
-  }
-  if (threadIdx.x == 1023) {
-    out[n] = s[1023];
-    if (total) *total = s[1023];
-  }
-}
-
-__global__ void k_ins_place(const int* __restrict__ gslot, int items, const unsigned* __restrict__ off,
-                            unsigned* __restrict__ cur, int* __restrict__ item_at) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= items) return;
-  const int slot = gslot[i];
-  item_at[off[slot] + atomicAdd(&cur[slot], 1u)] = i;
-}
-
-__global__ void k_ins_rank(const int* __restrict__ gslot, int T, const unsigned* __restrict__ total,
-                           const unsigned* __restrict__ off, const unsigned* __restrict__ cnt,
-                           const int* __restrict__ item_at, const uint32_t* __restrict__ seen, int kappa,
-                           uint64_t seed, int* __restrict__ tgt, int* __restrict__ rank) {
+// Leaf boundaries in sorted order: start[slot] = first position of the leaf's insertions.
+__global__ void k_ins_bounds(const uint32_t* __restrict__ key, const int* __restrict__ gcount, int T,
+                             int* __restrict__ start) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= static_cast<int>(*total)) return;
-  const int item = item_at[p];
-  const int g = item / T;
-  const int slot = gslot[item];
-  const unsigned s0 = off[slot], sn = cnt[slot];
-  int r = 0;
-  for (unsigned q = s0; q < s0 + sn; ++q) r += (item_at[q] / T) < g;
-  const uint32_t n = seen[slot] + static_cast<uint32_t>(r);
+  if (p >= gcount[0] * T) return;
+  if (p == 0 || key[p] != key[p - 1]) start[key[p]] = p;
+}
+
+__global__ void k_ins_target(const uint32_t* __restrict__ key, const int* __restrict__ gcount, int T,
+                             const int* __restrict__ start, const uint32_t* __restrict__ seen, int kappa,
+                             uint64_t seed, uint64_t pad_key2, int* __restrict__ tgt, uint64_t* __restrict__ key2,
+                             int* __restrict__ val2, int items_max) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= items_max) return;
+  if (p >= gcount[0] * T) {
+    key2[p] = pad_key2;
+    val2[p] = p;
+    return;
+  }
+  const uint32_t slot = key[p];
+  const uint32_t n = seen[slot] + static_cast<uint32_t>(p - start[slot]);
   int target;
   if (n < static_cast<uint32_t>(kappa)) {
     target = static_cast<int>(n);
@@ -329,25 +315,28 @@ __global__ void k_ins_rank(const int* __restrict__ gslot, int T, const unsigned*
     target = j < static_cast<uint64_t>(kappa) ? static_cast<int>(j) : -1;
   }
   tgt[p] = target;
-  rank[p] = r;
+  key2[p] = target >= 0 ? static_cast<uint64_t>(slot) * static_cast<uint64_t>(kappa) + static_cast<uint64_t>(target)
+                        : pad_key2;
+  val2[p] = p;
 }
 
-__global__ void k_ins_commit(const int* __restrict__ gslot, int T, const unsigned* __restrict__ total,
-                             const unsigned* __restrict__ off, const unsigned* __restrict__ cnt,
-                             const int* __restrict__ item_at, const int* __restrict__ tgt,
-                             const int* __restrict__ rank, const int* __restrict__ gpx, const uint2* __restrict__ tex,
-                             FrameGeom g, Pose pose, int kappa, scr_entry* __restrict__ entries,
+__global__ void k_ins_commit(const uint32_t* __restrict__ key, const int* __restrict__ item_at,
+                             const int* __restrict__ gcount, int T, const int* __restrict__ start,
+                             const uint64_t* __restrict__ key2, const int* __restrict__ pos2,
+                             const int* __restrict__ tgt, const int* __restrict__ gpx, const uint2* __restrict__ tex,
+                             FrameGeom g, Pose pose, int kappa, uint64_t pad_key2, scr_entry* __restrict__ entries,
                              uint32_t* __restrict__ seen) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= static_cast<int>(*total)) return;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int items = gcount[0] * T;
+  if (q >= items) return;
+  // seen += insertions of the leaf (one writer per leaf: its last position in sort 1)
+  if (q == items - 1 || key[q + 1] != key[q]) seen[key[q]] += static_cast<uint32_t>(q - start[key[q]] + 1);
+  const uint64_t k2 = key2[q];
+  if (k2 == pad_key2) return;                         // no target (or padding)
+  if (q + 1 < items && key2[q + 1] == k2) return;     // a later insertion overwrites this target
+  const int p = pos2[q];
+  const uint32_t slot = key[p];
   const int item = item_at[p];
-  const int slot = gslot[item];
-  const unsigned s0 = off[slot], sn = cnt[slot];
-  const int my_t = tgt[p], my_r = rank[p];
-  if (my_r == 0) seen[slot] += sn;  // one writer per leaf; seen was read by k_ins_rank
-  if (my_t < 0) return;
-  for (unsigned q = s0; q < s0 + sn; ++q)
-    if (tgt[q] == my_t && rank[q] > my_r) return;  // a later insertion overwrites this one
   const int gidx = item / T;
   const int px = gpx[gidx];
   const int x = px & 0xffff, y = px >> 16;
@@ -365,7 +354,7 @@ __global__ void k_ins_commit(const int* __restrict__ gslot, int T, const unsigne
   e.g = static_cast<uint8_t>((c.y >> 8) & 255u);
   e.b = static_cast<uint8_t>((c.y >> 16) & 255u);
   e.pad = 0;
-  entries[static_cast<size_t>(slot) * kappa + my_t] = e;
+  entries[static_cast<size_t>(slot) * kappa + tgt[p]] = e;
 }
 
 // =============================== K3: Really Quick Shift ==================================
@@ -420,36 +409,62 @@ __global__ void __launch_bounds__(256) k_rqs(const scr_entry* __restrict__ entri
   }
   if (threadIdx.x == 0) nroots = 0;
   __syncthreads();
-  // density
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float xi = sx[i], yi = sy[i], zi = sz[i];
-    double acc = 0.0;
+  // density: each thread owns two rows (i0, i0 + blockDim) so that every j loaded from
+  // shared memory serves two independent f64 sums (each still accumulated in j order)
+  for (int i0 = threadIdx.x; i0 < n; i0 += 2 * blockDim.x) {
+    const int i1 = i0 + blockDim.x;
+    const bool two = i1 < n;
+    const float x0 = sx[i0], y0 = sy[i0], z0 = sz[i0];
+    const float x1 = two ? sx[i1] : x0, y1 = two ? sy[i1] : y0, z1 = two ? sz[i1] : z0;
+    double acc0 = 0.0, acc1 = 0.0;
     for (int j = 0; j < n; ++j) {
-      const float dx = __fsub_rn(xi, sx[j]), dy = __fsub_rn(yi, sy[j]), dz = __fsub_rn(zi, sz[j]);
-      const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-      acc = acc + static_cast<double>(det_expf(__fmul_rn(d2, rp.c)));
+      const float xj = sx[j], yj = sy[j], zj = sz[j];
+      const float ax = __fsub_rn(x0, xj), ay = __fsub_rn(y0, yj), az = __fsub_rn(z0, zj);
+      const float bx = __fsub_rn(x1, xj), by = __fsub_rn(y1, yj), bz = __fsub_rn(z1, zj);
+      const float da = __fmaf_rn(az, az, __fmaf_rn(ay, ay, __fmul_rn(ax, ax)));
+      const float db = __fmaf_rn(bz, bz, __fmaf_rn(by, by, __fmul_rn(bx, bx)));
+      acc0 = acc0 + static_cast<double>(det_expf(__fmul_rn(da, rp.c)));
+      acc1 = acc1 + static_cast<double>(det_expf(__fmul_rn(db, rp.c)));
     }
-    rho[i] = acc;
+    rho[i0] = acc0;
+    if (two) rho[i1] = acc1;
   }
   __syncthreads();
-  // link
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float xi = sx[i], yi = sy[i], zi = sz[i];
-    const double ri = rho[i];
-    float best = __int_as_float(0x7f800000);
-    int bj = -1;
+  // link: nearest strictly-higher-density point within tau (ties: lower index), two rows
+  // per thread as above
+  for (int i0 = threadIdx.x; i0 < n; i0 += 2 * blockDim.x) {
+    const int i1 = i0 + blockDim.x;
+    const bool two = i1 < n;
+    const float x0 = sx[i0], y0 = sy[i0], z0 = sz[i0];
+    const float x1 = two ? sx[i1] : x0, y1 = two ? sy[i1] : y0, z1 = two ? sz[i1] : z0;
+    const double r0 = rho[i0], r1 = two ? rho[i1] : r0;
+    float best0 = __int_as_float(0x7f800000), best1 = best0;
+    int bj0 = -1, bj1 = -1;
     for (int j = 0; j < n; ++j) {
-      if (j == i) continue;
       const double rj = rho[j];
-      if (!(rj > ri || (rj == ri && j < i))) continue;
-      const float dx = __fsub_rn(xi, sx[j]), dy = __fsub_rn(yi, sy[j]), dz = __fsub_rn(zi, sz[j]);
-      const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-      if (d2 <= rp.tau2 && d2 < best) {
-        best = d2;
-        bj = j;
+      const bool up0 = j != i0 && (rj > r0 || (rj == r0 && j < i0));
+      const bool up1 = j != i1 && (rj > r1 || (rj == r1 && j < i1));
+      if (!(up0 || up1)) continue;
+      const float xj = sx[j], yj = sy[j], zj = sz[j];
+      if (up0) {
+        const float dx = __fsub_rn(x0, xj), dy = __fsub_rn(y0, yj), dz = __fsub_rn(z0, zj);
+        const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+        if (d2 <= rp.tau2 && d2 < best0) {
+          best0 = d2;
+          bj0 = j;
+        }
+      }
+      if (up1) {
+        const float dx = __fsub_rn(x1, xj), dy = __fsub_rn(y1, yj), dz = __fsub_rn(z1, zj);
+        const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+        if (d2 <= rp.tau2 && d2 < best1) {
+          best1 = d2;
+          bj1 = j;
+        }
       }
     }
-    parent[i] = bj;
+    parent[i0] = bj0;
+    if (two) parent[i1] = bj1;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -675,13 +690,25 @@ scr_status alloc_workspace(scr_scene s, int max_batch) {
   SCR_CUDA(cudaEventCreate(&w.ev_stage[0]));
   SCR_CUDA(cudaEventCreate(&w.ev_stage[1]));
   SCR_CUDA(cudaEventCreateWithFlags(&w.ev_upload, cudaEventDisableTiming));
-  if ((st = dalloc(&w.ins_cnt, L)) != SCR_OK) return st;
-  if ((st = dalloc(&w.ins_off, L + 1)) != SCR_OK) return st;
-  if ((st = dalloc(&w.ins_cur, L)) != SCR_OK) return st;
-  if ((st = dalloc(&w.ins_item, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return st;
-  if ((st = dalloc(&w.ins_tgt, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return st;
-  if ((st = dalloc(&w.ins_rank, static_cast<size_t>(w.gmax) * s->T)) != SCR_OK) return st;
-  if ((st = dalloc(&w.ins_total, 1)) != SCR_OK) return st;
+  const size_t items = static_cast<size_t>(w.gmax) * s->T;
+  if ((st = dalloc(&w.ins_start, L)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_key, items)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_key_s, items)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_val, items)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_item, items)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_tgt, items)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_key2, items)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_key2_s, items)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_val2, items)) != SCR_OK) return st;
+  if ((st = dalloc(&w.ins_pos2, items)) != SCR_OK) return st;
+  {  // radix-sort scratch for the larger (64-bit key) of the two sorts
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, w.ins_key, w.ins_key_s, w.ins_val, w.ins_item, static_cast<int>(items));
+    cub::DeviceRadixSort::SortPairs(nullptr, b, w.ins_key2, w.ins_key2_s, w.ins_val2, w.ins_pos2,
+                                    static_cast<int>(items));
+    w.ins_tmp_bytes = std::max(a, b);
+    if ((st = dalloc(reinterpret_cast<unsigned char**>(&w.ins_tmp), w.ins_tmp_bytes)) != SCR_OK) return st;
+  }
   return SCR_OK;
 }
 
@@ -708,7 +735,6 @@ scr_status refresh_lane(scr_scene s) {
 
 // Marks the end of an update of shared state on the scene's stream (lanes wait on it).
 scr_status publish(scr_scene s) {
-  if (!s->published) SCR_CUDA(cudaEventCreateWithFlags(&s->published, cudaEventDisableTiming));
   SCR_CUDA(cudaEventRecord(s->published, s->stream));
   return SCR_OK;
 }
@@ -857,6 +883,8 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   };
   cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) return fail(cuda_fail(e, "cudaStreamCreate"));
+  e = cudaEventCreateWithFlags(&s->published, cudaEventDisableTiming);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
   scr_status st;
   if ((st = dalloc(&s->d_nodes, nodes.size())) != SCR_OK) return fail(st);
   if ((st = dalloc(&s->d_specs, kFeatures)) != SCR_OK) return fail(st);
@@ -867,10 +895,12 @@ scr_status scr_scene_create(scr_device dev, const uint8_t* blob, size_t n, const
   if ((st = dalloc(&s->d_geom, static_cast<size_t>(L) * kMaxModes)) != SCR_OK) return fail(st);
   if ((st = dalloc(&s->d_col, static_cast<size_t>(L) * kMaxModes)) != SCR_OK) return fail(st);
   if ((st = dalloc(&s->d_cov, static_cast<size_t>(L) * kMaxModes * 6)) != SCR_OK) return fail(st);
-  e = cudaMemcpy(s->d_nodes, nodes.data(), nodes.size() * sizeof(int4), cudaMemcpyHostToDevice);
+  e = cudaMemcpyAsync(s->d_nodes, nodes.data(), nodes.size() * sizeof(int4), cudaMemcpyHostToDevice, s->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "upload nodes"));
-  e = cudaMemcpy(s->d_specs, specs.data(), kFeatures * sizeof(short4), cudaMemcpyHostToDevice);
+  e = cudaMemcpyAsync(s->d_specs, specs.data(), kFeatures * sizeof(short4), cudaMemcpyHostToDevice, s->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "upload specs"));
+  e = cudaStreamSynchronize(s->stream);  // the pageable sources are locals
+  if (e != cudaSuccess) return fail(cuda_fail(e, "upload sync"));
   if ((st = alloc_workspace(s, max_batch)) != SCR_OK) return fail(st);
   if ((st = scr_reset(s)) != SCR_OK) return fail(st);
   e = cudaFuncSetAttribute(k_rqs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -940,8 +970,8 @@ void scr_scene_destroy(scr_scene s) {
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hcand, s->ws.sus, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
-                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.dplane, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_cnt, s->ws.ins_off, s->ws.ins_cur, s->ws.ins_item, s->ws.ins_tgt,
-                  s->ws.ins_rank, s->ws.ins_total};
+                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.dplane, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_start, s->ws.ins_key, s->ws.ins_key_s, s->ws.ins_val, s->ws.ins_item,
+                  s->ws.ins_tgt, s->ws.ins_key2, s->ws.ins_key2_s, s->ws.ins_val2, s->ws.ins_pos2, s->ws.ins_tmp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (s->stream) cudaStreamDestroy(s->stream);
@@ -1009,7 +1039,8 @@ static scr_status scr_scene_set_analytic_model_impl(scr_scene s, const scr_prim*
   s->n_prims = n;
   if (n > 0) {
     SCR_CUDA(cudaMalloc(&s->d_prims, n * sizeof(Prim)));
-    SCR_CUDA(cudaMemcpy(s->d_prims, p.data(), n * sizeof(Prim), cudaMemcpyHostToDevice));
+    SCR_CUDA(cudaMemcpyAsync(s->d_prims, p.data(), n * sizeof(Prim), cudaMemcpyHostToDevice, s->stream));
+    SCR_CUDA(cudaStreamSynchronize(s->stream));
   }
   return SCR_OK;
 }
@@ -1087,35 +1118,41 @@ scr_status upload_frames(scr_scene s, const scr_frame* frames, int n) {
   return SCR_OK;
 }
 
-// integrate_frame for the frame packed in workspace slot 0.
+static int bits_for(uint64_t v) {  // bits needed to represent 0..v
+  int b = 1;
+  while (b < 64 && (v >> b) != 0) ++b;
+  return b;
+}
+
+// integrate_frame for the frame packed in workspace slot 0. No host
+// round trip: kernels read the frame's grid count on the device and the sorts run over
+// the workspace's item capacity (padding keys sort last and are skipped).
 scr_status integrate_slot0(scr_scene s, const scr_pose* pose) {
   Workspace& w = s->ws;
   const int T = s->T;
   const int items_max = w.gmax * T;
-  int G = 0;
-  SCR_CUDA(cudaMemcpyAsync(&G, w.gcount, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
-  SCR_CUDA(cudaStreamSynchronize(s->stream));
-  if (G == 0) return SCR_OK;
-  const int items = G * T;
-  (void)items_max;
-  SCR_CUDA(cudaMemsetAsync(w.ins_cnt, 0, s->L * sizeof(unsigned), s->stream));
-  SCR_CUDA(cudaMemsetAsync(w.ins_cur, 0, s->L * sizeof(unsigned), s->stream));
+  const uint32_t pad_key = static_cast<uint32_t>(s->L);
+  const uint64_t pad_key2 = static_cast<uint64_t>(s->L) * static_cast<uint64_t>(s->fp.capacity);
   Pose P;
   std::memcpy(P.R, pose->R, sizeof(P.R));
   std::memcpy(P.t, pose->t, sizeof(P.t));
-  const int tb = 256, nb = (items + tb - 1) / tb;
-  SCR_LAUNCH(s, K_INSERT, (k_ins_count<<<nb, tb, 0, s->stream>>>(w.gslot, items, w.ins_cnt)));
-  SCR_LAUNCH(s, K_INSERT,
-             (k_scan<<<1, 1024, 0, s->stream>>>(w.ins_cnt, w.ins_off, static_cast<int>(s->L), w.ins_total)));
-  SCR_LAUNCH(s, K_INSERT,
-             (k_ins_place<<<nb, tb, 0, s->stream>>>(w.gslot, items, w.ins_off, w.ins_cur, w.ins_item)));
-  SCR_LAUNCH(s, K_INSERT,
-             (k_ins_rank<<<nb, tb, 0, s->stream>>>(w.gslot, T, w.ins_total, w.ins_off, w.ins_cnt, w.ins_item,
-                                                  s->d_seen, s->fp.capacity, s->adapt_seed, w.ins_tgt, w.ins_rank)));
-  SCR_LAUNCH(s, K_INSERT,
-             (k_ins_commit<<<nb, tb, 0, s->stream>>>(w.gslot, T, w.ins_total, w.ins_off, w.ins_cnt, w.ins_item,
-                                                    w.ins_tgt, w.ins_rank, w.gpx, w.tex, s->geom, P,
-                                                    s->fp.capacity, s->d_entries, s->d_seen)));
+  const int tb = 256, nb = (items_max + tb - 1) / tb;
+  SCR_LAUNCH(s, K_INSERT, (k_ins_keys<<<nb, tb, 0, s->stream>>>(w.gslot, w.gcount, T, items_max, pad_key, w.ins_key,
+                                                                w.ins_val)));
+  size_t tmp = w.ins_tmp_bytes;
+  SCR_CUDA(cub::DeviceRadixSort::SortPairs(w.ins_tmp, tmp, w.ins_key, w.ins_key_s, w.ins_val, w.ins_item, items_max, 0,
+                                           bits_for(pad_key), s->stream));
+  SCR_LAUNCH(s, K_INSERT, (k_ins_bounds<<<nb, tb, 0, s->stream>>>(w.ins_key_s, w.gcount, T, w.ins_start)));
+  SCR_LAUNCH(s, K_INSERT, (k_ins_target<<<nb, tb, 0, s->stream>>>(w.ins_key_s, w.gcount, T, w.ins_start, s->d_seen,
+                                                                  s->fp.capacity, s->adapt_seed, pad_key2, w.ins_tgt,
+                                                                  w.ins_key2, w.ins_val2, items_max)));
+  tmp = w.ins_tmp_bytes;
+  SCR_CUDA(cub::DeviceRadixSort::SortPairs(w.ins_tmp, tmp, w.ins_key2, w.ins_key2_s, w.ins_val2, w.ins_pos2,
+                                           items_max, 0, bits_for(pad_key2), s->stream));
+  SCR_LAUNCH(s, K_INSERT, (k_ins_commit<<<nb, tb, 0, s->stream>>>(w.ins_key_s, w.ins_item, w.gcount, T, w.ins_start,
+                                                                  w.ins_key2_s, w.ins_pos2, w.ins_tgt, w.gpx, w.tex,
+                                                                  s->geom, P, s->fp.capacity, pad_key2, s->d_entries,
+                                                                  s->d_seen)));
   SCR_CUDA(cudaGetLastError());
   return SCR_OK;
 }
@@ -1252,6 +1289,7 @@ scr_status scr_dump_entries(scr_scene s, int64_t slot0, int64_t nslots, scr_entr
 
 scr_status scr_dump_predictions(scr_scene s, int32_t* counts, scr_mode* modes) {
   if (!s || !counts) return SCR_E_ARG;
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   SCR_CUDA(cudaStreamSynchronize(s->stream));
@@ -1280,6 +1318,12 @@ scr_status scr_dump_predictions(scr_scene s, int32_t* counts, scr_mode* modes) {
 
 static scr_status scr_load_predictions_impl(scr_scene s, const int32_t* counts, const scr_mode* modes) {
   if (!s || !counts || !modes) return SCR_E_ARG;
+  for (int64_t i = 0; i < s->L; ++i)
+    if (counts[i] < 0 || counts[i] > s->fp.max_clusters) {
+      set_error("scr_load_predictions: leaf " + std::to_string(i) + " has " + std::to_string(counts[i]) +
+                " modes (0.." + std::to_string(s->fp.max_clusters) + " allowed)");
+      return SCR_E_MALFORMED_DATA;
+    }
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   const size_t M = static_cast<size_t>(s->L) * kMaxModes;
   std::vector<ModeGeom> g(M);
@@ -1296,11 +1340,13 @@ static scr_status scr_load_predictions_impl(scr_scene s, const int32_t* counts, 
     c[i] = make_float4(m.colour[0], m.colour[1], m.colour[2], sz);
     for (int q = 0; q < 6; ++q) v[6 * i + q] = m.cov[q];
   }
+  // stream-ordered copies (the scene's stream does not synchronise with the legacy default
+  // stream); synchronised before the pageable sources go out of scope
+  SCR_CUDA(cudaMemcpyAsync(s->d_count, counts, s->L * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->d_geom, g.data(), M * sizeof(ModeGeom), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->d_col, c.data(), M * sizeof(float4), cudaMemcpyHostToDevice, s->stream));
+  SCR_CUDA(cudaMemcpyAsync(s->d_cov, v.data(), M * 6 * sizeof(float), cudaMemcpyHostToDevice, s->stream));
   SCR_CUDA(cudaStreamSynchronize(s->stream));
-  SCR_CUDA(cudaMemcpy(s->d_count, counts, s->L * sizeof(int), cudaMemcpyHostToDevice));
-  SCR_CUDA(cudaMemcpy(s->d_geom, g.data(), M * sizeof(ModeGeom), cudaMemcpyHostToDevice));
-  SCR_CUDA(cudaMemcpy(s->d_col, c.data(), M * sizeof(float4), cudaMemcpyHostToDevice));
-  SCR_CUDA(cudaMemcpy(s->d_cov, v.data(), M * 6 * sizeof(float), cudaMemcpyHostToDevice));
   return SCR_OK;
 }
 
@@ -1312,6 +1358,7 @@ size_t scr_predictions_bytes(scr_scene s) {
 
 scr_status scr_predictions_export(scr_scene s, void* dst) {
   if (!s || !dst) return SCR_E_ARG;
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t M = static_cast<size_t>(s->L) * kMaxModes;
@@ -1356,9 +1403,33 @@ static const NcclApi& nccl_api() {
   return api;
 }
 
+// Counts outside [0, max_clusters] would index past a leaf's modes (or overflow the 6-bit
+// per-tree counts of the K1 records): flagged on the device before a table is accepted.
+__global__ void k_check_counts(const int* __restrict__ counts, int64_t L, int max_clusters, int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < L;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (counts[i] < 0 || counts[i] > max_clusters) atomicAdd(bad, 1);
+}
+
 static scr_status scr_predictions_import_impl(scr_scene s, const void* src) {
   if (!s || !src) return SCR_E_ARG;
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
+  {
+    int* d_bad = nullptr;
+    int bad = 0;
+    SCR_CUDA(cudaMallocAsync(&d_bad, sizeof(int), s->stream));
+    SCR_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s->stream));
+    k_check_counts<<<148, 256, 0, s->stream>>>(static_cast<const int*>(src), s->L, s->fp.max_clusters, d_bad);
+    SCR_CUDA(cudaGetLastError());
+    SCR_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+    SCR_CUDA(cudaFreeAsync(d_bad, s->stream));
+    SCR_CUDA(cudaStreamSynchronize(s->stream));
+    if (bad) {
+      set_error("scr_predictions_import: " + std::to_string(bad) + " leaves with a mode count outside [0, " +
+                std::to_string(s->fp.max_clusters) + "]");
+      return SCR_E_MALFORMED_DATA;
+    }
+  }
   const size_t M = static_cast<size_t>(s->L) * kMaxModes;
   const char* p = static_cast<const char*>(src);
   SCR_CUDA(cudaMemcpyAsync(s->d_count, p, s->L * sizeof(int), cudaMemcpyDeviceToDevice, s->stream));
@@ -1375,6 +1446,7 @@ static scr_status scr_predictions_import_impl(scr_scene s, const void* src) {
 scr_status scr_debug_leaves(scr_scene s, const scr_frame* f, int32_t* grid_px, int32_t* leaves, int* n_grid) {
   if (!s || !f || !n_grid) return SCR_E_ARG;
   SCR_TRY(check_frames(s, f, 1));
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   SCR_TRY(upload_frames(s, f, 1));
@@ -1396,6 +1468,7 @@ scr_status scr_debug_leaves(scr_scene s, const scr_frame* f, int32_t* grid_px, i
 scr_status scr_debug_features(scr_scene s, const scr_frame* f, const int32_t* px, int n, float* out) {
   if (!s || !f || !px || !out || n < 0) return SCR_E_ARG;
   SCR_TRY(check_frames(s, f, 1));
+  StateReadLock lock(s);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   SCR_TRY(upload_frames(s, f, 1));
@@ -1475,6 +1548,7 @@ scr_status scr_frameset_render(scr_frameset fs, int first, const scr_pose* poses
     set_error("scr_frameset_render: no analytic model set");
     return SCR_E_ARG;
   }
+  StateReadLock lock(fs->scene);
   SCR_CUDA(cudaSetDevice(s->dev->ordinal));
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
@@ -1518,6 +1592,7 @@ scr_status scr_scene_set_tsdf_model(scr_scene s, scr_tsdf v) {
     set_error("scr_scene_set_tsdf_model: a relocalisation lane is read-only; set the model on its scene");
     return SCR_E_ARG;
   }
+  StateWriteLock lock(s);
   scr_status st = scr_scene_set_tsdf_model_impl(s, v);
   if (st == SCR_OK && s) st = publish(s);
   return st;
@@ -1529,6 +1604,7 @@ scr_status scr_scene_set_analytic_model(scr_scene s, const scr_prim* prims, int 
     set_error("scr_scene_set_analytic_model: a relocalisation lane is read-only; update the scene it was forked from");
     return SCR_E_ARG;
   }
+  StateWriteLock lock(s);
   scr_status st = scr_scene_set_analytic_model_impl(s, prims, n);
   if (st == SCR_OK && s) st = publish(s);
   return st;
@@ -1539,6 +1615,7 @@ scr_status scr_reset(scr_scene s) {
     set_error("scr_reset: a relocalisation lane is read-only; update the scene it was forked from");
     return SCR_E_ARG;
   }
+  StateWriteLock lock(s);
   scr_status st = scr_reset_impl(s);
   if (st == SCR_OK && s) st = publish(s);
   return st;
@@ -1569,6 +1646,7 @@ scr_status scr_update(scr_scene s, int64_t leaves_per_call) {
     set_error("scr_update: a relocalisation lane is read-only; update the scene it was forked from");
     return SCR_E_ARG;
   }
+  StateWriteLock lock(s);
   scr_status st = scr_update_impl(s, leaves_per_call);
   if (st == SCR_OK && s) st = publish(s);
   return st;
@@ -1579,6 +1657,7 @@ scr_status scr_load_predictions(scr_scene s, const int32_t* counts, const scr_mo
     set_error("scr_load_predictions: a relocalisation lane is read-only; update the scene it was forked from");
     return SCR_E_ARG;
   }
+  StateWriteLock lock(s);
   scr_status st = scr_load_predictions_impl(s, counts, modes);
   if (st == SCR_OK && s) st = publish(s);
   return st;
@@ -1608,6 +1687,9 @@ scr_status scr_broadcast_predictions(scr_scene* per_gpu, int ngpu, int root) {
       }
   }
   if (ngpu == 1) return SCR_OK;
+  std::vector<std::unique_ptr<StateWriteLock>> locks;  // receivers' tables are rewritten
+  for (int i = 0; i < ngpu; ++i)
+    if (i != root) locks.emplace_back(new StateWriteLock(per_gpu[i]));
   const NcclApi& nc = nccl_api();
   if (!nc.ok) {
     set_error("scr_broadcast_predictions: libnccl.so.2 could not be loaded");
@@ -1674,6 +1756,7 @@ scr_status scr_predictions_import(scr_scene s, const void* src) {
     set_error("scr_predictions_import: a relocalisation lane is read-only; update the scene it was forked from");
     return SCR_E_ARG;
   }
+  StateWriteLock lock(s);
   scr_status st = scr_predictions_import_impl(s, src);
   if (st == SCR_OK && s) st = publish(s);
   return st;
