@@ -36,7 +36,7 @@ int main() {
   scr_frameset_destroy(fs);
 
   for (int i = 0; i < n_adapt; ++i)  // train
-    reloc.integrate_frame({&depth[i * px], &rgb[i * px * 3], true}, adapt[i]);
+    reloc.integrate_frame({&depth[i * px], &rgb[i * px * 3], k.width, k.height, true}, adapt[i]);
   reloc.update_leaves_round_robin(reloc.total_leaf_count());  // update (every leaf once)
 
   std::vector<sg::RgbdFrame> frames;

@@ -409,62 +409,36 @@ __global__ void __launch_bounds__(256) k_rqs(const scr_entry* __restrict__ entri
   }
   if (threadIdx.x == 0) nroots = 0;
   __syncthreads();
-  // density: each thread owns two rows (i0, i0 + blockDim) so that every j loaded from
-  // shared memory serves two independent f64 sums (each still accumulated in j order)
-  for (int i0 = threadIdx.x; i0 < n; i0 += 2 * blockDim.x) {
-    const int i1 = i0 + blockDim.x;
-    const bool two = i1 < n;
-    const float x0 = sx[i0], y0 = sy[i0], z0 = sz[i0];
-    const float x1 = two ? sx[i1] : x0, y1 = two ? sy[i1] : y0, z1 = two ? sz[i1] : z0;
-    double acc0 = 0.0, acc1 = 0.0;
+  // density
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float xi = sx[i], yi = sy[i], zi = sz[i];
+    double acc = 0.0;
     for (int j = 0; j < n; ++j) {
-      const float xj = sx[j], yj = sy[j], zj = sz[j];
-      const float ax = __fsub_rn(x0, xj), ay = __fsub_rn(y0, yj), az = __fsub_rn(z0, zj);
-      const float bx = __fsub_rn(x1, xj), by = __fsub_rn(y1, yj), bz = __fsub_rn(z1, zj);
-      const float da = __fmaf_rn(az, az, __fmaf_rn(ay, ay, __fmul_rn(ax, ax)));
-      const float db = __fmaf_rn(bz, bz, __fmaf_rn(by, by, __fmul_rn(bx, bx)));
-      acc0 = acc0 + static_cast<double>(det_expf(__fmul_rn(da, rp.c)));
-      acc1 = acc1 + static_cast<double>(det_expf(__fmul_rn(db, rp.c)));
+      const float dx = __fsub_rn(xi, sx[j]), dy = __fsub_rn(yi, sy[j]), dz = __fsub_rn(zi, sz[j]);
+      const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+      acc = acc + static_cast<double>(det_expf(__fmul_rn(d2, rp.c)));
     }
-    rho[i0] = acc0;
-    if (two) rho[i1] = acc1;
+    rho[i] = acc;
   }
   __syncthreads();
-  // link: nearest strictly-higher-density point within tau (ties: lower index), two rows
-  // per thread as above
-  for (int i0 = threadIdx.x; i0 < n; i0 += 2 * blockDim.x) {
-    const int i1 = i0 + blockDim.x;
-    const bool two = i1 < n;
-    const float x0 = sx[i0], y0 = sy[i0], z0 = sz[i0];
-    const float x1 = two ? sx[i1] : x0, y1 = two ? sy[i1] : y0, z1 = two ? sz[i1] : z0;
-    const double r0 = rho[i0], r1 = two ? rho[i1] : r0;
-    float best0 = __int_as_float(0x7f800000), best1 = best0;
-    int bj0 = -1, bj1 = -1;
+  // link
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float xi = sx[i], yi = sy[i], zi = sz[i];
+    const double ri = rho[i];
+    float best = __int_as_float(0x7f800000);
+    int bj = -1;
     for (int j = 0; j < n; ++j) {
+      if (j == i) continue;
       const double rj = rho[j];
-      const bool up0 = j != i0 && (rj > r0 || (rj == r0 && j < i0));
-      const bool up1 = j != i1 && (rj > r1 || (rj == r1 && j < i1));
-      if (!(up0 || up1)) continue;
-      const float xj = sx[j], yj = sy[j], zj = sz[j];
-      if (up0) {
-        const float dx = __fsub_rn(x0, xj), dy = __fsub_rn(y0, yj), dz = __fsub_rn(z0, zj);
-        const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-        if (d2 <= rp.tau2 && d2 < best0) {
-          best0 = d2;
-          bj0 = j;
-        }
-      }
-      if (up1) {
-        const float dx = __fsub_rn(x1, xj), dy = __fsub_rn(y1, yj), dz = __fsub_rn(z1, zj);
-        const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-        if (d2 <= rp.tau2 && d2 < best1) {
-          best1 = d2;
-          bj1 = j;
-        }
+      if (!(rj > ri || (rj == ri && j < i))) continue;
+      const float dx = __fsub_rn(xi, sx[j]), dy = __fsub_rn(yi, sy[j]), dz = __fsub_rn(zi, sz[j]);
+      const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+      if (d2 <= rp.tau2 && d2 < best) {
+        best = d2;
+        bj = j;
       }
     }
-    parent[i0] = bj0;
-    if (two) parent[i1] = bj1;
+    parent[i] = bj;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
