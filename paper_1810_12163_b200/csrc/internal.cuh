@@ -240,6 +240,9 @@ scr_status check_frames(const scr_scene_s* s, const scr_frame* frames, int n);
 struct StateReadLock {
   std::shared_mutex* m = nullptr;
   explicit StateReadLock(scr_scene_s* s) {
+#ifdef SCR_NO_STATE_LOCK
+    s = nullptr;
+#endif
     if (s) {
       m = &(s->parent ? s->parent : s)->state_mu;
       m->lock_shared();
