@@ -251,7 +251,7 @@ RelocResult run_cascade(const RansacParams* stages, const int* modes, const doub
 uint64_t stage_seed(uint64_t seed, int stage);
 
 // Canonical reduction orders shared (by definition, not by code) with the GPU.
-constexpr int kLmLanes = 32;
+constexpr int kLmLanes = 128;  // canonical LM reduction lanes (4 warps of 32)
 constexpr int kIcpCtas = 8;                    // ICP / score: 8-CTA cluster
 constexpr int kIcpLanes = 256 * kIcpCtas;      // lanes = threads of the cluster
 constexpr int kIcpIters[3] = {4, 5, 10};  // level 0 (fine), 1, 2 (coarse)

@@ -228,22 +228,23 @@ inline void lm_term(const Pose& H, const LmSample& s, bool use_cov, double acc[k
   for (int a = 0; a < 6; ++a) acc[21 + a] = acc[21 + a] + ((J[0][a] * r[0] + J[1][a] * r[1]) + J[2][a] * r[2]);
 }
 
-// Canonical 32-lane order: lane l accumulates samples l, l+32, ... in order, then an
-// xor butterfly (16, 8, 4, 2, 1) combines lanes.
+// Canonical 128-lane order: lane l accumulates samples l, l+128, ... in order, then an xor
+// butterfly combines lanes, first inside each 32-lane warp (16, 8, 4, 2, 1), then across the
+// four warps (32, 64): the total is (W0 + W1) + (W2 + W3).
 void lm_accumulate(const Pose& H, const std::vector<LmSample>& smp, bool use_cov, bool with_jac, double out[kAcc]) {
-  double lanes[kLmLanes][kAcc];
-  for (auto& l : lanes)
+  thread_local double L[kLmLanes][kAcc], nxt[kLmLanes][kAcc];
+  for (auto& l : L)
     for (double& v : l) v = 0.0;
   for (size_t i = 0; i < smp.size(); ++i)
-    if (smp[i].m) lm_term(H, smp[i], use_cov, lanes[i % kLmLanes], with_jac);
-  for (int off = kLmLanes / 2; off >= 1; off >>= 1) {
-    double nxt[kLmLanes][kAcc];
+    if (smp[i].m) lm_term(H, smp[i], use_cov, L[i % kLmLanes], with_jac);
+  static const int kOffsets[7] = {16, 8, 4, 2, 1, 32, 64};
+  for (int off : kOffsets) {
     for (int l = 0; l < kLmLanes; ++l)
-      for (int a = 0; a < kAcc; ++a) nxt[l][a] = lanes[l][a] + lanes[l ^ off][a];
+      for (int a = 0; a < kAcc; ++a) nxt[l][a] = L[l][a] + L[l ^ off][a];
     for (int l = 0; l < kLmLanes; ++l)
-      for (int a = 0; a < kAcc; ++a) lanes[l][a] = nxt[l][a];
+      for (int a = 0; a < kAcc; ++a) L[l][a] = nxt[l][a];
   }
-  for (int a = 0; a < kAcc; ++a) out[a] = lanes[0][a];
+  for (int a = 0; a < kAcc; ++a) out[a] = L[0][a];
 }
 }  // namespace
 

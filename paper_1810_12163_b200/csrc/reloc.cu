@@ -1182,16 +1182,36 @@ struct LmArgs {
   int ns, scap, cand_stride, n_out, use_cov;
 };
 
-SCR_DEV void lm_accum(const Pose& H, const double x[3], const ModeGeom& mg, bool use_cov, double acc[28], bool jac) {
+// The part of a mode record LM needs: mu and Sigma^-1/2 (s00 s01 s02 s11 s12 s22).
+struct LmMode {
+  float mu[3], s[6];
+};
+SCR_DEV LmMode lm_mode(const ModeGeom* geom, int mi, bool use_cov) {
+  LmMode m;
+  const float4 q0 = geom[mi].q0;
+  m.mu[0] = q0.x;
+  m.mu[1] = q0.y;
+  m.mu[2] = q0.z;
+  if (use_cov) {
+    const float4 q2 = geom[mi].q2, q3 = geom[mi].q3;
+    m.s[0] = q2.y; m.s[1] = q2.z; m.s[2] = q2.w; m.s[3] = q3.x; m.s[4] = q3.y; m.s[5] = q3.z;
+  } else {
+    m.s[0] = m.s[3] = m.s[5] = 1.0f;
+    m.s[1] = m.s[2] = m.s[4] = 0.0f;
+  }
+  return m;
+}
+
+SCR_DEV void lm_accum(const Pose& H, const double x[3], const LmMode& mg, bool use_cov, double acc[28], bool jac) {
   double y[3];
   pose_apply(H, x, y);
-  const double d0 = y[0] - static_cast<double>(mg.q0.x), d1 = y[1] - static_cast<double>(mg.q0.y),
-               d2 = y[2] - static_cast<double>(mg.q0.z);
+  const double d0 = y[0] - static_cast<double>(mg.mu[0]), d1 = y[1] - static_cast<double>(mg.mu[1]),
+               d2 = y[2] - static_cast<double>(mg.mu[2]);
   double S[9];
   if (use_cov) {
-    S[0] = mg.q2.y; S[1] = mg.q2.z; S[2] = mg.q2.w;
-    S[3] = mg.q2.z; S[4] = mg.q3.x; S[5] = mg.q3.y;
-    S[6] = mg.q2.w; S[7] = mg.q3.y; S[8] = mg.q3.z;
+    S[0] = mg.s[0]; S[1] = mg.s[1]; S[2] = mg.s[2];
+    S[3] = mg.s[1]; S[4] = mg.s[3]; S[5] = mg.s[4];
+    S[6] = mg.s[2]; S[7] = mg.s[4]; S[8] = mg.s[5];
   } else {
 #pragma unroll
     for (int i = 0; i < 9; ++i) S[i] = (i % 4 == 0) ? 1.0 : 0.0;
@@ -1485,16 +1505,24 @@ __device__ __noinline__ bool lm_solve(const double* acc, double lambda, double d
 #define SCR_LM_INFLIGHT 4
 #endif
 constexpr int kLmInFlight = SCR_LM_INFLIGHT;  // sample gathers in flight per lane
+constexpr int kLmThreads = 128;  // canonical LM reduction lanes per candidate (4 warps)
 
-__global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmArgs la,
+#ifndef SCR_LM_STEP_MINB
+#define SCR_LM_STEP_MINB 1
+#endif
+__global__ void __launch_bounds__(kLmThreads, SCR_LM_STEP_MINB) k_lm_step(FrameRefs fr, PredView pv, LmArgs la,
                                                  const int* __restrict__ samples, Pose* __restrict__ cand,
                                                  const int* __restrict__ ncand, LmState* __restrict__ st,
                                                  const int* __restrict__ assoc, unsigned long long* __restrict__ work) {
+  __shared__ double s_red[kLmThreads / 32][28];
+  __shared__ double s_tot[28];
+  __shared__ Pose s_Hn;
+  __shared__ int s_ok;
   const int a = blockIdx.y;
-  const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int h = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int n = ncand[a];
-  if (n <= la.n_out || h >= n) return;
+  if (n <= la.n_out || h >= n) return;  // uniform over the CTA
   const size_t hi = static_cast<size_t>(a) * la.cand_stride + h;
   LmState ls = st[hi];
   if (ls.done) return;
@@ -1502,62 +1530,76 @@ __global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmAr
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
   const int* smp = samples + static_cast<size_t>(a) * la.scap;
   const int* as = assoc + hi * la.scap;
-  Pose H = cand[hi];
+  const bool use_cov = la.use_cov != 0;
+  const Pose H = cand[hi];
   double acc[28];
 #pragma unroll
   for (int k = 0; k < 28; ++k) acc[k] = 0.0;
   int terms = 0;
-  // lane l accumulates samples l, l + 32, l + 64, ... in order; kLmInFlight of them are
-  // gathered before any is accumulated (the loads are independent, the sums are not)
-  for (int i0 = lane; i0 < la.ns; i0 += 32 * kLmInFlight) {
+  // lane l of the CTA accumulates samples l, l + 128, ... in order; kLmInFlight of them
+  // are gathered before any is accumulated (the loads are independent, the sums are not)
+  for (int i0 = tid; i0 < la.ns; i0 += kLmThreads * kLmInFlight) {
     int mi[kLmInFlight];
     float4 c[kLmInFlight];
-    ModeGeom gm[kLmInFlight];
+    LmMode gm[kLmInFlight];
 #pragma unroll
     for (int u = 0; u < kLmInFlight; ++u) {
-      const int i = i0 + 32 * u;
+      const int i = i0 + kLmThreads * u;
       mi[u] = i < la.ns ? as[i] : -1;
       if (mi[u] >= 0) {
         c[u] = fr.gcam[fbase + smp[i]];
-        gm[u] = pv.geom[mi[u]];
+        gm[u] = lm_mode(pv.geom, mi[u], use_cov);
       }
     }
 #pragma unroll
     for (int u = 0; u < kLmInFlight; ++u)
       if (mi[u] >= 0) {
         const double x[3] = {static_cast<double>(c[u].x), static_cast<double>(c[u].y), static_cast<double>(c[u].z)};
-        lm_accum(H, x, gm[u], la.use_cov != 0, acc, true);
+        lm_accum(H, x, gm[u], use_cov, acc, true);
         ++terms;
       }
   }
   if (work) work_add(work, W_LM_TERMS, static_cast<unsigned>(terms));
+  // canonical 128-lane reduction: xor butterfly inside each warp, then (W0 + W1) + (W2 + W3)
 #pragma unroll
-  for (int k = 0; k < 28; ++k) acc[k] = warp_sum_xor(acc[k]);
+  for (int k = 0; k < 28; ++k) {
+    const double v = warp_sum_xor(acc[k]);
+    if (lane == 0) s_red[wid][k] = v;
+  }
+  __syncthreads();
+  if (tid < 28) s_tot[tid] = (s_red[0][tid] + s_red[1][tid]) + (s_red[2][tid] + s_red[3][tid]);
+  __syncthreads();
   ls.need_assoc = 0;
-  const double E = acc[27];
+  const double E = s_tot[27];
   if (!(E > 0.0)) {
     ls.done = 1;
   } else {
-    double delta[6];
-    if (!lm_solve(acc, ls.lambda, delta)) {
+    if (tid == 0) {  // damped solve + update once per candidate, shared through shared memory
+      double delta[6];
+      s_ok = lm_solve(s_tot, ls.lambda, delta) ? 1 : 0;
+      if (s_ok) {
+        Pose D;
+        exp_se3(delta, D);
+        pose_compose(D, H, s_Hn);
+      }
+    }
+    __syncthreads();
+    if (!s_ok) {
       ls.lambda = ls.lambda * 10.0;
     } else {
-      Pose D, Hn;
-      exp_se3(delta, D);
-      pose_compose(D, H, Hn);
-      double accn[28];
-      accn[27] = 0.0;
-      for (int i0 = lane; i0 < la.ns; i0 += 32 * kLmInFlight) {
+      const Pose Hn = s_Hn;
+      double en[1] = {0.0};
+      for (int i0 = tid; i0 < la.ns; i0 += kLmThreads * kLmInFlight) {
         int mi[kLmInFlight];
         float4 c[kLmInFlight];
-        ModeGeom gm[kLmInFlight];
+        LmMode gm[kLmInFlight];
 #pragma unroll
         for (int u = 0; u < kLmInFlight; ++u) {
-          const int i = i0 + 32 * u;
+          const int i = i0 + kLmThreads * u;
           mi[u] = i < la.ns ? as[i] : -1;
           if (mi[u] >= 0) {
             c[u] = fr.gcam[fbase + smp[i]];
-            gm[u] = pv.geom[mi[u]];
+            gm[u] = lm_mode(pv.geom, mi[u], use_cov);
           }
         }
 #pragma unroll
@@ -1565,22 +1607,28 @@ __global__ void __launch_bounds__(128) k_lm_step(FrameRefs fr, PredView pv, LmAr
           if (mi[u] >= 0) {
             const double x[3] = {static_cast<double>(c[u].x), static_cast<double>(c[u].y),
                                  static_cast<double>(c[u].z)};
-            lm_accum(Hn, x, gm[u], la.use_cov != 0, accn, false);
+            double accn[28];
+            accn[27] = en[0];
+            lm_accum(Hn, x, gm[u], use_cov, accn, false);
+            en[0] = accn[27];
           }
       }
-      const double En = warp_sum_xor(accn[27]);
+      const double ew = warp_sum_xor(en[0]);
+      __syncthreads();  // s_red reuse
+      if (lane == 0) s_red[wid][0] = ew;
+      __syncthreads();
+      const double En = (s_red[0][0] + s_red[1][0]) + (s_red[2][0] + s_red[3][0]);
       if (En < E) {
-        H = Hn;
         ls.lambda = ls.lambda * 0.1;
         ls.need_assoc = 1;
         if ((E - En) / E < 1e-6) ls.done = 1;
-        if (lane == 0) cand[hi] = H;
+        if (tid == 0) cand[hi] = Hn;
       } else {
         ls.lambda = ls.lambda * 10.0;
       }
     }
   }
-  if (lane == 0) st[hi] = ls;
+  if (tid == 0) st[hi] = ls;
 }
 
 // ================================ K8-K10: ICP + raycast + depth-difference score ============
@@ -2275,7 +2323,7 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
           SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<32><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand,
                                                                            lmst, w.assoc, wk)));
         }
-        SCR_LAUNCH(s, K_LM, (k_lm_step<<<dim3((p.n_cull + 3) / 4, nA), 128, 0, s->stream>>>(
+        SCR_LAUNCH(s, K_LM, (k_lm_step<<<dim3(nk, nA), kLmThreads, 0, s->stream>>>(
                                 fr, pv, la, w.samples, w.cand, w.ncand, lmst, w.assoc, wk)));
       }
     }
