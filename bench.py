@@ -182,8 +182,11 @@ class ClockSampler:
 
     def __enter__(self):
         try:
+            if os.environ.get("SCR_CLOCK_MS") == "0":
+                return self
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                                          "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                          "-lms", os.environ.get("SCR_CLOCK_MS", "50"), "-i", str(self.index)],
+                                         stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()

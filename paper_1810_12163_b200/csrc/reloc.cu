@@ -2258,7 +2258,9 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
   }
   SCR_TRY(ensure_ransac_ws(s, p.n_max, p.n_cull, scap));
   const int jobs_per = mode == SCR_MODE_RANKED ? std::min(p.n_out, p.n_cull) : 1;
-  SCR_TRY(ensure_icp_ws(s, std::min(nA * jobs_per, 1024)));
+  // sized for a full batch, not this stage's active frames: growing the map buffer later
+  // (cudaFree + cudaMalloc) would synchronise the whole device under every other lane
+  SCR_TRY(ensure_icp_ws(s, std::min(w.cap * jobs_per, 1024)));
   const FrameRefs fr = frame_refs(s);
   const PredView pv = s->pred_view();
   GenParams gp{p.max_gen_iters, p.n_max, p.min_sq_dist, p.colour_thresh, p.rigidity_tol,
