@@ -254,6 +254,7 @@ uint64_t stage_seed(uint64_t seed, int stage);
 constexpr int kLmLanes = 128;  // canonical LM reduction lanes (4 warps of 32)
 constexpr int kIcpCtas = 8;                    // ICP / score: 8-CTA cluster
 constexpr int kIcpLanes = 256 * kIcpCtas;      // lanes = threads of the cluster
-constexpr int kIcpIters[3] = {4, 5, 10};  // level 0 (fine), 1, 2 (coarse)
+constexpr int kIcpIters[3] = {4, 5, 10};  // at most, level 0 (fine), 1, 2 (coarse)
+constexpr double kIcpStopStep = 1e-6;    // a level stops once every |twist component| < this
 
 }  // namespace oracle

@@ -1642,6 +1642,7 @@ namespace cg = cooperative_groups;
 constexpr int kIcpCtas = 8;
 constexpr int kIcpThreads = 256;
 constexpr int kIcpLanes = kIcpCtas * kIcpThreads;
+constexpr double kIcpStopStep = 1e-6;  // oracle.hpp: a level stops once every |twist component| < this
 
 struct IcpArgs {
   int cand_stride, n_cand_jobs;  // jobs per frame (1 for icp/raw, n_out for ranked)
@@ -1742,7 +1743,7 @@ SCR_DEV
 #else
 __device__ __noinline__
 #endif
-bool icp_step(const double* tot, Pose* T) {
+int icp_step(const double* tot, Pose* T) {
   double M[36], rhs[6], delta[6];
   int k = 0;
 #pragma unroll 1
@@ -1758,12 +1759,17 @@ bool icp_step(const double* tot, Pose* T) {
     rhs[p] = -tot[21 + p];
     M[6 * p + p] = M[6 * p + p] + mu;
   }
-  if (!chol6(M, rhs, delta)) return false;
+  if (!chol6(M, rhs, delta)) return 0;
   Pose D, Tn;
   exp_se3(delta, D);
   pose_compose(D, *T, Tn);
   *T = Tn;
-  return true;
+  // the level has converged once the step is below kIcpStopStep in every twist component
+  // (further steps only move the pose within the f32 noise floor; A8)
+  double dmax = 0.0;
+#pragma unroll 1
+  for (int a = 0; a < 6; ++a) dmax = fmax(dmax, fabs(delta[a]));
+  return dmax < kIcpStopStep ? 2 : 1;
 }
 
 #ifndef SCR_ICP_PIX
@@ -2031,7 +2037,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
             lstat[1] = valid_t;
             lstat_r2 = tot[27];
           }
-          stop_level = (inl_t < 6 || !icp_step(tot, &Ts)) ? 1 : 0;
+          stop_level = (inl_t < 6 || icp_step(tot, &Ts) != 1) ? 1 : 0;
         }
         __syncthreads();
         pbuf ^= 1;
