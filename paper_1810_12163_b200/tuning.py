@@ -7,6 +7,10 @@ tuning module).
   value); stops after a sweep without change or `max_sweeps`; every evaluation is memoised
   by assignment. Evaluations of one coordinate scan are independent, so they run
   concurrently on relocalisation lanes of the scene (one host thread per lane).
+* `sharded_parallel`: the same scans sharded across GPUs (one process per GPU,
+  torch.distributed): the uncached assignments of a scan go to rank i mod N, each rank
+  evaluates its share (on its own lanes), and the costs are all-gathered into every rank's
+  memo, so all ranks take identical decisions.
 * `tune_single`: objective = sum over (adapt, validation) sequence pairs of the cost of the
   profile on the validation frames after adapting on the training frames.
 * `tune_cascade`: the four-step procedure of Appendix B.2 (tune the fastest stage fully,
@@ -86,6 +90,49 @@ class Memo:
             del self._pending[k]
         ev.set()
         return v
+
+    def cached(self, a: dict) -> bool:
+        with self._lock:
+            return self.key(a) in self.table
+
+    def put(self, k: tuple, v: float) -> None:
+        """Inserts a cost computed elsewhere (another rank); never overwrites."""
+        with self._lock:
+            self.table.setdefault(k, v)
+
+
+def sharded_parallel(memo: Memo, dist=None, local: Callable[[list], list] | None = None) -> Callable[[list], list]:
+    """`parallel` for coordinate_descent over N ranks: the scan's uncached assignments (in scan
+    order, deduplicated) go to rank i mod N; each rank evaluates its share with `local` (e.g.
+    GpuObjective.parallel on its lanes) or sequentially, then every rank all-gathers the
+    (assignment, cost) pairs into its memo. Every rank therefore holds the same table and
+    takes the same decisions; no rank evaluates an assignment another rank owns."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return local or (lambda cands: [memo(c) for c in cands])
+    rank, world = dist.get_rank(), dist.get_world_size()
+
+    def run(cands: list) -> list:
+        todo, seen = [], set()
+        for c in cands:
+            k = Memo.key(c)
+            if k not in seen and not memo.cached(c):
+                seen.add(k)
+                todo.append(c)
+        mine = todo[rank::world]
+        if local:
+            local(mine)
+        else:
+            for c in mine:
+                memo(c)
+        pairs = [(Memo.key(c), memo(c)) for c in mine]
+        parts = [None] * world
+        dist.all_gather_object(parts, pairs)
+        for part in parts:
+            for k, v in part:
+                memo.put(k, v)
+        return [memo(c) for c in cands]
+
+    return run
 
 
 @dataclass
@@ -221,8 +268,11 @@ class GpuObjective:
 
 
 def tune_single(domains: Sequence[ParamDomain], objective: GpuObjective, start: dict,
-                max_sweeps: int = 4) -> DescentResult:
-    return coordinate_descent(domains, objective.memo, start, max_sweeps, parallel=objective.parallel)
+                max_sweeps: int = 4, dist=None) -> DescentResult:
+    """Coordinate descent of one profile; with `dist` (torch.distributed, one process per GPU,
+    each with its own GpuObjective on its own device) every scan is sharded across the ranks."""
+    par = sharded_parallel(objective.memo, dist, objective.parallel)
+    return coordinate_descent(domains, objective.memo, start, max_sweeps, parallel=par)
 
 
 def tune_cascade(stage_domains: Sequence[Sequence[ParamDomain]], objectives: Sequence[GpuObjective],

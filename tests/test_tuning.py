@@ -115,3 +115,68 @@ def test_tune_cascade_step_order_shares_forest_params():
     assert res[1].assignment["tau"] == 0.2 and res[2].assignment["tau"] == 0.2  # shared phi*
     assert [s.n_max for s in cfg.stages] == [1024, 2048, 512]
     assert list(cfg.thresholds) == [0.05, 0.075]
+
+
+def _sharded_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1810_12163_b200.tuning import Memo, ParamDomain, coordinate_descent, sharded_parallel
+
+        doms = [ParamDomain("a", list(range(9))), ParamDomain("b", [-3, -2, -1, 0, 1, 2]),
+                ParamDomain("c", [0.25, 0.75, 1.25])]
+        mine = []
+
+        def f(x):
+            mine.append(dict(x))
+            return (x["a"] - 6) ** 2 + (x["b"] + 2) ** 2 + (x["c"] - 0.75) ** 2 + 0.1 * x["a"] * (x["b"] + 2)
+
+        memo = Memo(f)
+        r = coordinate_descent(doms, memo, {"a": 0, "b": 0, "c": 0.25}, max_sweeps=10,
+                               parallel=sharded_parallel(memo, dist))
+        q.put((rank, r.assignment, r.cost, r.history, [tuple(sorted(m.items())) for m in mine],
+               len(memo.table)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_coordinate_descent_sharded_over_two_ranks():
+    """scans sharded across ranks (gloo, world size 2 on CPU) reach the
+    same result as the sequential descent, every rank holds the full memo, and the ranks split
+    the evaluations without overlap."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_1810_12163_b200.tuning import ParamDomain, coordinate_descent
+
+    doms = [ParamDomain("a", list(range(9))), ParamDomain("b", [-3, -2, -1, 0, 1, 2]),
+            ParamDomain("c", [0.25, 0.75, 1.25])]
+
+    def f(x):
+        return (x["a"] - 6) ** 2 + (x["b"] + 2) ** 2 + (x["c"] - 0.75) ** 2 + 0.1 * x["a"] * (x["b"] + 2)
+
+    ref = coordinate_descent(doms, f, {"a": 0, "b": 0, "c": 0.25}, max_sweeps=10)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    res = sorted(q.get() for _ in range(2))
+    for rank, a, c, hist, mine, ntable in res:
+        assert a == ref.assignment and c == ref.cost and hist == ref.history
+        assert ntable == ref.evaluations  # the whole memo on every rank
+    e0, e1 = set(res[0][4]), set(res[1][4])
+    assert not (e0 & e1 - {tuple(sorted({"a": 0, "b": 0, "c": 0.25}.items()))})  # disjoint (start on both)
+    assert len(e0 | e1) == ref.evaluations
