@@ -184,6 +184,83 @@ SCR_DEV bool geometry_prefilter(double min_sq_dist, double rigidity_tol, const i
   return true;
 }
 
+// Three-way f32 classification of checks 2-3 plus Kabsch regularity, for the attempt loop
+// (keeps the f64 arithmetic, and its registers, out of k_hypgen):
+//  kClsFail    — the exact f64 checks certainly reject (outside a 1e-3 m / m^2 margin);
+//  kClsPass    — they certainly accept (inside the margin) and Kabsch is certainly regular;
+//  kClsSuspect — anything else: k_hypfin decides it exactly, in attempt order.
+// The world points are the same f32 values as in f64 and the f32 camera points are within
+// ~1e-5 m of the exact ones, far inside the margins. Regularity: the centred 3-pair
+// cross-covariance H has rank <= 2, so r = sqrt(sum of squared 2x2 minors) / |H|_F^2 bounds
+// sigma1 / sigma0 from below; the f64 finisher needs r > 1e-6, the f32 test asks r > 1e-3
+// (and a non-vanishing |H|), three orders of magnitude above the f32 error of r.
+enum { kClsFail = 0, kClsPass = 1, kClsSuspect = 2 };
+SCR_DEV int geometry_classify(double min_sq_dist, double rigidity_tol, const int4* grec, const FrameGeom& g,
+                              float ifx, float ify, const ModeGeom* geom, int g0, int g1, int g2, int m0, int m1,
+                              int m2) {
+  const float4 wq[3] = {geom[m0].q0, geom[m1].q0, geom[m2].q0};
+  const int4 rr[3] = {grec[2 * g0], grec[2 * g1], grec[2 * g2]};
+  float cf[3][3], wf[3][3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float d = __int_as_float(rr[k].y);
+    cf[k][0] = (static_cast<float>(rr[k].x & 0xffff) - g.cx) * d * ifx;
+    cf[k][1] = (static_cast<float>(rr[k].x >> 16) - g.cy) * d * ify;
+    cf[k][2] = d;
+    wf[k][0] = wq[k].x;
+    wf[k][1] = wq[k].y;
+    wf[k][2] = wq[k].z;
+  }
+  const float rig = static_cast<float>(rigidity_tol), msq = static_cast<float>(min_sq_dist);
+  bool sure = true;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int pa = q == 2 ? 1 : 0, pb = q == 0 ? 1 : 2;
+    const float ax = wf[pa][0] - wf[pb][0], ay = wf[pa][1] - wf[pb][1], az = wf[pa][2] - wf[pb][2];
+    const float bx = cf[pa][0] - cf[pb][0], by = cf[pa][1] - cf[pb][1], bz = cf[pa][2] - cf[pb][2];
+    const float dw2f = ax * ax + ay * ay + az * az, dc2f = bx * bx + by * by + bz * bz;
+    if (dw2f < msq - 1e-3f) return kClsFail;
+    const float dev = fabsf(sqrtf(dw2f) - sqrtf(dc2f));
+    if (dev > rig + 1e-3f) return kClsFail;
+    if ((min_sq_dist > 0.0 && dw2f < msq + 1e-3f) || dev > rig - 1e-3f) sure = false;
+  }
+  if (!sure) return kClsSuspect;
+  float H[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) H[i] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float wc = (wf[0][c] + wf[1][c] + wf[2][c]) * (1.0f / 3.0f);
+    const float cc = (cf[0][c] + cf[1][c] + cf[2][c]) * (1.0f / 3.0f);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      wf[k][c] -= wc;
+      cf[k][c] -= cc;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) H[3 * r + c] += wf[k][r] * cf[k][c];
+  float f2 = 0.0f, e2 = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) f2 += H[i] * H[i];
+#pragma unroll
+  for (int r0 = 0; r0 < 3; ++r0)
+#pragma unroll
+    for (int r1 = r0 + 1; r1 < 3; ++r1)
+#pragma unroll
+      for (int c0 = 0; c0 < 3; ++c0)
+#pragma unroll
+        for (int c1 = c0 + 1; c1 < 3; ++c1) {
+          const float mnr = H[3 * r0 + c0] * H[3 * r1 + c1] - H[3 * r0 + c1] * H[3 * r1 + c0];
+          e2 += mnr * mnr;
+        }
+  return (f2 > 1e-10f && sqrtf(e2) > 1e-3f * f2) ? kClsPass : kClsSuspect;
+}
+
 // Exact checks 2-3 (distances in f64) and Kabsch. Camera points are the
 // exact f64 backprojection of the records (geometry.hpp:194-199, the same operations as K1).
 // Scalars and pointers only: passing the kernel-parameter structs by reference would force
@@ -522,12 +599,10 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
             e.r2.x = mode_from_record(s_lbase, static_cast<uint32_t>(A2.w), L2, p2);
           }
           const int em0 = static_cast<int>(e.r0.x), em1 = static_cast<int>(e.r1.x), em2 = static_cast<int>(e.r2.x);
-          bool regular = true;
-          pass = geometry_prefilter(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, ifx, ify, pv.geom,
-                                    eg0, eg1, eg2, em0, em1, em2) &&
-                 distance_checks_f64(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, pv.geom, eg0, eg1,
-                                     eg2, em0, em1, em2, nullptr, nullptr, &regular);
-          if (pass && (!regular || gp.force_suspect)) {  // Kabsch may be degenerate: k_hypfin decides, the slot goes on
+          const int cls = geometry_classify(gp.min_sq_dist, gp.rigidity_tol, fr.grec + 2 * fbase, g, ifx, ify,
+                                            pv.geom, eg0, eg1, eg2, em0, em1, em2);
+          pass = cls != kClsFail;
+          if (pass && (cls == kClsSuspect || gp.force_suspect)) {  // k_hypfin decides it exactly, the slot goes on
             const int i = atomicAdd(&sus_cnt[a], 1);
             if (i < kMaxSuspects) {
               int4* sp = sus + 2 * (static_cast<size_t>(a) * kMaxSuspects + i);
