@@ -405,7 +405,7 @@ SCR_DEV int attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, co
 // suspects and the slot goes on, so k_hypfin never has to re-run a slot's attempt chain
 // (unless the suspect list overflows).
 #ifndef SCR_HYPGEN_MINB
-#define SCR_HYPGEN_MINB 2  // resident CTAs per SM the register budget is sized for (16 warps)
+#define SCR_HYPGEN_MINB 3  // resident CTAs per SM the register budget is sized for (24 warps, 80 registers)
 #endif
 #ifndef SCR_GEN_WARPS
 #define SCR_GEN_WARPS 8
