@@ -54,6 +54,7 @@ def test_criterion_6_default_profile_modes(gpu_device):
         fs.close()
         s.close()
     raw, icp, ranked = (float(np.mean(rates[m])) for m in (0, 1, 2))
+    print(f"criterion 6 success raw {raw:.3f} icp {icp:.3f} ranked {ranked:.3f}")
     assert icp >= 0.95, rates
     assert ranked >= icp >= raw, rates
 
@@ -81,6 +82,7 @@ def test_criterion_9_cascade_fast_on_average(gpu_device):
         ft.close()
         fs.close()
         s.close()
+    print(f"criterion 9: stage 0 {st0}/{n}, cascade {t_c:.1f} ms vs slow {t_s:.1f} ms, success {np.mean(ok_c):.3f} vs {np.mean(ok_s):.3f}")
     assert st0 >= 0.8 * n, (st0, n)
     assert t_c < t_s, (t_c, t_s)
     assert np.mean(ok_c) >= np.mean(ok_s) - 0.02, (ok_c, ok_s)

@@ -105,3 +105,29 @@ def test_out_of_range_ransac_parameters_are_rejected(adapted):
     for bad in (dict(n_max=8192), dict(n_cull=128), dict(eta=1024)):
         with pytest.raises(N.ScrelocError):
             s.relocalise_batch(w.Dt[:1], w.RGBt[:1], P.ransac_params("fast", **bad), 1, [1])
+
+
+def test_wrong_sized_frames_raise_dimension_mismatch_at_the_abi(adapted):
+    """core.hpp:57 DimensionMismatch: a C caller handing a frame whose width/height differ
+    from the scene's intrinsics gets SCR_E_DIMENSION_MISMATCH before any pixel is read (the
+    Python mirror raises the same exception earlier); a null plane is SCR_E_ARG."""
+    import paper_1810_12163_b200 as P
+    from paper_1810_12163_b200 import native as N
+
+    w, s = adapted
+    d = np.ascontiguousarray(w.Dt[0][:, : K.width // 2], np.float32)
+    c = np.ascontiguousarray(w.RGBt[0][:, : K.width // 2], np.uint8)
+    fr = (N.Frame * 1)()
+    fr[0].depth, fr[0].rgb = d.ctypes.data, c.ctypes.data
+    fr[0].width, fr[0].height, fr[0].pose_reliable = K.width // 2, K.height, 1
+    p = P.ransac_params("fast")
+    sd = np.array([1], np.uint64)
+    out = (N.Result * 1)()
+    st = s.lib.scr_relocalise_batch(s.handle, fr, 1, C.byref(p), 1, N.ptr(sd, C.c_uint64), out)
+    assert st == 7  # SCR_E_DIMENSION_MISMATCH
+    pose = P.to_pose(w.adapt_poses[0])
+    assert s.lib.scr_train(s.handle, fr, C.byref(pose)) == 7
+    fr[0].width, fr[0].depth = K.width, None
+    assert s.lib.scr_relocalise_batch(s.handle, fr, 1, C.byref(p), 1, N.ptr(sd, C.c_uint64), out) == 1
+    with pytest.raises(N.DimensionMismatch):
+        s.relocalise_batch([d], [c], p, 1, [1])
