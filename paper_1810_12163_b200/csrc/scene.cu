@@ -363,6 +363,31 @@ __global__ void k_ins_commit(const uint32_t* __restrict__ key, const int* __rest
 // the nearest strictly-higher-density point within tau (ties: lower index), components by
 // pointer chasing, clusters of size >= min sorted by (size desc, root asc), top M_max,
 // mu / colour / Sigma + 1e-6 I in f64, Sigma^-1 and Sigma^-1/2 via 3x3 Jacobi.
+SCR_DEV uint32_t spread3_10(uint32_t v) {  // 10 bits -> every third bit of 30
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+SCR_DEV uint32_t morton3_10(uint32_t x, uint32_t y, uint32_t z) {
+  return spread3_10(x) | (spread3_10(y) << 1) | (spread3_10(z) << 2);
+}
+SCR_DEV void atomic_min_float(float* a, float v) {  // via the ordered int view (no NaNs here)
+  if (v >= 0.0f) atomicMin(reinterpret_cast<int*>(a), __float_as_int(v));
+  else atomicMax(reinterpret_cast<unsigned*>(a), __float_as_uint(v));
+}
+SCR_DEV void atomic_max_float(float* a, float v) {
+  if (v >= 0.0f) atomicMax(reinterpret_cast<int*>(a), __float_as_int(v));
+  else atomicMin(reinterpret_cast<unsigned*>(a), __float_as_uint(v));
+}
+SCR_DEV int rqs_pow2(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
 struct RqsParams {
   float c;       // -1 / (2 sigma^2), rounded once on the host
   float tau2;    // tau^2
@@ -373,6 +398,14 @@ struct RqsParams {
 #define SCR_RQS_THREADS 1024  // 4 rows per thread at kappa 4096: RQS 2.96 -> 1.43 ms per 256-leaf refresh (256 threads: 8 rows)
 #endif
 constexpr int kRqsThreads = SCR_RQS_THREADS;
+// shared memory of k_rqs: per entry x, y, z, colour, density, parent, root, size, rank
+// (40 B) + the 64-bit Morton sort keys (power-of-two count)
+inline size_t rqs_smem(int kappa) {
+  size_t p2 = 1;
+  while (p2 < static_cast<size_t>(kappa)) p2 <<= 1;
+  return ((static_cast<size_t>(kappa) * 40 + 7) & ~static_cast<size_t>(7)) + p2 * 8;
+}
+
 __global__ void __launch_bounds__(kRqsThreads) k_rqs(const scr_entry* __restrict__ entries, const uint32_t* __restrict__ seen,
                                              int64_t L, int64_t cursor, int nleaves, RqsParams rp,
                                              int* __restrict__ pcount, ModeGeom* __restrict__ pgeom,
@@ -413,36 +446,115 @@ __global__ void __launch_bounds__(kRqsThreads) k_rqs(const scr_entry* __restrict
   }
   if (threadIdx.x == 0) nroots = 0;
   __syncthreads();
-  // density
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float xi = sx[i], yi = sy[i], zi = sz[i];
+  // Rows are handed to threads in Morton order of their points (sorted (code, index) keys,
+  // perm[r] = index of the r-th point), so the 32 rows of a warp are spatially close. For a
+  // given j the warp then usually agrees that every exp(-|xi - xj|^2 / 2 sigma^2) underflows
+  // to exactly 0 (det_expf(x) = 0 for x <= -87, i.e. beyond 1.32 m at sigma = 0.1) and skips
+  // it: adding +0 leaves a sum unchanged, and each row is still summed in j order, so the
+  // densities are bit-identical to the sequential definition. The link pass skips j likewise
+  // when no row of the warp is within tau of it.
+  const int np2 = rqs_pow2(n);
+  unsigned long long* skey = reinterpret_cast<unsigned long long*>(
+      smem_raw + ((static_cast<size_t>(kappa) * 40 + 7) & ~static_cast<size_t>(7)));
+  {
+    __shared__ float s_box[6];
+    if (threadIdx.x == 0) {
+      s_box[0] = s_box[1] = s_box[2] = __int_as_float(0x7f800000);
+      s_box[3] = s_box[4] = s_box[5] = -__int_as_float(0x7f800000);
+    }
+    __syncthreads();
+    float lo[3] = {__int_as_float(0x7f800000), __int_as_float(0x7f800000), __int_as_float(0x7f800000)};
+    float hi[3] = {-lo[0], -lo[1], -lo[2]};
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      lo[0] = fminf(lo[0], sx[i]); hi[0] = fmaxf(hi[0], sx[i]);
+      lo[1] = fminf(lo[1], sy[i]); hi[1] = fmaxf(hi[1], sy[i]);
+      lo[2] = fminf(lo[2], sz[i]); hi[2] = fmaxf(hi[2], sz[i]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float l = lo[a], h = hi[a];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        l = fminf(l, __shfl_xor_sync(0xffffffffu, l, o));
+        h = fmaxf(h, __shfl_xor_sync(0xffffffffu, h, o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        atomic_min_float(&s_box[a], l);
+        atomic_max_float(&s_box[3 + a], h);
+      }
+    }
+    __syncthreads();
+    float scale[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float ext = s_box[3 + a] - s_box[a];
+      scale[a] = ext > 0.0f ? 1023.0f / ext : 0.0f;
+    }
+    for (int r = threadIdx.x; r < np2; r += blockDim.x) {
+      unsigned long long k = ~0ull;
+      if (r < n) {
+        const uint32_t qx = min(1023u, static_cast<uint32_t>(fmaxf(0.0f, (sx[r] - s_box[0]) * scale[0])));
+        const uint32_t qy = min(1023u, static_cast<uint32_t>(fmaxf(0.0f, (sy[r] - s_box[1]) * scale[1])));
+        const uint32_t qz = min(1023u, static_cast<uint32_t>(fmaxf(0.0f, (sz[r] - s_box[2]) * scale[2])));
+        k = (static_cast<unsigned long long>(morton3_10(qx, qy, qz)) << 32) | static_cast<unsigned>(r);
+      }
+      skey[r] = k;
+    }
+    __syncthreads();
+    for (int size2 = 2; size2 <= np2; size2 <<= 1)  // bitonic sort, ascending
+      for (int stride = size2 >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < (np2 >> 1); t += blockDim.x) {
+          const int lo_i = 2 * t - (t & (stride - 1));
+          const int hi_i = lo_i + stride;
+          const bool up = (lo_i & size2) == 0;
+          const unsigned long long a = skey[lo_i], b = skey[hi_i];
+          if ((a > b) == up) {
+            skey[lo_i] = b;
+            skey[hi_i] = a;
+          }
+        }
+        __syncthreads();
+      }
+  }
+  // density (f64 sum over j in index order)
+  for (int r0 = 0; r0 < n; r0 += blockDim.x) {  // uniform trip count: every lane votes
+    const int r = r0 + static_cast<int>(threadIdx.x);
+    const bool live = r < n;
+    const int i = live ? static_cast<int>(skey[r] & 0xffffffffu) : 0;
+    const float xi = live ? sx[i] : 1e18f, yi = live ? sy[i] : 1e18f, zi = live ? sz[i] : 1e18f;
     double acc = 0.0;
     for (int j = 0; j < n; ++j) {
       const float dx = __fsub_rn(xi, sx[j]), dy = __fsub_rn(yi, sy[j]), dz = __fsub_rn(zi, sz[j]);
       const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-      acc = acc + static_cast<double>(det_expf(__fmul_rn(d2, rp.c)));
+      const float x = __fmul_rn(d2, rp.c);
+      if (__any_sync(0xffffffffu, x > -87.0f)) acc = acc + static_cast<double>(det_expf(x));
     }
-    rho[i] = acc;
+    if (live) rho[i] = acc;
   }
   __syncthreads();
-  // link
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float xi = sx[i], yi = sy[i], zi = sz[i];
+  // link: nearest strictly-higher-density point within tau (ties: lower index)
+  for (int r0 = 0; r0 < n; r0 += blockDim.x) {
+    const int r = r0 + static_cast<int>(threadIdx.x);
+    const bool live = r < n;
+    const int i = live ? static_cast<int>(skey[r] & 0xffffffffu) : 0;
+    const float xi = live ? sx[i] : 1e18f, yi = live ? sy[i] : 1e18f, zi = live ? sz[i] : 1e18f;
     const double ri = rho[i];
     float best = __int_as_float(0x7f800000);
     int bj = -1;
     for (int j = 0; j < n; ++j) {
-      if (j == i) continue;
-      const double rj = rho[j];
-      if (!(rj > ri || (rj == ri && j < i))) continue;
       const float dx = __fsub_rn(xi, sx[j]), dy = __fsub_rn(yi, sy[j]), dz = __fsub_rn(zi, sz[j]);
       const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-      if (d2 <= rp.tau2 && d2 < best) {
+      const bool near = d2 <= rp.tau2;
+      if (!__any_sync(0xffffffffu, near)) continue;
+      if (!near || j == i) continue;
+      const double rj = rho[j];
+      if (!(rj > ri || (rj == ri && j < i))) continue;
+      if (d2 < best) {
         best = d2;
         bj = j;
       }
     }
-    parent[i] = bj;
+    if (live) parent[i] = bj;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1180,7 +1292,7 @@ static scr_status scr_update_impl(scr_scene s, int64_t leaves_per_call) {
   rp.min_size = s->fp.min_cluster_size;
   rp.max_clusters = s->fp.max_clusters;
   rp.kappa = s->fp.capacity;
-  const size_t smem = static_cast<size_t>(rp.kappa) * (4 * 4 + 8 + 4 * 4);
+  const size_t smem = rqs_smem(rp.kappa);
   for (int64_t done = 0; done < n; done += 65535) {
     const int chunk = static_cast<int>(std::min<int64_t>(65535, n - done));
     SCR_LAUNCH(s, K_RQS,
@@ -1217,7 +1329,7 @@ scr_status scr_debug_cluster(scr_scene s, const scr_entry* e, int n, scr_mode* o
   rp.min_size = s->fp.min_cluster_size;
   rp.max_clusters = s->fp.max_clusters;
   rp.kappa = s->fp.capacity;
-  const size_t smem = static_cast<size_t>(rp.kappa) * (4 * 4 + 8 + 4 * 4);
+  const size_t smem = rqs_smem(rp.kappa);
   k_rqs<<<1, kRqsThreads, smem, s->stream>>>(nullptr, nullptr, 1, 0, 1, rp, d_cnt, d_g, d_c, d_v, d_e, n, d_lab);
   SCR_CUDA(cudaGetLastError());
   SCR_CUDA(cudaStreamSynchronize(s->stream));
