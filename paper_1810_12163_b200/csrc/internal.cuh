@@ -72,14 +72,7 @@ struct Workspace {
   int* h_idx = nullptr;         // pinned [cap] stage frame list
   int* h_fsidx = nullptr;       // pinned [cap] frameset indices of a call
   uint64_t* h_seeds = nullptr;  // pinned [cap]
-  cudaEvent_t ev_stage[2] = {nullptr, nullptr};  // (unused since device-side stage control)
-  static constexpr int kMaxStages = 8;
-  cudaEvent_t ev_st[kMaxStages + 1] = {};  // stage boundaries of one cascade (no host sync between)
-  int* nact = nullptr;          // device [kMaxStages + 1]: active frames entering each stage
-  int* h_nact = nullptr;        // pinned mirror
-  int cur_stage = 0;            // stage whose active count the kernels read (frame_refs)
-  uint64_t* seeds0 = nullptr;   // [cap] per-frame cascade seeds (stage i uses stage_seed(seed, i))
-  scr_result* d_out = nullptr;  // [cap] per-frame results, filled stage by stage on the device
+  cudaEvent_t ev_stage[2] = {nullptr, nullptr};
   cudaEvent_t ev_upload = nullptr;
   int gmax = 0;   // grid pixels per frame
   float* depth = nullptr;     // staging for host uploads [cap * WH]

@@ -41,7 +41,6 @@ enum { kAttPass = 0, kAttNoModes = 1, kAttColour = 2, kAttTooClose = 3, kAttNotR
 
 struct FrameRefs {  // per-batch views of the packed frames
   const int* fidx;       // active index -> workspace slot
-  const int* nact;       // active frames of the current stage (device; grids are sized for the batch)
   const int* gcount;
   const int* gpx;
   const float4* gcam;
@@ -460,7 +459,6 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
   s_cur[wid][lane] = -1;
   __syncthreads();
   const int a = blockIdx.y;
-  if (a >= *fr.nact) return;  // frame not active in this stage (uniform over the CTA)
   const int f = fr.fidx[a];
   const uint64_t G = static_cast<uint64_t>(fr.gcount[f]);
   const uint64_t mG = G ? barrett_m(G) : 1, tG = G ? mod_barrett(0 - G, G, mG) : 0;
@@ -673,7 +671,6 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
   __shared__ int s_lbase[kMaxTrees];
   __shared__ int4 s_sus[kMaxSuspects][2];
   const int a = blockIdx.y;
-  if (a >= *fr.nact) return;
   const int slot = blockIdx.x * kFinThreads + threadIdx.x;
   const size_t out = static_cast<size_t>(a) * gp.nmax + slot;
   const int ns = min(sus_cnt[a], kMaxSuspects);
@@ -821,7 +818,7 @@ __global__ void k_draw_samples(FrameRefs fr, const uint64_t* __restrict__ seeds,
                                int scap, int* __restrict__ samples) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   const int batch = blockIdx.y;
-  if (a >= nA || a >= *fr.nact) return;
+  if (a >= nA) return;
   const uint64_t G = static_cast<uint64_t>(fr.gcount[fr.fidx[a]]);
   int* out = samples + static_cast<size_t>(a) * scap + static_cast<size_t>(batch) * eta;
   if (G == 0) {
@@ -872,13 +869,9 @@ constexpr int kCompactThreads = 1024;
 
 __global__ void __launch_bounds__(kCompactThreads) k_compact(const Pose* __restrict__ hyp, const int* __restrict__ hok,
                                                             int nmax, Pose* __restrict__ hypc, int* __restrict__ hslot,
-                                                            int* __restrict__ hvalid, const int* __restrict__ nact) {
+                                                            int* __restrict__ hvalid) {
   __shared__ int s_warp[kCompactThreads / 32];
   const int a = blockIdx.x;
-  if (a >= *nact) {  // inactive frame: no hypotheses, so every later kernel skips it
-    if (threadIdx.x == 0) hvalid[a] = 0;
-    return;
-  }
   const size_t base = static_cast<size_t>(a) * nmax;
   const int per = (nmax + kCompactThreads - 1) / kCompactThreads;  // consecutive slots per thread (<= 4)
   const int i0 = min(nmax, threadIdx.x * per), i1 = min(nmax, i0 + per);
@@ -2292,7 +2285,6 @@ namespace {
 FrameRefs frame_refs(scr_scene s) {
   FrameRefs fr;
   fr.fidx = s->ws.fidx;
-  fr.nact = s->ws.nact + s->ws.cur_stage;
   fr.gcount = s->ws.gcount;
   fr.gpx = s->ws.gpx;
   fr.gcam = s->ws.gcam;
@@ -2371,8 +2363,7 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
              (k_draw_samples<<<dim3((nA + 63) / 64, K + 1), 64, 0, s->stream>>>(fr, w.seeds, nA, p.n_max, p.eta,
                                                                                 w.samples_cap, w.samples)));
   SCR_LAUNCH(s, K_COMPACT,
-             (k_compact<<<nA, kCompactThreads, 0, s->stream>>>(w.hyp, w.hok, p.n_max, w.hypc, w.hslot, w.hvalid,
-                                                               fr.nact)));
+             (k_compact<<<nA, kCompactThreads, 0, s->stream>>>(w.hyp, w.hok, p.n_max, w.hypc, w.hslot, w.hvalid)));
   {
     EnergyArgs ea{w.hypc, nullptr, p.n_max, w.hvalid, 0, w.samples, w.samples_cap, p.eta, 0, w.henergy, 0};
     const size_t smem = static_cast<size_t>(kSmallHyps) * (p.eta + 1) * sizeof(float);
@@ -2556,104 +2547,47 @@ scr_status ensure_icp_ws(scr_scene s, int jobs) {
 }
 
 uint64_t stage_seed(uint64_t seed, int stage) { return seed + static_cast<uint64_t>(stage) * 0x9e3779b97f4a7c15ull; }
-SCR_DEV uint64_t stage_seed_dev(uint64_t seed, int stage) {
-  return seed + static_cast<uint64_t>(stage) * 0x9e3779b97f4a7c15ull;
-}
 
-// Device-side stage control: stage 0 takes every frame of the batch; after
-// each stage one CTA stores the stage's results per frame and compacts, in order, the frames
-// whose best score exceeds the stage's threshold into the next stage's active list (frame
-// slot and stage seed). The next stage's kernels read the active count on the device, so a
-// whole cascade is enqueued without a host round trip.
-constexpr int kStageThreads = 1024;
-__global__ void __launch_bounds__(kStageThreads) k_stage_init(int n, int* __restrict__ fidx,
-                                                               uint64_t* __restrict__ seeds,
-                                                               const uint64_t* __restrict__ seeds0,
-                                                               int* __restrict__ nact) {
-  for (int a = threadIdx.x; a < n; a += blockDim.x) {
-    fidx[a] = a;
-    seeds[a] = stage_seed_dev(seeds0[a], 0);
-  }
-  if (threadIdx.x == 0) nact[0] = n;
-}
-
-__global__ void __launch_bounds__(kStageThreads) k_stage_next(const scr_result* __restrict__ res,
-                                                               const int* __restrict__ nact_in, int* __restrict__ fidx,
-                                                               uint64_t* __restrict__ seeds,
-                                                               const uint64_t* __restrict__ seeds0, int st, int last,
-                                                               double thr, scr_result* __restrict__ out,
-                                                               int* __restrict__ nact_out) {
-  __shared__ int s_warp[kStageThreads / 32];
-  const int nA = *nact_in;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int base = 0;
-  for (int c0 = 0; c0 < nA; c0 += blockDim.x) {  // in place: a chunk is read before it is written
-    const int a = c0 + threadIdx.x;
-    bool go = false;
-    int f = 0;
-    if (a < nA) {
-      f = fidx[a];
-      scr_result r = res[a];
-      r.stage_used = st;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) r.stage_ms[k] = 0.0f;
-      out[f] = r;
-      go = !last && !(r.score <= thr);
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, go);
-    if (lane == 0) s_warp[wid] = __popc(bal);
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-      before += w < wid ? s_warp[w] : 0;
-      total += s_warp[w];
-    }
-    if (go) {
-      const int pos = base + before + __popc(bal & ((1u << lane) - 1u));
-      fidx[pos] = f;
-      seeds[pos] = stage_seed_dev(seeds0[f], st + 1);
-    }
-    base += total;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *nact_out = base;
-}
-
-// run_cascade for frames packed in workspace slots 0..n-1: every stage is
-// enqueued at once (grids sized for the batch, the kernels read the stage's active count),
-// one synchronisation at the end; per-stage device time from events between the stages.
+// run_cascade for frames packed in workspace slots 0..n-1.
 scr_status run_cascade(scr_scene s, int n, const scr_ransac_params* stages, const int32_t* modes, const double* thr,
                        int nstages, const uint64_t* seeds, scr_result* out) {
+  // Host control between stages only: stage i+1 takes the frames whose stage-i score exceeds
+  // the threshold. Staging buffers are pinned and allocated once per
+  // workspace, so a call makes no allocation and no implicit device synchronisation.
   Workspace& w = s->ws;
-  if (nstages > Workspace::kMaxStages) {
-    set_error("run_cascade: at most 8 stages");
-    return SCR_E_ARG;
+  std::vector<int> active(n);
+  for (int i = 0; i < n; ++i) active[i] = i;
+  std::vector<scr_result> res(n);
+  for (int st = 0; st < nstages && !active.empty(); ++st) {
+    const int nA = static_cast<int>(active.size());
+    for (int i = 0; i < nA; ++i) {
+      w.h_idx[i] = active[i];
+      w.h_seeds[i] = stage_seed(seeds[active[i]], st);
+    }
+    SCR_CUDA(cudaMemcpyAsync(w.fidx, w.h_idx, nA * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    SCR_CUDA(cudaMemcpyAsync(w.seeds, w.h_seeds, nA * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream));
+    cudaEventRecord(w.ev_stage[0], s->stream);
+    SCR_TRY(run_stage(s, nA, stages[st], modes[st], w.d_res));
+    cudaEventRecord(w.ev_stage[1], s->stream);
+    SCR_CUDA(cudaMemcpyAsync(w.h_res, w.d_res, nA * sizeof(scr_result), cudaMemcpyDeviceToHost, s->stream));
+    SCR_CUDA(cudaStreamSynchronize(s->stream));
+    prof_flush(s);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, w.ev_stage[0], w.ev_stage[1]);
+    std::vector<int> next;
+    for (int i = 0; i < nA; ++i) {
+      const int f = active[i];
+      float keep[4];
+      std::memcpy(keep, res[f].stage_ms, sizeof(keep));
+      res[f] = w.h_res[i];
+      std::memcpy(res[f].stage_ms, keep, sizeof(keep));
+      if (st < 4) res[f].stage_ms[st] = ms / nA;
+      res[f].stage_used = st;
+      if (st < nstages - 1 && !(w.h_res[i].score <= thr[st])) next.push_back(f);
+    }
+    active.swap(next);
   }
-  std::memcpy(w.h_seeds, seeds, n * sizeof(uint64_t));
-  SCR_CUDA(cudaMemcpyAsync(w.seeds0, w.h_seeds, n * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream));
-  SCR_LAUNCH(s, K_FINALIZE, (k_stage_init<<<1, kStageThreads, 0, s->stream>>>(n, w.fidx, w.seeds, w.seeds0, w.nact)));
-  for (int st = 0; st < nstages; ++st) {
-    w.cur_stage = st;
-    SCR_CUDA(cudaEventRecord(w.ev_st[st], s->stream));
-    SCR_TRY(run_stage(s, n, stages[st], modes[st], w.d_res));
-    const int last = st == nstages - 1;
-    SCR_LAUNCH(s, K_FINALIZE, (k_stage_next<<<1, kStageThreads, 0, s->stream>>>(
-                                  w.d_res, w.nact + st, w.fidx, w.seeds, w.seeds0, st, last, last ? 0.0 : thr[st],
-                                  w.d_out, w.nact + st + 1)));
-  }
-  w.cur_stage = 0;
-  SCR_CUDA(cudaEventRecord(w.ev_st[nstages], s->stream));
-  SCR_CUDA(cudaMemcpyAsync(w.h_res, w.d_out, n * sizeof(scr_result), cudaMemcpyDeviceToHost, s->stream));
-  SCR_CUDA(cudaMemcpyAsync(w.h_nact, w.nact, (nstages + 1) * sizeof(int), cudaMemcpyDeviceToHost, s->stream));
-  SCR_CUDA(cudaStreamSynchronize(s->stream));
-  prof_flush(s);
-  float ms[Workspace::kMaxStages] = {};
-  for (int st = 0; st < nstages; ++st) cudaEventElapsedTime(&ms[st], w.ev_st[st], w.ev_st[st + 1]);
-  for (int i = 0; i < n; ++i) {
-    scr_result r = w.h_res[i];
-    for (int st = 0; st <= r.stage_used && st < 4; ++st) r.stage_ms[st] = ms[st] / std::max(1, w.h_nact[st]);
-    out[i] = r;
-  }
+  std::memcpy(out, res.data(), n * sizeof(scr_result));
   return SCR_OK;
 }
 
@@ -2764,9 +2698,6 @@ scr_status scr_debug_ransac(scr_scene s, const scr_frame* f, const scr_ransac_pa
   SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, 1));
   const int zero = 0;
   SCR_CUDA(cudaMemcpyAsync(s->ws.fidx, &zero, sizeof(int), cudaMemcpyHostToDevice, s->stream));
-  const int one = 1;
-  s->ws.cur_stage = 0;
-  SCR_CUDA(cudaMemcpyAsync(s->ws.nact, &one, sizeof(int), cudaMemcpyHostToDevice, s->stream));
   SCR_CUDA(cudaMemcpyAsync(s->ws.seeds, &seed, sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream));
   scr_result* d_res = nullptr;
   SCR_CUDA(cudaMalloc(&d_res, sizeof(scr_result)));

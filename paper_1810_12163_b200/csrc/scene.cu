@@ -770,11 +770,6 @@ scr_status alloc_workspace(scr_scene s, int max_batch) {
   if ((st = dalloc(&w.grec, 2 * B * w.gmax)) != SCR_OK) return st;  // interleaved with the leaf ids
   if ((st = dalloc(&w.fidx, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return st;
-  if ((st = dalloc(&w.seeds0, B)) != SCR_OK) return st;
-  if ((st = dalloc(&w.d_out, B)) != SCR_OK) return st;
-  if ((st = dalloc(&w.nact, Workspace::kMaxStages + 1)) != SCR_OK) return st;
-  SCR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w.h_nact), (Workspace::kMaxStages + 1) * sizeof(int)));
-  for (auto& e : w.ev_st) SCR_CUDA(cudaEventCreate(&e));
   if ((st = dalloc(&w.status, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.hctr, 2 * B)) != SCR_OK) return st;  // slot counters, then suspect counts
   if ((st = dalloc(&w.d_res, B)) != SCR_OK) return st;
@@ -1056,11 +1051,6 @@ void scr_scene_destroy(scr_scene s) {
   if (s->published) cudaEventDestroy(s->published);
   for (cudaEvent_t e : {s->ws.ev_stage[0], s->ws.ev_stage[1], s->ws.ev_upload})
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : s->ws.ev_st)
-    if (e) cudaEventDestroy(e);
-  if (s->ws.h_nact) cudaFreeHost(s->ws.h_nact);
-  for (void* p : {static_cast<void*>(s->ws.seeds0), static_cast<void*>(s->ws.d_out), static_cast<void*>(s->ws.nact)})
-    if (p) cudaFree(p);
   for (void* h : {static_cast<void*>(s->ws.h_res), static_cast<void*>(s->ws.h_idx), static_cast<void*>(s->ws.h_fsidx),
                   static_cast<void*>(s->ws.h_seeds)})
     if (h) cudaFreeHost(h);
