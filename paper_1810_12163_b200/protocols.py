@@ -10,6 +10,8 @@ reference's bench_cli module, §4.1-4.3).
   runs on a lane of the scene, adaptation on the scene itself, so the lane always sees the
   last *published* prediction state.
 * `compute_novelty_bins` (§4.3).
+* `perturb_missing_depth`, `perturb_noisy_depth` (§A.4.1-A.4.2): the
+  depth perturbations of the robustness experiments (host-side, seeded numpy).
 
 Every relocalisation goes through the B200 library (`Scene` / lanes); this module only
 sequences calls and does the report arithmetic.
@@ -179,3 +181,26 @@ def compute_novelty_bins(test_poses, outcomes: Sequence[FrameOutcome], training_
     for key, o in zip(keys, outcomes):
         bins[int(key)].append(bool(o.success))
     return {b: (len(v), (sum(v) / len(v)) if v else math.nan) for b, v in bins.items()}
+
+
+def perturb_missing_depth(depth: np.ndarray, p: float, rng: np.random.Generator) -> np.ndarray:
+    """PAPER.md §A.4.1: draw r_i ~ U[0, 1] per pixel and set the pixel to 0 iff r_i <= p
+    (invalid pixels stay invalid)."""
+    if not (0.0 <= p <= 1.0):
+        raise ValueError("p must be in [0, 1]")
+    d = np.array(depth, np.float32, copy=True)
+    r = rng.random(d.shape)
+    d[r <= p] = 0.0
+    return d
+
+
+def perturb_noisy_depth(depth: np.ndarray, sigma: float, rng: np.random.Generator) -> np.ndarray:
+    """PAPER.md §A.4.2: d_i <- d_i + n_i d_i with n_i ~ N(0, sigma^2); invalid pixels stay
+    invalid."""
+    if sigma < 0:
+        raise ValueError("sigma must be >= 0")
+    d = np.array(depth, np.float32, copy=True)
+    valid = (d > 0) & (d <= 20.0) & np.isfinite(d)
+    n = rng.normal(0.0, sigma, d.shape).astype(np.float32) if sigma > 0 else np.zeros(d.shape, np.float32)
+    d[valid] = d[valid] + n[valid] * d[valid]
+    return d

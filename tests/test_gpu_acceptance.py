@@ -86,3 +86,57 @@ def test_criterion_9_cascade_fast_on_average(gpu_device):
     assert st0 >= 0.8 * n, (st0, n)
     assert t_c < t_s, (t_c, t_s)
     assert np.mean(ok_c) >= np.mean(ok_s) - 0.02, (ok_c, ok_s)
+
+
+def test_criterion_10_tracking_loss_recovery(gpu_device):
+    """Acceptance criterion 10 (§4.2 / Fig. 5): on a fresh synthetic
+    sequence, relocalising every frame with the forest adapted so far and then integrating it,
+    the first success comes within 10 frames and the windowed success after frame 50 is
+    >= 80 %."""
+    import paper_1810_12163_b200 as P
+    from paper_1810_12163_b200.protocols import run_tracking_loss_protocol, success_curve
+
+    k = P.intrinsics()
+    s = P.Scene(gpu_device, P.generate_random_forest(42), P.forest_params("cascade"), k, adapt_seed=7, max_batch=4)
+    s.set_model(P.generate_synthetic_scene(5, 20))
+    poses = P.generate_trajectory(5, 700, 0)[:80]
+    fs = P.FrameSet(s, 80)
+    fs.render(poses)
+    D, RGB = fs.download(0, 80)
+    fs.close()
+    cfg = P.CascadeConfig.paper_three_stage()
+    outs = run_tracking_loss_protocol(s, (list(D), list(RGB), poses), cfg, [500 + i for i in range(80)],
+                                      leaves_per_frame=8192)
+    first = next(i for i, o in enumerate(outs) if o is not None and o.success)
+    win = success_curve(outs[51:], window=20)
+    print(f"criterion 10: first success at frame {first}, windowed success after 50: min {win[-10:].min():.2f}, "
+          f"mean {np.mean([o.success for o in outs[51:]]):.2f}")
+    assert first <= 10
+    assert np.mean([o.success for o in outs[51:]]) >= 0.8
+    s.close()
+
+
+def test_criterion_11_perturbation_monotonicity(gpu_device):
+    """Acceptance criterion 11 (§A.4): success is non-increasing in the
+    missing-depth fraction p over {0, 0.5, 0.9} and in the depth noise sigma over
+    {0, 0.05, 0.1}; at p = 0.5 the post-ICP success stays >= 85 % of the p = 0 value."""
+    import paper_1810_12163_b200 as P
+    from paper_1810_12163_b200.protocols import perturb_missing_depth, perturb_noisy_depth
+
+    s, fs, ft, test = _world(gpu_device, 1, "default")
+    D, RGB = ft.download(0, 100)
+    cfg = P.CascadeConfig([P.ransac_params("default")], [1], [])
+    seeds = [3000 + i for i in range(100)]
+
+    def rate(depths):
+        return _success(s.run_cascade_batch(list(depths), list(RGB), cfg, seeds), test)
+
+    rng = np.random.default_rng(11)
+    miss = [rate([perturb_missing_depth(d, p, rng) for d in D]) for p in (0.0, 0.5, 0.9)]
+    noisy = [rate([perturb_noisy_depth(d, sg, rng) for d in D]) for sg in (0.0, 0.05, 0.1)]
+    print(f"criterion 11: missing {miss}, noise {noisy}")
+    assert miss[0] >= miss[1] >= miss[2] and noisy[0] >= noisy[1] >= noisy[2]
+    assert miss[1] >= 0.85 * miss[0]
+    ft.close()
+    fs.close()
+    s.close()

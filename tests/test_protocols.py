@@ -106,3 +106,23 @@ def test_headline_eval_matches_oracle(oracle, gpu_device):
             Rg, tg = of.pose_np(gt)
             assert (o.t_err, o.r_err) == pose_error(R, t, Rg, tg)
     assert rep.success_fraction >= 0.5
+
+
+def test_perturbation_kats():
+    """p = 0 leaves the frame unchanged, p = 0.5 masks half the pixels (binomial
+    bound on 1e6 pixels), sigma = 0.025 gives 2.5 % relative noise, invalid pixels stay
+    invalid."""
+    import numpy as np
+
+    from paper_1810_12163_b200.protocols import perturb_missing_depth, perturb_noisy_depth
+
+    rng = np.random.default_rng(0)
+    d = np.full((1000, 1000), 2.0, np.float32)
+    d[0, :10] = 0.0
+    assert np.array_equal(perturb_missing_depth(d, 0.0, rng), d)
+    m = perturb_missing_depth(d, 0.5, rng)
+    assert abs((m == 0).mean() - 0.5) < 0.002 + 1e-5
+    nz = perturb_noisy_depth(d, 0.025, rng)
+    assert np.all(nz[0, :10] == 0.0)
+    v = nz[1:] / 2.0 - 1.0
+    assert abs(v.std() - 0.025) < 0.025 * 0.02
