@@ -194,13 +194,13 @@ IcpResult icp_refine(const Scene& s, const Pose& init, const Frame& fr) {
         M[6 * a + a] = M[6 * a + a] + mu;
       }
       if (!chol6_solve(M, rhs, delta)) break;
-      T = compose(exp_se3(delta), T);
       // the level has converged once the Gauss-Newton step is below kIcpStopStep in every
-      // twist component (rad / m): further steps only move the pose within the f32 noise
-      // floor of the sums (A8)
+      // twist component (rad / m): such a step only moves the pose within the f32 noise floor
+      // of the sums, so it is not applied and the level ends (A8)
       double dmax = 0.0;
       for (int a = 0; a < 6; ++a) dmax = std::fmax(dmax, std::fabs(delta[a]));
       if (dmax < kIcpStopStep) break;
+      T = compose(exp_se3(delta), T);
     }
   }
   res.pose = T;

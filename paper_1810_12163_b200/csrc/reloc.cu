@@ -1835,16 +1835,18 @@ int icp_step(const double* tot, Pose* T) {
     M[6 * p + p] = M[6 * p + p] + mu;
   }
   if (!chol6(M, rhs, delta)) return 0;
+  // the level has converged once the step is below kIcpStopStep in every twist component:
+  // such a step only moves the pose within the f32 noise floor, so it is not applied and
+  // the level ends (A8)
+  double dmax = 0.0;
+#pragma unroll 1
+  for (int a = 0; a < 6; ++a) dmax = fmax(dmax, fabs(delta[a]));
+  if (dmax < kIcpStopStep) return 2;
   Pose D, Tn;
   exp_se3(delta, D);
   pose_compose(D, *T, Tn);
   *T = Tn;
-  // the level has converged once the step is below kIcpStopStep in every twist component
-  // (further steps only move the pose within the f32 noise floor; A8)
-  double dmax = 0.0;
-#pragma unroll 1
-  for (int a = 0; a < 6; ++a) dmax = fmax(dmax, fabs(delta[a]));
-  return dmax < kIcpStopStep ? 2 : 1;
+  return 1;
 }
 
 #ifndef SCR_ICP_PIX
@@ -1902,6 +1904,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
   __shared__ int ired[kIcpThreads / 32];
   __shared__ Pose Ts;           // current estimate (authoritative copy in CTA 0)
   __shared__ int stop_level;
+  __shared__ int moved0;  // the pose changed after the level-0 map was cast
   __shared__ unsigned char s_plist[256];
   __shared__ int s_pn;
   // ray tables and tile masks sized to the frame (dynamic shared memory): a smaller
@@ -1922,7 +1925,10 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
   const size_t WHf = static_cast<size_t>(g.W) * g.H;
   const float* dpl0 = fr.dplane + static_cast<size_t>(f) * (WHf + WHf / 4 + WHf / 16);
   uint2* map = maps + static_cast<size_t>(jl) * ia.map_stride;
-  if (threadIdx.x == 0) Ts = cand[cidx];
+  if (threadIdx.x == 0) {
+    Ts = cand[cidx];
+    moved0 = 0;
+  }
   __syncthreads();
   int last_inl = 0, last_valid = 0;
   double last_r2 = 0.0;
@@ -2112,7 +2118,9 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
             lstat[1] = valid_t;
             lstat_r2 = tot[27];
           }
-          stop_level = (inl_t < 6 || icp_step(tot, &Ts) != 1) ? 1 : 0;
+          const int stepped = inl_t < 6 ? 0 : icp_step(tot, &Ts);
+          stop_level = stepped != 1 ? 1 : 0;
+          if (level == 0 && stepped == 1) moved0 = 1;
         }
         __syncthreads();
         pbuf ^= 1;
@@ -2152,8 +2160,29 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
     for (int i = 0; i < 3; ++i) t[i] = static_cast<float>(Tf.t[i]);
     float sum = 0.0f;
     int mutual = 0, synth = 0;
-    if (work && rank == 0 && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(g.W * g.H));
     __syncthreads();
+    // With ICP on the analytic model, a final pose equal to the level-0 map's pose (level 0
+    // ended at its first step, A8) gives exactly the level-0 map's hits: the depth difference
+    // reads them instead of casting the 307 k rays again.
+    const bool reuse = !kTsdf && ia.do_icp && !moved0;
+    if (reuse) {
+      const int fdx = kIcpLanes % g.W, fdy = kIcpLanes / g.W;
+      const float invW = __fdiv_rn(1.0f, static_cast<float>(g.W));
+      int fx0, fy0;
+      divmod_w(lane_id, g.W, invW, fx0, fy0);
+      for (int p = lane_id; p < g.W * g.H; p += kIcpLanes, xy_advance(fx0, fy0, fdx, fdy, g.W)) {
+        const uint2 v = map[p];
+        if (v.y == 0xffffffffu) continue;
+        const float ht = __uint_as_float(v.x);
+        if (!depth_valid(ht)) continue;
+        ++synth;
+        const float dl = dpl0[p];
+        if (!depth_valid(dl)) continue;
+        ++mutual;
+        sum = __fadd_rn(sum, fabsf(__fsub_rn(dl, ht)));
+      }
+    } else {
+    if (work && rank == 0 && threadIdx.x == 0) atomicAdd(&work[W_RAYS], static_cast<unsigned long long>(g.W * g.H));
     fill_ray_tables(g.W, g.H, g.fx, g.fy, g.cx, g.cy, s_dcx, s_dcy);
     int npl = 0;
     if (!kTsdf) {
@@ -2194,6 +2223,7 @@ __global__ void __cluster_dims__(kIcpCtas, 1, 1) __launch_bounds__(kIcpThreads, 
       sum = __fadd_rn(sum, fabsf(__fsub_rn(dl, h.t)));
     }
     if (work) work_add(work, W_RAY_PRIMS, static_cast<unsigned>(tests));
+    }
     cta_reduce_f32<1>(&sum, red, part);
     const int mutual_c = cta_isum(mutual, ired);
     const int synth_c = cta_isum(synth, ired);
