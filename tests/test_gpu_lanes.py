@@ -116,3 +116,56 @@ def test_scenes_are_isolated(oracle, gpu_device, adapted):
         if r.has_pose:
             assert bytes(r.pose) == bytes(ref.pose)
     s2.close()
+
+
+def test_root_updates_never_tear_concurrent_lane_reads(oracle, gpu_device):
+    """ADVICE r1 / SPEC.md:407: while the root scene keeps rewriting its prediction table
+    (scr_load_predictions, two different adapted tables in turn), relocalisations on a lane
+    from another thread see one table or the other, never a mixture: every lane result equals
+    the result under table A or under table B (the scene's state lock orders readers and
+    writers)."""
+    import paper_1810_12163_b200 as P
+
+    w = OracleWorld(oracle, scene_seed=6, n_adapt=24, n_test=6)
+    s = gpu_scene(gpu_device, w)
+    s.integrate_frames(list(w.D[:12]), list(w.RGB[:12]), w.adapt_poses[:12])
+    s.update_leaves_round_robin(s.total_leaves)
+    ta = s.predictions()
+    s.integrate_frames(list(w.D[12:]), list(w.RGB[12:]), w.adapt_poses[12:])
+    s.update_leaves_round_robin(s.total_leaves)
+    tb = s.predictions()
+    lane = s.fork(8)
+    p = P.ransac_params("fast")
+    seeds = [70 + i for i in range(len(w.test_poses))]
+
+    def key(res):
+        return tuple(bytes(r.pose) if r.has_pose else b"-" for r in res)
+
+    s.load_predictions(*ta)
+    ref_a = key(lane.relocalise_batch(w.Dt, w.RGBt, p, 1, seeds))
+    s.load_predictions(*tb)
+    ref_b = key(lane.relocalise_batch(w.Dt, w.RGBt, p, 1, seeds))
+    assert ref_a != ref_b  # the two tables are distinguishable
+    stop = threading.Event()
+    errs = []
+
+    def writer():
+        try:
+            for _ in range(8):
+                s.load_predictions(*ta)
+                s.load_predictions(*tb)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+        finally:
+            stop.set()
+
+    seen = []
+    th = threading.Thread(target=writer)
+    th.start()
+    while not stop.is_set() or len(seen) < 3:
+        seen.append(key(lane.relocalise_batch(w.Dt, w.RGBt, p, 1, seeds)))
+    th.join()
+    assert not errs, errs
+    assert all(k in (ref_a, ref_b) for k in seen), "a lane read a half-written table"
+    lane.close()
+    s.close()
