@@ -77,6 +77,9 @@ struct Workspace {
   int gmax = 0;   // grid pixels per frame
   float* depth = nullptr;     // staging for host uploads [cap * WH]
   uint8_t* rgb = nullptr;     // [cap * WH * 3]
+  float* depth2 = nullptr;    // second staging buffer (calls with more than cap frames)
+  uint8_t* rgb2 = nullptr;
+  cudaEvent_t ev_upload2 = nullptr;
   uint2* tex = nullptr;       // packed texels [cap * WH]: {depth or 0, rgb|valid<<24}
   float* dplane = nullptr;    // live depth (or 0) per ICP pyramid level, dense: [cap][WH + WH/4 + WH/16]
   int* gcount = nullptr;      // [cap]

@@ -2658,21 +2658,35 @@ scr_status scr_cascade_batch(scr_scene s, const scr_frame* frames, int n, const 
   SCR_TRY(refresh_lane(s));
   const size_t WH = static_cast<size_t>(s->k.width) * s->k.height;
   SCR_TRY(check_frames(s, frames, n));
-  for (int b0 = 0; b0 < n; b0 += s->ws.cap) {
-    const int nb = std::min(s->ws.cap, n - b0);
-    {  // this call's frames, contiguous on the device's copy stream (staging is free: the
-       // previous call on this lane synchronised its stream)
-      std::lock_guard<std::mutex> lk(s->dev->copy_mu);
-      for (int i = 0; i < nb; ++i) {
-        const scr_frame& fr = frames[b0 + i];
-        SCR_CUDA(cudaMemcpyAsync(s->ws.depth + i * WH, fr.depth, WH * sizeof(float), cudaMemcpyHostToDevice,
-                                 s->dev->copy));
-        SCR_CUDA(cudaMemcpyAsync(s->ws.rgb + i * WH * 3, fr.rgb, WH * 3, cudaMemcpyHostToDevice, s->dev->copy));
-      }
-      SCR_CUDA(cudaEventRecord(s->ws.ev_upload, s->dev->copy));
+  Workspace& w = s->ws;
+  if (n > w.cap && !w.depth2) {  // second staging buffer: chunk j + 1 uploads while chunk j runs
+    SCR_CUDA(cudaMalloc(&w.depth2, static_cast<size_t>(w.cap) * WH * sizeof(float)));
+    SCR_CUDA(cudaMalloc(&w.rgb2, static_cast<size_t>(w.cap) * WH * 3));
+    SCR_CUDA(cudaEventCreateWithFlags(&w.ev_upload2, cudaEventDisableTiming));
+  }
+  // chunk j's frames, contiguous on the device's copy stream, into staging buffer j % 2
+  auto upload = [&](int j) -> scr_status {
+    const int b0 = j * w.cap, nb = std::min(w.cap, n - b0);
+    float* dd = (j & 1) ? w.depth2 : w.depth;
+    uint8_t* dc = (j & 1) ? w.rgb2 : w.rgb;
+    std::lock_guard<std::mutex> lk(s->dev->copy_mu);
+    for (int i = 0; i < nb; ++i) {
+      const scr_frame& fr = frames[b0 + i];
+      SCR_CUDA(cudaMemcpyAsync(dd + i * WH, fr.depth, WH * sizeof(float), cudaMemcpyHostToDevice, s->dev->copy));
+      SCR_CUDA(cudaMemcpyAsync(dc + i * WH * 3, fr.rgb, WH * 3, cudaMemcpyHostToDevice, s->dev->copy));
     }
-    SCR_CUDA(cudaStreamWaitEvent(s->stream, s->ws.ev_upload, 0));
-    SCR_TRY(pack_frames(s, s->ws.depth, s->ws.rgb, nullptr, nb));
+    SCR_CUDA(cudaEventRecord((j & 1) ? w.ev_upload2 : w.ev_upload, s->dev->copy));
+    return SCR_OK;
+  };
+  // staging is free on entry: the previous call on this lane synchronised its stream; buffer
+  // j % 2 is free again for chunk j + 2 once chunk j's cascade (which synchronises) is done
+  const int nchunks = (n + w.cap - 1) / w.cap;
+  if (nchunks > 0) SCR_TRY(upload(0));
+  for (int j = 0; j < nchunks; ++j) {
+    const int b0 = j * w.cap, nb = std::min(w.cap, n - b0);
+    SCR_CUDA(cudaStreamWaitEvent(s->stream, (j & 1) ? w.ev_upload2 : w.ev_upload, 0));
+    SCR_TRY(pack_frames(s, (j & 1) ? w.depth2 : w.depth, (j & 1) ? w.rgb2 : w.rgb, nullptr, nb));
+    if (j + 1 < nchunks) SCR_TRY(upload(j + 1));  // overlaps this chunk's cascade
     SCR_TRY(run_cascade(s, nb, stages, modes, thr, nstages, seeds + b0, out + b0));
   }
   return SCR_OK;

@@ -1049,8 +1049,10 @@ void scr_scene_destroy(scr_scene s) {
     s->tsdf_model = nullptr;
   }
   if (s->published) cudaEventDestroy(s->published);
-  for (cudaEvent_t e : {s->ws.ev_stage[0], s->ws.ev_stage[1], s->ws.ev_upload})
+  for (cudaEvent_t e : {s->ws.ev_stage[0], s->ws.ev_stage[1], s->ws.ev_upload, s->ws.ev_upload2})
     if (e) cudaEventDestroy(e);
+  for (void* p : {static_cast<void*>(s->ws.depth2), static_cast<void*>(s->ws.rgb2)})
+    if (p) cudaFree(p);
   for (void* h : {static_cast<void*>(s->ws.h_res), static_cast<void*>(s->ws.h_idx), static_cast<void*>(s->ws.h_fsidx),
                   static_cast<void*>(s->ws.h_seeds)})
     if (h) cudaFreeHost(h);
