@@ -259,3 +259,22 @@ def test_features_match_reference_golden(gpu_device):
         s.debug_features(depth, rgb, bad)
     gpx, _ = s.debug_leaves(depth, rgb)
     assert np.array_equal(gpx, G["grid_4"])
+
+
+def test_multi_chunk_calls_match_single_chunk(oracle, gpu_device, world):
+    """A call with more frames than the workspace holds runs in chunks whose uploads are
+    double-buffered (chunk j + 1 uploads while chunk j runs); results equal one-chunk calls."""
+    import paper_1810_12163_b200 as P
+
+    small = gpu_scene(gpu_device, world, max_batch=2)
+    small.integrate_frames(list(world.D), list(world.RGB), world.adapt_poses)
+    small.update_leaves_round_robin(small.total_leaves)
+    cfg = P.CascadeConfig.paper_three_stage()
+    n = len(world.test_poses)
+    seeds = [300 + i for i in range(n)]
+    chunked = small.run_cascade_batch(world.Dt, world.RGBt, cfg, seeds)  # chunks of <= 2 frames
+    single = [small.run_cascade_batch(world.Dt[i:i + 1], world.RGBt[i:i + 1], cfg, [seeds[i]])[0] for i in range(n)]
+    for a, b in zip(chunked, single):
+        assert a.stage_used == b.stage_used and a.has_pose == b.has_pose
+        assert bytes(a.pose) == bytes(b.pose) and (a.score == b.score or (np.isinf(a.score) and np.isinf(b.score)))
+    small.close()
