@@ -913,7 +913,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(const Pose* __restr
 
 // Lane l stages mode j0 + l of the sample into buf[3 l .. 3 l + 2] (coalesced fetch, one
 // L2 round trip per 32 modes); returns the global mode index it staged (-1 if none).
-SCR_DEV int stage_modes(const PredView& pv, const SampleModes& sm, int T, int nm, int j0, int lane, float4* buf) {
+SCR_DEV int stage_modes(const PredView& pv, const SampleModes& sm, int T, int nm, int j0, int lane, float4* buf,
+                        bool with_cov = true) {
   const int j = j0 + lane;
   if (j >= nm) return -1;
   // tree of mode j and the modes before it; the slot is selected in registers (a runtime
@@ -928,8 +929,10 @@ SCR_DEV int stage_modes(const PredView& pv, const SampleModes& sm, int T, int nm
   const int mi = slot * kMaxModes + (j - before);
   const ModeGeom& g = pv.geom[mi];
   buf[3 * lane + 0] = g.q0;
-  buf[3 * lane + 1] = g.q1;
-  buf[3 * lane + 2] = g.q2;
+  if (with_cov) {  // the Euclidean association (no prediction covariance) needs only mu
+    buf[3 * lane + 1] = g.q1;
+    buf[3 * lane + 2] = g.q2;
+  }
   return mi;
 }
 
@@ -1398,7 +1401,7 @@ __global__ void __launch_bounds__(256) k_lm_assoc(FrameRefs fr, PredView pv, LmA
     float4* wbuf = s_modes + wid * 96;
     int* wmi = s_mi + wid * 32;
     for (int j0 = 0; j0 < nm; j0 += 32) {
-      wmi[lane] = stage_modes(pv, sm, fr.T, nm, j0, lane, wbuf);
+      wmi[lane] = stage_modes(pv, sm, fr.T, nm, j0, lane, wbuf, la.use_cov != 0);
       __syncwarp();
       const int cnt = min(32, nm - j0);
       for (int m = 0; m < cnt; ++m) {
