@@ -47,11 +47,22 @@ def prims(bump: bool = True) -> np.ndarray:
             pa, pb = m(a), m(b)
             box(tuple(min(u, v) for u, v in zip(pa, pb)), tuple(max(u, v) for u, v in zip(pa, pb)), col, seed)
 
-        mbox((0.0, 0.9, 0.0), (0.6, 2.1, 1.2), cab, 21)
-        mbox((0.0, 1.2, 1.2), (0.4, 1.8, 1.6), top, 22)
-        mbox((0.0, 0.5, 0.8), (0.25, 0.8, 1.1), top, 23)
+        # a furnished niche: cabinet with drawers, objects on top, a picture and a shelf on the
+        # wall (flat colours, so A and B look exactly alike)
+        mbox((0.0, 0.9, 0.0), (0.6, 2.1, 1.0), cab, 21)
+        mbox((0.6, 1.0, 0.15), (0.63, 1.45, 0.45), (220.0, 200.0, 60.0), 24)   # drawer
+        mbox((0.6, 1.55, 0.15), (0.63, 2.0, 0.45), (60.0, 90.0, 200.0), 25)    # drawer
+        mbox((0.6, 1.0, 0.55), (0.63, 2.0, 0.85), (230.0, 120.0, 170.0), 26)   # drawer
+        mbox((0.1, 1.0, 1.0), (0.35, 1.25, 1.35), top, 22)                     # box on top
+        mbox((0.15, 1.4, 1.0), (0.3, 1.55, 1.55), (40.0, 40.0, 40.0), 27)      # tall thin box
+        mbox((0.05, 1.7, 1.0), (0.45, 2.05, 1.12), (240.0, 240.0, 120.0), 28)  # flat box
+        mbox((0.0, 1.1, 1.65), (0.03, 1.9, 2.1), (90.0, 50.0, 30.0), 29)       # picture frame
+        mbox((0.03, 1.2, 1.73), (0.04, 1.8, 2.02), (70.0, 200.0, 210.0), 30)   # picture
+        mbox((0.0, 0.3, 1.3), (0.3, 0.75, 1.35), (150.0, 100.0, 60.0), 31)     # shelf
+        mbox((0.05, 0.35, 1.35), (0.25, 0.5, 1.6), (200.0, 60.0, 60.0), 32)    # object on the shelf
+        mbox((0.0, 2.3, 0.0), (0.35, 2.65, 0.7), (120.0, 60.0, 160.0), 33)     # side box
     if bump:  # the asymmetry: a shallow panel of the wall's own colour beside alcove A
-        box((0.0, 2.2, 0.9), (0.15, 2.6, 1.5), wall_x, 13)
+        box((0.0, 2.3, 1.0), (0.15, 2.7, 1.6), wall_x, 13)
     out = np.zeros(len(rows), P.native.PRIM_DTYPE)
     for i, (t, a, b, col, cell, seed) in enumerate(rows):
         out[i] = (t, a, b, col, cell, seed)
