@@ -87,9 +87,6 @@ struct Workspace {
   float4* gcam = nullptr;     // [cap * gmax] camera point (f32 of the f64 backprojection)
   int* gslot = nullptr;       // [cap * gmax * T]
   int* gnm = nullptr;         // [cap * gmax] number of modes (union over trees)
-  uint32_t* cmask = nullptr;  // [cap * gmax * 8] colour-check bit per (grid pixel, predicted mode)
-  float cmask_thresh = -1.0f; // colour threshold the mask was built with (< 0: stale)
-  int packed = 0;             // frames packed by the last pack_frames
   int4* grec = nullptr;       // [cap * gmax * 2] 32-B pixel records: {x|y<<16, depth bits, rgb | nm<<24,
                               // 6-bit counts of trees 0..4} then the 16-bit leaf ids of trees 0..7
   // RANSAC (grown on demand)

@@ -48,7 +48,6 @@ struct FrameRefs {  // per-batch views of the packed frames
   const int* gnm;
   const int4* grec;    // interleaved 32-B pixel records: grec[2 i] = {x|y<<16, depth, rgb|nm<<24, counts},
   const uint4* gleaf;  // gleaf[2 i + 1] = 16-bit leaf ids (one sector per pixel)
-  const uint32_t* cmask;  // cmask[8 i + w] bit b: colour check of grid pixel i against its mode 32 w + b
   const uint2* tex;
   const float* dplane;  // per frame: level-0, level-1, level-2 live depth planes
   int gmax, T;
@@ -398,32 +397,6 @@ SCR_DEV int attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, co
   return colour_ok(col, pv.col[cc == 0 ? m0 : (cc == 1 ? m1 : m2)], gp.colour_thresh) ? kAttPass : kAttColour;
 }
 
-// Colour-check mask of the packed frames (fast path: <= 5 trees, 16-bit leaf ids): bit
-// (i, j) = colour_ok(rgb(i), colour(j-th predicted mode of grid pixel i)), the exact test the
-// attempt loop makes. Built once per batch and colour threshold, it serves
-// every stage: the attempts then load one word instead of a record and a mode colour.
-__global__ void k_colour_mask(FrameRefs fr, PredView pv, GenParams gp, uint32_t* __restrict__ cmask) {
-  __shared__ int s_lbase[kMaxTrees];
-  const float thresh = gp.colour_thresh;
-  if (threadIdx.x < kMaxTrees) s_lbase[threadIdx.x] = gp.leaf_base[threadIdx.x];
-  __syncthreads();
-  const int f = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int gi = t >> 3, w = t & 7;
-  if (gi >= fr.gcount[f]) return;
-  const size_t i = static_cast<size_t>(f) * fr.gmax + gi;
-  const int4 rec = fr.grec[2 * i];
-  const uint4 lv = fr.gleaf[2 * i + 1];
-  const int nm = static_cast<int>(static_cast<uint32_t>(rec.z) >> 24);
-  const uint32_t col = static_cast<uint32_t>(rec.z);
-  uint32_t bits = 0;
-  const int j1 = min(nm, 32 * w + 32);
-  for (int j = 32 * w; j < j1; ++j)
-    if (colour_ok(col, pv.col[mode_from_record(s_lbase, static_cast<uint32_t>(rec.w), lv, j)], thresh))
-      bits |= 1u << (j - 32 * w);
-  cmask[8 * i + w] = bits;
-}
-
 // Per-warp queue of colour-check survivors, evaluated 32 at a time at full SIMD width.
 // They get the f32 pre-filter and the exact f64 checks 2-3 here; Kabsch (a 3x3 f64 SVD) is
 // left to k_hypfin, which keeps the SVD's code and registers out of the attempt loop. A slot
@@ -556,11 +529,11 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
           const int gc = cc == 0 ? g0 : (cc == 1 ? g1 : g2);
           const uint64_t vc = cc == 0 ? v1 : (cc == 1 ? v3 : v5);
           const uint32_t nmc = cc == 0 ? nm0 : (cc == 1 ? nm1 : nm2);
+          const int4 Ac = fr.grec[2 * (fbase + gc)];
+          const uint4 Lc = fr.gleaf[2 * (fbase + gc) + 1];
           const uint32_t pc = mod_barrett32(vc, nmc, s_m[nmc]);
-          // colour check from the per-frame mask k_colour_mask built: one
-          // 4-byte load instead of record -> mode index -> mode colour
-          const uint32_t cw = fr.cmask[8 * (fbase + gc) + (pc >> 5)];
-          if ((cw >> (pc & 31u)) & 1u) {
+          const float4 mcol = pv.col[mode_from_record(s_lbase, static_cast<uint32_t>(Ac.w), Lc, static_cast<int>(pc))];
+          if (colour_ok(static_cast<uint32_t>(Ac.z), mcol, gp.colour_thresh)) {
             push = true;
             c.slot = slot;
             c.owner_att = lane | (it << 5);
@@ -2352,7 +2325,6 @@ FrameRefs frame_refs(scr_scene s) {
   fr.gnm = s->ws.gnm;
   fr.grec = s->ws.grec;
   fr.gleaf = reinterpret_cast<const uint4*>(s->ws.grec);
-  fr.cmask = s->ws.cmask;
   fr.tex = s->ws.tex;
   fr.dplane = s->ws.dplane;
   fr.gmax = s->ws.gmax;
@@ -2409,11 +2381,6 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
                (s->T <= 5 && s->leaves16) ? 1 : 0, s->gen_force_suspect, {0}};
   for (int t = 0; t < s->T && t < kMaxTrees; ++t) gp.leaf_base[t] = s->leaf_base[t];
   unsigned long long* wk = work_ptr(s);
-  if (gp.fast && !(w.cmask_thresh == p.colour_thresh)) {  // colour-check mask of the packed frames
-    SCR_LAUNCH(s, K_HYPGEN, (k_colour_mask<<<dim3((w.gmax * 8 + 255) / 256, w.packed), 256, 0, s->stream>>>(
-                                fr, pv, gp, w.cmask)));
-    w.cmask_thresh = p.colour_thresh;
-  }
   SCR_CUDA(cudaMemsetAsync(w.hctr, 0, nA * sizeof(int), s->stream));  // per-frame slot counters
   SCR_CUDA(cudaMemsetAsync(w.hctr + w.cap, 0, nA * sizeof(int), s->stream));  // per-frame suspect counts
   const int gen_threads = std::min(p.n_max, kGenThreadsPerFrame);

@@ -768,7 +768,6 @@ scr_status alloc_workspace(scr_scene s, int max_batch) {
   if ((st = dalloc(&w.gslot, B * w.gmax * s->T)) != SCR_OK) return st;
   if ((st = dalloc(&w.gnm, B * w.gmax)) != SCR_OK) return st;
   if ((st = dalloc(&w.grec, 2 * B * w.gmax)) != SCR_OK) return st;  // interleaved with the leaf ids
-  if ((st = dalloc(&w.cmask, 8 * B * w.gmax)) != SCR_OK) return st;
   if ((st = dalloc(&w.fidx, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.seeds, B)) != SCR_OK) return st;
   if ((st = dalloc(&w.status, B)) != SCR_OK) return st;
@@ -1063,7 +1062,7 @@ void scr_scene_destroy(scr_scene s) {
                   s->ws.gnm, s->ws.hyp, s->ws.henergy, s->ws.hok, s->ws.hcand, s->ws.sus, s->ws.hiters, s->ws.cand, s->ws.cenergy,
                   s->ws.cslot, s->ws.ncand, s->ws.samples, s->ws.assoc, s->ws.icp_map, s->ws.icp_pose,
                   s->ws.icp_score, s->ws.icp_conv, s->ws.icp_rms, s->ws.icp_inl, s->ws.fidx, s->ws.seeds,
-                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.dplane, s->ws.cmask, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_start, s->ws.ins_key, s->ws.ins_key_s, s->ws.ins_val, s->ws.ins_item,
+                  s->ws.status, s->ws.hctr, s->ws.epart, s->ws.grec, s->ws.dplane, s->ws.hypc, s->ws.hslot, s->ws.hvalid, s->ws.lmst, s->ws.ins_start, s->ws.ins_key, s->ws.ins_key_s, s->ws.ins_val, s->ws.ins_item,
                   s->ws.ins_tgt, s->ws.ins_key2, s->ws.ins_key2_s, s->ws.ins_val2, s->ws.ins_pos2, s->ws.ins_tmp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1170,8 +1169,6 @@ scr_status pack_frames(scr_scene s, const float* depth_base, const uint8_t* rgb_
                  s->forest_view(), s->geom, w.tex, w.gcount, w.gpx, w.gmax, w.gslot, w.gnm, w.gcam, w.grec,
                  s->d_count, work_ptr(s))));
   SCR_CUDA(cudaGetLastError());
-  w.packed = n;
-  w.cmask_thresh = -1.0f;  // the colour-check mask belongs to the previous frames
   return SCR_OK;
 }
 
