@@ -410,6 +410,9 @@ SCR_DEV int attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, co
 #ifndef SCR_GEN_WARPS
 #define SCR_GEN_WARPS 8
 #endif
+#ifndef SCR_GEN_SPEC
+#define SCR_GEN_SPEC 1  // draw an attempt's seven values at once (exact; see the attempt loop)
+#endif
 constexpr int kGenWarps = SCR_GEN_WARPS;  // warps per generation CTA
 constexpr int kGenQ = 64;
 constexpr int kMaxSuspects = 64;  // per frame: triplets whose Kabsch may be degenerate
@@ -505,11 +508,39 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
         // consumption (1, 3, 5 or 7 values) is known without touching global memory, and
         // only the colour-check pixel's record, leaf ids and mode colour are loaded.
         int g0, g1 = 0, g2 = 0, cc = 0;
-        uint32_t nm1 = 0, nm2 = 0;
+        uint32_t nm0, nm1 = 0, nm2 = 0;
         uint64_t v1 = 0, v3 = 0, v5 = 0;
         bool full = false;
+#if SCR_GEN_SPEC
+        // Speculative form of the same draws: every rejection threshold is below 2^32, so a
+        // value with a non-zero high word is always accepted, and an attempt whose three
+        // pixels all have modes consumes exactly seven values. Draw the seven at once (the
+        // state chain no longer waits on the shared-memory mode-count loads and branches)
+        // and fall back to the sequential draws from the saved state otherwise.
+        const Rng rs = rng;
+        const uint64_t x0 = rng_next(rng), x1 = rng_next(rng), x2 = rng_next(rng), x3 = rng_next(rng),
+                       x4 = rng_next(rng), x5 = rng_next(rng), x6 = rng_next(rng);
+        g0 = static_cast<int>(mod_barrett32(x0, G32, mG));
+        g1 = static_cast<int>(mod_barrett32(x2, G32, mG));
+        g2 = static_cast<int>(mod_barrett32(x4, G32, mG));
+        nm0 = s_nm[g0];
+        nm1 = s_nm[g1];
+        nm2 = s_nm[g2];
+        const bool hi = (x0 >> 32) != 0 && (x1 >> 32) != 0 && (x2 >> 32) != 0 && (x3 >> 32) != 0 &&
+                        (x4 >> 32) != 0 && (x5 >> 32) != 0 && (x6 >> 32) != 0;
+        if (hi && nm0 != 0 && nm1 != 0 && nm2 != 0) {
+          v1 = x1;
+          v3 = x3;
+          v5 = x5;
+          cc = static_cast<int>(mod_barrett32(x6, 3u, m3));
+          full = true;
+        } else {
+          rng = rs;
+          g1 = g2 = 0;
+          nm1 = nm2 = 0;
+#endif
         g0 = static_cast<int>(draw32(rng, G32, mG, tG));
-        const uint32_t nm0 = s_nm[g0];
+        nm0 = s_nm[g0];
         if (nm0) {
           v1 = draw_raw(rng, s_thr[nm0]);
           g1 = static_cast<int>(draw32(rng, G32, mG, tG));
@@ -525,6 +556,9 @@ __global__ void __launch_bounds__(kGenWarps * 32, SCR_HYPGEN_MINB) k_hypgen(GenP
             }
           }
         }
+#if SCR_GEN_SPEC
+        }
+#endif
         if (full) {
           const int gc = cc == 0 ? g0 : (cc == 1 ? g1 : g2);
           const uint64_t vc = cc == 0 ? v1 : (cc == 1 ? v3 : v5);
@@ -1585,6 +1619,9 @@ __device__ __noinline__ bool lm_solve(const double* acc, double lambda, double d
 constexpr int kLmInFlight = SCR_LM_INFLIGHT;  // sample gathers in flight per lane
 constexpr int kLmThreads = 128;  // canonical LM reduction lanes per candidate (4 warps)
 
+#ifndef SCR_LM_G1
+#define SCR_LM_G1 1  // 17-32 candidates: association with one candidate per lane
+#endif
 #ifndef SCR_LM_STEP_MINB
 #define SCR_LM_STEP_MINB 1
 #endif
@@ -2420,9 +2457,12 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
       const int nk = (p.n_cull + (1 << (k - 1)) - 1) >> (k - 1);
       for (int it = 0; it < 10; ++it) {
         const dim3 ag((ns + 7) / 8, nA);
-        if (nk > 16) {
+        if (nk > (SCR_LM_G1 ? 32 : 16)) {
           SCR_LAUNCH(s, K_LM, (k_lm_assoc<<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
                                                                      w.assoc, wk)));
+        } else if (nk > 16) {  // one candidate per lane (k_lm_assoc would idle its second set)
+          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<1><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
+                                                                          w.assoc, wk)));
         } else if (nk > 8) {
           SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<2><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
                                                                           w.assoc, wk)));
