@@ -1354,9 +1354,9 @@ SCR_DEV void lm_accum(const Pose& H, const double x[3], const LmMode& mg, bool u
 
 // LM state per (frame, candidate) lives in global memory so that each LM iteration can be
 // split into two well-shaped kernels:
-//  k_lm_assoc — warp per sample, lanes over hypotheses: nearest mode of H x (f32 metric of
-//               Eq. 5, or Euclidean without covariance) for every hypothesis that needs a
-//               fresh association; each mode is loaded once per warp (uniform load);
+//  k_lm_assoc_c — warp per sample: nearest mode of H x (f32 metric of Eq. 5, or Euclidean
+//               without covariance) for every hypothesis that needs a fresh association,
+//               over the compacted list of those hypotheses; modes staged 32 at a time;
 //  k_lm_step  — warp per hypothesis, lanes over samples in the canonical 32-lane order:
 //               normal equations with the frozen association, damped solve, trial
 //               energy, accept/reject (identical on every lane).
@@ -1375,101 +1375,6 @@ __global__ void k_lm_init(const int* __restrict__ ncand, int n_out, int cand_str
   st[static_cast<size_t>(a) * cand_stride + h] = s;
 }
 
-__global__ void __launch_bounds__(256) k_lm_assoc(FrameRefs fr, PredView pv, LmArgs la,
-                                                  const int* __restrict__ samples, const Pose* __restrict__ cand,
-                                                  const int* __restrict__ ncand, const LmState* __restrict__ st,
-                                                  int* __restrict__ assoc, unsigned long long* __restrict__ work) {
-  __shared__ float s_pose[kSmallHyps][12];
-  __shared__ int s_need[kSmallHyps];
-  __shared__ int s_any;
-  __shared__ float4 s_modes[8 * 96];
-  __shared__ int s_mi[8 * 32];
-  const int a = blockIdx.y;
-  const int n = ncand[a];
-  if (n <= la.n_out) return;
-  if (threadIdx.x == 0) s_any = 0;
-  __syncthreads();
-  for (int h = threadIdx.x; h < n; h += blockDim.x) {
-    const LmState ls = st[static_cast<size_t>(a) * la.cand_stride + h];
-    const int need = (!ls.done && ls.need_assoc) ? 1 : 0;
-    s_need[h] = need;
-    if (need) {
-      s_any = 1;
-      const Pose& P = cand[static_cast<size_t>(a) * la.cand_stride + h];
-#pragma unroll
-      for (int i = 0; i < 9; ++i) s_pose[h][i] = static_cast<float>(P.R[i]);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) s_pose[h][9 + i] = static_cast<float>(P.t[i]);
-    }
-  }
-  __syncthreads();
-  if (!s_any) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int s = blockIdx.x * (blockDim.x >> 5) + wid;
-  if (s >= la.ns) return;
-  const int h0 = lane, h1 = lane + 32;
-  const bool v0 = h0 < n && s_need[h0], v1 = h1 < n && s_need[h1];
-  const int f = fr.fidx[a];
-  const size_t gb = static_cast<size_t>(f) * fr.gmax + samples[static_cast<size_t>(a) * la.scap + s];
-  int best0 = -1, best1 = -1;
-  if (fr.gnm[gb] > 0 && __any_sync(0xffffffffu, v0 || v1)) {  // warp-uniform: lanes cooperate below
-    float R0[9], t0[3], R1[9], t1[3];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      R0[i] = v0 ? s_pose[h0][i] : 0.0f;
-      R1[i] = v1 ? s_pose[h1][i] : 0.0f;
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      t0[i] = v0 ? s_pose[h0][9 + i] : 0.0f;
-      t1[i] = v1 ? s_pose[h1][9 + i] : 0.0f;
-    }
-    const float4 c = fr.gcam[gb];
-    float y0[3], y1[3];
-    xform_f32(R0, t0, c.x, c.y, c.z, y0);
-    xform_f32(R1, t1, c.x, c.y, c.z, y1);
-    float q0b = 0.0f, q1b = 0.0f;
-    const int nm = fr.gnm[gb];
-    SampleModes sm;
-    sample_modes(fr, pv.count, gb, lane, sm);
-    float4* wbuf = s_modes + wid * 96;
-    int* wmi = s_mi + wid * 32;
-    for (int j0 = 0; j0 < nm; j0 += 32) {
-      wmi[lane] = stage_modes(pv, sm, fr.T, nm, j0, lane, wbuf, la.use_cov != 0);
-      __syncwarp();
-      const int cnt = min(32, nm - j0);
-      for (int m = 0; m < cnt; ++m) {
-        const float4 g0 = wbuf[3 * m];
-        const int mi = wmi[m];
-        float qa, qb;
-        const float a0 = __fsub_rn(y0[0], g0.x), a1 = __fsub_rn(y0[1], g0.y), a2 = __fsub_rn(y0[2], g0.z);
-        const float b0 = __fsub_rn(y1[0], g0.x), b1 = __fsub_rn(y1[1], g0.y), b2 = __fsub_rn(y1[2], g0.z);
-        if (la.use_cov) {
-          const float4 g1 = wbuf[3 * m + 1], g2 = wbuf[3 * m + 2];
-          qa = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, a0, a1, a2);
-          qb = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, b0, b1, b2);
-        } else {
-          qa = quad_eucl(a0, a1, a2);
-          qb = quad_eucl(b0, b1, b2);
-        }
-        if (best0 < 0 || qa < q0b) {  // first minimum wins ties
-          q0b = qa;
-          best0 = mi;
-        }
-        if (best1 < 0 || qb < q1b) {
-          q1b = qb;
-          best1 = mi;
-        }
-      }
-      __syncwarp();
-    }
-    if (work && lane == 0)
-      atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(fr.gnm[gb]) * static_cast<unsigned long long>(n));
-  }
-  if (v0) assoc[(static_cast<size_t>(a) * la.cand_stride + h0) * la.scap + s] = best0;
-  if (v1) assoc[(static_cast<size_t>(a) * la.cand_stride + h1) * la.scap + s] = best1;
-}
-
 // Global mode index of union position j of a sample's predicted modes (trees in order).
 SCR_DEV int union_mode(const SampleModes& sm, int T, int j) {
   int slot = sm.slot[0], before = 0;
@@ -1482,70 +1387,93 @@ SCR_DEV int union_mode(const SampleModes& sm, int T, int j) {
   return slot * kMaxModes + (j - before);
 }
 
-// k_lm_assoc for <= 32 / G candidates per frame (the later preemption steps): warp per
-// sample, a group of G lanes per candidate, the group's lanes stride the sample's modes and
-// the group min-reduces (quadratic form, union position) — the same mode as the sequential
-// first-minimum scan. Keeps every lane busy when only a few candidates remain (with lanes
-// over candidates, 2 candidates would leave 30 of 32 lanes idle).
-template <int G>
-__global__ void __launch_bounds__(256) k_lm_assoc_g(FrameRefs fr, PredView pv, LmArgs la,
+// Association over the candidates that need it (<= 64 per frame), compacted: only the
+// candidates of this frame with !done && need_assoc take part (after the first iteration most
+// have converged or had their step rejected). Warp per sample; with nn <= 32 of them, each
+// gets G = 32 / pow2ceil(nn) lanes that stride the staged modes and min-reduce (quadratic
+// form, union position); with nn > 32 every lane scans all modes for two of
+// them. Both give the sequential first minimum over union positions.
+__global__ void __launch_bounds__(256) k_lm_assoc_c(FrameRefs fr, PredView pv, LmArgs la,
                                                     const int* __restrict__ samples, const Pose* __restrict__ cand,
                                                     const int* __restrict__ ncand, const LmState* __restrict__ st,
                                                     int* __restrict__ assoc, unsigned long long* __restrict__ work) {
-  constexpr int NH = 32 / G;
-  __shared__ float s_pose[NH][12];
-  __shared__ int s_need[NH];
-  __shared__ int s_any;
+  __shared__ float s_pose[64][12];
+  __shared__ int s_list[64];
+  __shared__ int s_nn;
   __shared__ float4 s_modes[8 * 64];  // per warp: 32 staged modes x {mu + c00, c11 c22 2c01 2c02}
   __shared__ float s_c12[8 * 32];     // ... and 2c12
   const int a = blockIdx.y;
   const int n = ncand[a];
   if (n <= la.n_out) return;
-  if (threadIdx.x == 0) s_any = 0;
-  __syncthreads();
-  for (int h = threadIdx.x; h < NH; h += blockDim.x) {
-    int need = 0;
-    if (h < n) {
-      const LmState ls = st[static_cast<size_t>(a) * la.cand_stride + h];
-      need = (!ls.done && ls.need_assoc) ? 1 : 0;
-    }
-    s_need[h] = need;
-    if (need) {
-      s_any = 1;
-      const Pose& P = cand[static_cast<size_t>(a) * la.cand_stride + h];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid == 0) {  // ascending list of the candidates that need a fresh association
+    int need[2];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) s_pose[h][i] = static_cast<float>(P.R[i]);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) s_pose[h][9 + i] = static_cast<float>(P.t[i]);
+    for (int u = 0; u < 2; ++u) {
+      const int h = lane + 32 * u;
+      need[u] = 0;
+      if (h < n) {
+        const LmState ls = st[static_cast<size_t>(a) * la.cand_stride + h];
+        need[u] = (!ls.done && ls.need_assoc) ? 1 : 0;
+      }
     }
+    const unsigned b0 = __ballot_sync(0xffffffffu, need[0]), b1 = __ballot_sync(0xffffffffu, need[1]);
+    const unsigned below = (1u << lane) - 1u;
+    if (need[0]) s_list[__popc(b0 & below)] = lane;
+    if (need[1]) s_list[__popc(b0) + __popc(b1 & below)] = lane + 32;
+    if (lane == 0) s_nn = __popc(b0) + __popc(b1);
   }
   __syncthreads();
-  if (!s_any) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nn = s_nn;
+  if (nn == 0) return;
+  for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+    const Pose& P = cand[static_cast<size_t>(a) * la.cand_stride + s_list[i]];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) s_pose[i][k] = static_cast<float>(P.R[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s_pose[i][9 + k] = static_cast<float>(P.t[k]);
+  }
+  __syncthreads();
   const int s = blockIdx.x * (blockDim.x >> 5) + wid;
   if (s >= la.ns) return;
-  const int h = lane / G, sub = lane % G;
-  const bool v = s_need[h] != 0;
   const int f = fr.fidx[a];
   const size_t gb = static_cast<size_t>(f) * fr.gmax + samples[static_cast<size_t>(a) * la.scap + s];
   const int nm = fr.gnm[gb];
-  int bj = 0x7fffffff, bmi = -1;
-  if (nm > 0 && __any_sync(0xffffffffu, v)) {  // warp-uniform
-    SampleModes sm;
+  const bool two = nn > 32;
+  int G = 1;
+  if (!two)
+    while (G * 2 * nn <= 32) G *= 2;
+  const int h = two ? lane : lane / G, sub = two ? 0 : lane % G;
+  const bool v = h < nn, v2 = two && lane + 32 < nn;
+  int bj = 0x7fffffff, bj2 = 0x7fffffff, bmi = -1, bmi2 = -1;
+  SampleModes sm;
+  if (nm > 0) {  // warp-uniform
     sample_modes(fr, pv.count, gb, lane, sm);
-    float bq = 0.0f;
-    float R[9], t[3], y[3];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) R[i] = s_pose[h][i];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) t[i] = s_pose[h][9 + i];
     const float4 c = fr.gcam[gb];
-    xform_f32(R, t, c.x, c.y, c.z, y);
+    float y[3], y2[3];
+    {
+      const int hh = v ? h : 0;
+      float R[9], t[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) R[i] = s_pose[hh][i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) t[i] = s_pose[hh][9 + i];
+      xform_f32(R, t, c.x, c.y, c.z, y);
+    }
+    if (two) {
+      const int hh = v2 ? lane + 32 : 0;
+      float R[9], t[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) R[i] = s_pose[hh][i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) t[i] = s_pose[hh][9 + i];
+      xform_f32(R, t, c.x, c.y, c.z, y2);
+    }
+    float bq = 0.0f, bq2 = 0.0f;
     float4* wbuf = s_modes + wid * 64;
     float* wc12 = s_c12 + wid * 32;
     for (int j0 = 0; j0 < nm; j0 += 32) {
-      // lane l stages mode j0 + l (one coalesced round trip per 32 modes)
-      const int jl = j0 + lane;
+      const int jl = j0 + lane;  // lane l stages mode j0 + l
       if (jl < nm) {
         const int mi = union_mode(sm, fr.T, jl);
         wbuf[2 * lane] = pv.geom[mi].q0;
@@ -1556,7 +1484,31 @@ __global__ void __launch_bounds__(256) k_lm_assoc_g(FrameRefs fr, PredView pv, L
       }
       __syncwarp();
       const int cnt = min(32, nm - j0);
-      if (v) {
+      if (two) {
+        for (int jj = 0; jj < cnt; ++jj) {
+          const float4 g0 = wbuf[2 * jj];
+          const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
+          const float e0 = __fsub_rn(y2[0], g0.x), e1 = __fsub_rn(y2[1], g0.y), e2 = __fsub_rn(y2[2], g0.z);
+          float q, q2;
+          if (la.use_cov) {
+            const float4 g1 = wbuf[2 * jj + 1];
+            const float c12 = wc12[jj];
+            q = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, c12, d0, d1, d2);
+            q2 = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, c12, e0, e1, e2);
+          } else {
+            q = quad_eucl(d0, d1, d2);
+            q2 = quad_eucl(e0, e1, e2);
+          }
+          if (bj == 0x7fffffff || q < bq) {
+            bq = q;
+            bj = j0 + jj;
+          }
+          if (bj2 == 0x7fffffff || q2 < bq2) {
+            bq2 = q2;
+            bj2 = j0 + jj;
+          }
+        }
+      } else if (v) {
         for (int jj = sub; jj < cnt; jj += G) {
           const float4 g0 = wbuf[2 * jj];
           const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
@@ -1575,8 +1527,7 @@ __global__ void __launch_bounds__(256) k_lm_assoc_g(FrameRefs fr, PredView pv, L
       }
       __syncwarp();
     }
-#pragma unroll
-    for (int off = G / 2; off >= 1; off >>= 1) {  // stays inside the aligned G-lane group
+    for (int off = two ? 0 : G >> 1; off >= 1; off >>= 1) {  // stays inside the aligned G-lane group
       const float oq = __shfl_xor_sync(0xffffffffu, bq, off);
       const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
       if (oj != 0x7fffffff && (bj == 0x7fffffff || oq < bq || (oq == bq && oj < bj))) {
@@ -1585,13 +1536,12 @@ __global__ void __launch_bounds__(256) k_lm_assoc_g(FrameRefs fr, PredView pv, L
       }
     }
     if (bj != 0x7fffffff) bmi = union_mode(sm, fr.T, bj);
-    if (work && lane == 0) {
-      int nv = 0;
-      for (int hh = 0; hh < NH; ++hh) nv += s_need[hh];
-      atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(nm) * static_cast<unsigned long long>(nv));
-    }
+    if (bj2 != 0x7fffffff) bmi2 = union_mode(sm, fr.T, bj2);
+    if (work && lane == 0)
+      atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(nm) * static_cast<unsigned long long>(nn));
   }
-  if (v && sub == 0) assoc[(static_cast<size_t>(a) * la.cand_stride + h) * la.scap + s] = bmi;
+  if (v && sub == 0) assoc[(static_cast<size_t>(a) * la.cand_stride + s_list[h]) * la.scap + s] = bmi;
+  if (v2) assoc[(static_cast<size_t>(a) * la.cand_stride + s_list[lane + 32]) * la.scap + s] = bmi2;
 }
 
 // One LM iteration of one hypothesis, all lanes in lockstep.
@@ -1619,9 +1569,6 @@ __device__ __noinline__ bool lm_solve(const double* acc, double lambda, double d
 constexpr int kLmInFlight = SCR_LM_INFLIGHT;  // sample gathers in flight per lane
 constexpr int kLmThreads = 128;  // canonical LM reduction lanes per candidate (4 warps)
 
-#ifndef SCR_LM_G1
-#define SCR_LM_G1 1  // 17-32 candidates: association with one candidate per lane
-#endif
 #ifndef SCR_LM_STEP_MINB
 #define SCR_LM_STEP_MINB 1
 #endif
@@ -2457,28 +2404,8 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
       const int nk = (p.n_cull + (1 << (k - 1)) - 1) >> (k - 1);
       for (int it = 0; it < 10; ++it) {
         const dim3 ag((ns + 7) / 8, nA);
-        if (nk > (SCR_LM_G1 ? 32 : 16)) {
-          SCR_LAUNCH(s, K_LM, (k_lm_assoc<<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
+        SCR_LAUNCH(s, K_LM, (k_lm_assoc_c<<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
                                                                      w.assoc, wk)));
-        } else if (nk > 16) {  // one candidate per lane (k_lm_assoc would idle its second set)
-          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<1><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
-                                                                          w.assoc, wk)));
-        } else if (nk > 8) {
-          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<2><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
-                                                                          w.assoc, wk)));
-        } else if (nk > 4) {
-          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<4><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
-                                                                          w.assoc, wk)));
-        } else if (nk > 2) {
-          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<8><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
-                                                                          w.assoc, wk)));
-        } else if (nk > 1) {
-          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<16><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand,
-                                                                           lmst, w.assoc, wk)));
-        } else {
-          SCR_LAUNCH(s, K_LM, (k_lm_assoc_g<32><<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand,
-                                                                           lmst, w.assoc, wk)));
-        }
         SCR_LAUNCH(s, K_LM, (k_lm_step<<<dim3(nk, nA), kLmThreads, 0, s->stream>>>(
                                 fr, pv, la, w.samples, w.cand, w.ncand, lmst, w.assoc, wk)));
       }
