@@ -1387,13 +1387,76 @@ SCR_DEV int union_mode(const SampleModes& sm, int T, int j) {
   return slot * kMaxModes + (j - before);
 }
 
+// Quadratic form of staged mode jj at point y (Eq. 5 metric, or Euclidean).
+template <bool kCov>
+SCR_DEV float assoc_q(const float4* wbuf, const float* wc12, int jj, const float* y) {
+  const float4 g0 = wbuf[2 * jj];
+  const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
+  if (kCov) {
+    const float4 g1 = wbuf[2 * jj + 1];
+    return quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, wc12[jj], d0, d1, d2);
+  }
+  return quad_eucl(d0, d1, d2);
+}
+// One staged chunk of the first-minimum scans. A lane's first evaluated mode is taken
+// unconditionally (whatever its value, as the sequential scan does), later ones on q < best.
+template <bool kCov>
+SCR_DEV void assoc_chunk_two(const float4* wbuf, const float* wc12, int j0, int cnt, const float* y, const float* y2,
+                             float& bq, int& bj, float& bq2, int& bj2) {
+  int jj = 0;
+  if (j0 == 0) {
+    bq = assoc_q<kCov>(wbuf, wc12, 0, y);
+    bq2 = assoc_q<kCov>(wbuf, wc12, 0, y2);
+    bj = bj2 = 0;
+    jj = 1;
+  }
+#pragma unroll 4
+  for (; jj < cnt; ++jj) {
+    const float q = assoc_q<kCov>(wbuf, wc12, jj, y), q2 = assoc_q<kCov>(wbuf, wc12, jj, y2);
+    if (q < bq) {
+      bq = q;
+      bj = j0 + jj;
+    }
+    if (q2 < bq2) {
+      bq2 = q2;
+      bj2 = j0 + jj;
+    }
+  }
+}
+template <bool kCov>
+SCR_DEV void assoc_chunk_g(const float4* wbuf, const float* wc12, int j0, int cnt, int sub, int G, const float* y,
+                           float& bq, int& bj) {
+  int jj = sub;
+  if (j0 == 0 && jj < cnt) {
+    bq = assoc_q<kCov>(wbuf, wc12, jj, y);
+    bj = jj;
+    jj += G;
+  }
+#pragma unroll 4
+  for (; jj < cnt; jj += G) {
+    const float q = assoc_q<kCov>(wbuf, wc12, jj, y);
+    if (q < bq) {
+      bq = q;
+      bj = j0 + jj;
+    }
+  }
+}
+
+#ifndef SCR_ASSOC_SPW
+#define SCR_ASSOC_SPW 8
+#endif
+constexpr int kAssocSpw = SCR_ASSOC_SPW;  // samples per warp in k_lm_assoc_c
+#ifndef SCR_ASSOC_MINB
+#define SCR_ASSOC_MINB 4  // 64 registers, 32 warps per SM: the association is latency-bound
+#endif
+
 // Association over the candidates that need it (<= 64 per frame), compacted: only the
 // candidates of this frame with !done && need_assoc take part (after the first iteration most
 // have converged or had their step rejected). Warp per sample; with nn <= 32 of them, each
 // gets G = 32 / pow2ceil(nn) lanes that stride the staged modes and min-reduce (quadratic
 // form, union position); with nn > 32 every lane scans all modes for two of
 // them. Both give the sequential first minimum over union positions.
-__global__ void __launch_bounds__(256) k_lm_assoc_c(FrameRefs fr, PredView pv, LmArgs la,
+__global__ void __launch_bounds__(256, SCR_ASSOC_MINB) k_lm_assoc_c(FrameRefs fr, PredView pv, LmArgs la,
                                                     const int* __restrict__ samples, const Pose* __restrict__ cand,
                                                     const int* __restrict__ ncand, const LmState* __restrict__ st,
                                                     int* __restrict__ assoc, unsigned long long* __restrict__ work) {
@@ -1434,114 +1497,82 @@ __global__ void __launch_bounds__(256) k_lm_assoc_c(FrameRefs fr, PredView pv, L
     for (int k = 0; k < 3; ++k) s_pose[i][9 + k] = static_cast<float>(P.t[k]);
   }
   __syncthreads();
-  const int s = blockIdx.x * (blockDim.x >> 5) + wid;
-  if (s >= la.ns) return;
   const int f = fr.fidx[a];
-  const size_t gb = static_cast<size_t>(f) * fr.gmax + samples[static_cast<size_t>(a) * la.scap + s];
-  const int nm = fr.gnm[gb];
   const bool two = nn > 32;
   int G = 1;
   if (!two)
     while (G * 2 * nn <= 32) G *= 2;
   const int h = two ? lane : lane / G, sub = two ? 0 : lane % G;
   const bool v = h < nn, v2 = two && lane + 32 < nn;
-  int bj = 0x7fffffff, bj2 = 0x7fffffff, bmi = -1, bmi2 = -1;
-  SampleModes sm;
-  if (nm > 0) {  // warp-uniform
-    sample_modes(fr, pv.count, gb, lane, sm);
-    const float4 c = fr.gcam[gb];
-    float y[3], y2[3];
-    {
-      const int hh = v ? h : 0;
-      float R[9], t[3];
-#pragma unroll
-      for (int i = 0; i < 9; ++i) R[i] = s_pose[hh][i];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) t[i] = s_pose[hh][9 + i];
-      xform_f32(R, t, c.x, c.y, c.z, y);
-    }
-    if (two) {
-      const int hh = v2 ? lane + 32 : 0;
-      float R[9], t[3];
-#pragma unroll
-      for (int i = 0; i < 9; ++i) R[i] = s_pose[hh][i];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) t[i] = s_pose[hh][9 + i];
-      xform_f32(R, t, c.x, c.y, c.z, y2);
-    }
-    float bq = 0.0f, bq2 = 0.0f;
-    float4* wbuf = s_modes + wid * 64;
-    float* wc12 = s_c12 + wid * 32;
-    for (int j0 = 0; j0 < nm; j0 += 32) {
-      const int jl = j0 + lane;  // lane l stages mode j0 + l
-      if (jl < nm) {
-        const int mi = union_mode(sm, fr.T, jl);
-        wbuf[2 * lane] = pv.geom[mi].q0;
-        if (la.use_cov) {
-          wbuf[2 * lane + 1] = pv.geom[mi].q1;
-          wc12[lane] = pv.geom[mi].q2.x;
-        }
+  // each warp takes samples s, s + 8 * gridDim.x, ... (the candidate list and poses above
+  // are set up once per CTA for several samples)
+  for (int s = blockIdx.x * (blockDim.x >> 5) + wid; s < la.ns; s += gridDim.x * (blockDim.x >> 5)) {
+    const size_t gb = static_cast<size_t>(f) * fr.gmax + samples[static_cast<size_t>(a) * la.scap + s];
+    const int nm = fr.gnm[gb];
+    int bj = 0x7fffffff, bj2 = 0x7fffffff, bmi = -1, bmi2 = -1;
+    SampleModes sm;
+    if (nm > 0) {  // warp-uniform
+      sample_modes(fr, pv.count, gb, lane, sm);
+      const float4 c = fr.gcam[gb];
+      float y[3], y2[3];
+      {
+        const int hh = v ? h : 0;
+        float R[9], t[3];
+  #pragma unroll
+        for (int i = 0; i < 9; ++i) R[i] = s_pose[hh][i];
+  #pragma unroll
+        for (int i = 0; i < 3; ++i) t[i] = s_pose[hh][9 + i];
+        xform_f32(R, t, c.x, c.y, c.z, y);
       }
-      __syncwarp();
-      const int cnt = min(32, nm - j0);
       if (two) {
-        for (int jj = 0; jj < cnt; ++jj) {
-          const float4 g0 = wbuf[2 * jj];
-          const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
-          const float e0 = __fsub_rn(y2[0], g0.x), e1 = __fsub_rn(y2[1], g0.y), e2 = __fsub_rn(y2[2], g0.z);
-          float q, q2;
+        const int hh = v2 ? lane + 32 : 0;
+        float R[9], t[3];
+  #pragma unroll
+        for (int i = 0; i < 9; ++i) R[i] = s_pose[hh][i];
+  #pragma unroll
+        for (int i = 0; i < 3; ++i) t[i] = s_pose[hh][9 + i];
+        xform_f32(R, t, c.x, c.y, c.z, y2);
+      }
+      float bq = 0.0f, bq2 = 0.0f;
+      float4* wbuf = s_modes + wid * 64;
+      float* wc12 = s_c12 + wid * 32;
+      for (int j0 = 0; j0 < nm; j0 += 32) {
+        const int jl = j0 + lane;  // lane l stages mode j0 + l
+        if (jl < nm) {
+          const int mi = union_mode(sm, fr.T, jl);
+          wbuf[2 * lane] = pv.geom[mi].q0;
           if (la.use_cov) {
-            const float4 g1 = wbuf[2 * jj + 1];
-            const float c12 = wc12[jj];
-            q = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, c12, d0, d1, d2);
-            q2 = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, c12, e0, e1, e2);
-          } else {
-            q = quad_eucl(d0, d1, d2);
-            q2 = quad_eucl(e0, e1, e2);
-          }
-          if (bj == 0x7fffffff || q < bq) {
-            bq = q;
-            bj = j0 + jj;
-          }
-          if (bj2 == 0x7fffffff || q2 < bq2) {
-            bq2 = q2;
-            bj2 = j0 + jj;
+            wbuf[2 * lane + 1] = pv.geom[mi].q1;
+            wc12[lane] = pv.geom[mi].q2.x;
           }
         }
-      } else if (v) {
-        for (int jj = sub; jj < cnt; jj += G) {
-          const float4 g0 = wbuf[2 * jj];
-          const float d0 = __fsub_rn(y[0], g0.x), d1 = __fsub_rn(y[1], g0.y), d2 = __fsub_rn(y[2], g0.z);
-          float q;
-          if (la.use_cov) {
-            const float4 g1 = wbuf[2 * jj + 1];
-            q = quad_icov(g0.w, g1.x, g1.y, g1.z, g1.w, wc12[jj], d0, d1, d2);
-          } else {
-            q = quad_eucl(d0, d1, d2);
-          }
-          if (bj == 0x7fffffff || q < bq) {  // first minimum of this lane's (increasing) positions
-            bq = q;
-            bj = j0 + jj;
-          }
+        __syncwarp();
+        const int cnt = min(32, nm - j0);
+        if (two) {
+          if (la.use_cov) assoc_chunk_two<true>(wbuf, wc12, j0, cnt, y, y2, bq, bj, bq2, bj2);
+          else assoc_chunk_two<false>(wbuf, wc12, j0, cnt, y, y2, bq, bj, bq2, bj2);
+        } else if (v) {
+          if (la.use_cov) assoc_chunk_g<true>(wbuf, wc12, j0, cnt, sub, G, y, bq, bj);
+          else assoc_chunk_g<false>(wbuf, wc12, j0, cnt, sub, G, y, bq, bj);
+        }
+        __syncwarp();
+      }
+      for (int off = two ? 0 : G >> 1; off >= 1; off >>= 1) {  // stays inside the aligned G-lane group
+        const float oq = __shfl_xor_sync(0xffffffffu, bq, off);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
+        if (oj != 0x7fffffff && (bj == 0x7fffffff || oq < bq || (oq == bq && oj < bj))) {
+          bq = oq;
+          bj = oj;
         }
       }
-      __syncwarp();
+      if (bj != 0x7fffffff) bmi = union_mode(sm, fr.T, bj);
+      if (bj2 != 0x7fffffff) bmi2 = union_mode(sm, fr.T, bj2);
+      if (work && lane == 0)
+        atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(nm) * static_cast<unsigned long long>(nn));
     }
-    for (int off = two ? 0 : G >> 1; off >= 1; off >>= 1) {  // stays inside the aligned G-lane group
-      const float oq = __shfl_xor_sync(0xffffffffu, bq, off);
-      const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
-      if (oj != 0x7fffffff && (bj == 0x7fffffff || oq < bq || (oq == bq && oj < bj))) {
-        bq = oq;
-        bj = oj;
-      }
-    }
-    if (bj != 0x7fffffff) bmi = union_mode(sm, fr.T, bj);
-    if (bj2 != 0x7fffffff) bmi2 = union_mode(sm, fr.T, bj2);
-    if (work && lane == 0)
-      atomicAdd(&work[W_LM_ASSOC], static_cast<unsigned long long>(nm) * static_cast<unsigned long long>(nn));
+    if (v && sub == 0) assoc[(static_cast<size_t>(a) * la.cand_stride + s_list[h]) * la.scap + s] = bmi;
+    if (v2) assoc[(static_cast<size_t>(a) * la.cand_stride + s_list[lane + 32]) * la.scap + s] = bmi2;
   }
-  if (v && sub == 0) assoc[(static_cast<size_t>(a) * la.cand_stride + s_list[h]) * la.scap + s] = bmi;
-  if (v2) assoc[(static_cast<size_t>(a) * la.cand_stride + s_list[lane + 32]) * la.scap + s] = bmi2;
 }
 
 // One LM iteration of one hypothesis, all lanes in lockstep.
@@ -2403,7 +2434,7 @@ scr_status run_stage(scr_scene s, int nA, const scr_ransac_params& p, int mode, 
       // candidates still in play at step k: at most ceil(n_cull / 2^(k-1))
       const int nk = (p.n_cull + (1 << (k - 1)) - 1) >> (k - 1);
       for (int it = 0; it < 10; ++it) {
-        const dim3 ag((ns + 7) / 8, nA);
+        const dim3 ag((ns + 8 * kAssocSpw - 1) / (8 * kAssocSpw), nA);
         SCR_LAUNCH(s, K_LM, (k_lm_assoc_c<<<ag, 256, 0, s->stream>>>(fr, pv, la, w.samples, w.cand, w.ncand, lmst,
                                                                      w.assoc, wk)));
         SCR_LAUNCH(s, K_LM, (k_lm_step<<<dim3(nk, nA), kLmThreads, 0, s->stream>>>(
