@@ -1601,7 +1601,7 @@ constexpr int kLmInFlight = SCR_LM_INFLIGHT;  // sample gathers in flight per la
 constexpr int kLmThreads = 128;  // canonical LM reduction lanes per candidate (4 warps)
 
 #ifndef SCR_LM_STEP_MINB
-#define SCR_LM_STEP_MINB 1
+#define SCR_LM_STEP_MINB 4  // 128 registers (a little spilling), 16 warps per SM
 #endif
 __global__ void __launch_bounds__(kLmThreads, SCR_LM_STEP_MINB) k_lm_step(FrameRefs fr, PredView pv, LmArgs la,
                                                  const int* __restrict__ samples, Pose* __restrict__ cand,
