@@ -141,6 +141,28 @@ def test_ransac_exact_finisher_paths(oracle, world, gscene):
         gscene.debug_generation_mode(0)
 
 
+@pytest.mark.parametrize("prof,over", [
+    ("default", dict(n_cull=40, n_out=1)),      # 40 -> 20 -> 10 -> 5 -> 3 -> 2 -> 1: every lane layout
+    ("default", dict(n_cull=33, n_out=2)),
+    ("intermediate", dict(n_cull=20, n_out=1)),  # Euclidean association
+    ("intermediate", dict(n_cull=7, n_out=3)),
+])
+def test_ransac_lm_candidate_counts(oracle, world, gscene, prof, over):
+    """LM association over the compacted candidate list picks its lane layout from the number
+    of candidates that need it (two per lane, one per lane, G lanes per candidate): culls that
+    are not powers of two and several survivors keep every layout bit-exact."""
+    import paper_1810_12163_b200 as P
+
+    i = 0
+    p = of.ransac_params(prof, **over)
+    gp = P.ransac_params(prof, **over)
+    st, gs, gpz, ss, sp, se = gscene.debug_ransac(world.Dt[i], world.RGBt[i], gp, 300 + i)
+    rc, ogs, ogp, oss, osp, ose = oracle.ransac(world.forest, world.state, world.Dt[i], world.RGBt[i], K, p, 300 + i)
+    assert np.array_equal(ss, oss), (prof, over, ss, oss)
+    assert np.array_equal(se.view(np.uint32), ose.view(np.uint32))
+    assert all(bytes(a) == bytes(b) for a, b in zip(sp, osp))
+
+
 def test_icp_matches_oracle(oracle, world, gscene):
     import ctypes as C
 
