@@ -261,6 +261,33 @@ SURVEY_FLOP_PER_ATTEMPT = 600
 GEN_OPS_PER_ATTEMPT = 7 * 21 + 7 * 23 + 3 * 14 + 12 + 12
 
 
+# SURVEY.md §8(d) whole-frame model: flop constants per counted unit (transform 21,
+# Mahalanobis + min 30 per mode, LM ~300 per sample-iteration, Kabsch + checks ~600 per
+# attempt, ICP 100 per pixel-iteration, ray cast 40 per primitive tested) on the FP32 pipe,
+# plus the feature / forest bytes (frame W*H*7 + 16 B per node visit) on HBM.
+SURVEY_FLOPS = {"sample_eval": 21, "mode_eval": 30, "lm_term": 300, "lm_assoc_eval": 30, "gen_attempt": 600,
+                "icp_term": 100, "ray_prim": 40}
+
+
+def frame_model(work: dict, frames: int, res, per_gpu_value: float, peaks: dict, fp32_peak: float) -> dict | None:
+    """Ideal time per relocalisation on the SURVEY.md §8(d) model (counted on device over the
+    instrumented pass, which is bit-identical to the oracle's work) against the measured one."""
+    if frames <= 0 or per_gpu_value <= 0:
+        return None
+    flop = (SURVEY_FLOPS["sample_eval"] * work.get("sample_evals", 0) + SURVEY_FLOPS["mode_eval"] * work.get("mode_evals", 0)
+            + SURVEY_FLOPS["lm_term"] * work.get("lm_terms", 0) + SURVEY_FLOPS["lm_assoc_eval"] * work.get("lm_assoc_evals", 0)
+            + SURVEY_FLOPS["gen_attempt"] * work.get("gen_attempts", 0) + SURVEY_FLOPS["icp_term"] * work.get("icp_terms", 0)
+            + SURVEY_FLOPS["ray_prim"] * work.get("ray_prim_tests", 0)) / frames
+    byts = res[0] * res[1] * 7 + 16 * work.get("node_visits", 0) / frames
+    hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+    t_ideal = flop / (fp32_peak * 1e12) + byts / hbm
+    t_meas = 1.0 / per_gpu_value
+    return {"flop_per_frame": round(flop), "bytes_per_frame": round(byts), "ideal_us_per_frame": round(t_ideal * 1e6, 2),
+            "measured_us_per_frame": round(t_meas * 1e6, 2), "frac": round(t_ideal / t_meas, 4),
+            "model": "SURVEY.md §8(d): sum of FP32 flops / 74.4 TFLOP/s + feature bytes / HBM, per relocalisation",
+            "frames_counted": frames}
+
+
 def kernel_model(name: str, work: dict) -> tuple | None:
     """(algorithmic work, bound) of a kernel from the device work counters."""
     if name == "k_hypgen":
@@ -501,13 +528,14 @@ def run_ours(args, wl: Workload):
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(stream)
-    prof_batches = 0
+    prof_batches = prof_frames = 0
     for st in range(args.steps):
         for li in range(L):
             if lanes[li][0] is r0:
                 idx, sd = batch_at(li, args.warmup + st)
                 r0.fs.cascade(idx, cfg, sd)
                 prof_batches += 1
+                prof_frames += len(idx)
     p1.record(stream)
     torch.cuda.synchronize()
     prof_ms = p0.elapsed_time(p1)
@@ -611,6 +639,7 @@ def run_ours(args, wl: Workload):
         return r
 
     roofline = roof(dom)
+    frame_roof = frame_model(prof["work"], prof_frames, wl.res, value / max(1, world), peaks, fp32_peak)
     rooflines = {n: roof(n) for n in sorted(kern, key=lambda n: -kern[n]["ms"])[:6]
                  if n != dom and kernel_model(n, prof["work"]) is not None}
     tot_ms = sum(x["ms"] for x in kern.values())
@@ -637,6 +666,7 @@ def run_ours(args, wl: Workload):
         "gpu_launches": int(sum_over_ranks(float(launches), dist, dev_t)),
         "roofline": roofline,
         "rooflines_other": rooflines,
+        "roofline_frame": frame_roof,
         "clocks": clk.summary(),
         "accuracy": {"success_5cm_5deg": round(succ, 4), "frames": n_res, "stage_mix": stage_hist,
                      "stage_share": [round(x / max(1, n_res), 4) for x in stage_hist],
