@@ -710,9 +710,6 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
   const int ns = min(sus_cnt[a], kMaxSuspects);
   for (int i = threadIdx.x; i < 2 * ns; i += blockDim.x) s_sus[i >> 1][i & 1] = sus[2 * static_cast<size_t>(a) * kMaxSuspects + i];
   const bool clear = slot < gp.nmax && hok[out] == 2;
-#ifdef SCR_FIN_DEBUG
-  if (threadIdx.x == 0 && blockIdx.x == 0 && sus_cnt[a]) printf("hypfin-sus a=%d n=%d\n", a, sus_cnt[a]);
-#endif
   if (!__syncthreads_or(clear) && ns == 0) return;
   const int f = fr.fidx[a];
   const size_t fbase = static_cast<size_t>(f) * fr.gmax;
@@ -782,9 +779,6 @@ __global__ void __launch_bounds__(kFinThreads) k_hypfin(GenParams gp, FrameGeom 
         geometry_prefilter(gp.min_sq_dist, gp.rigidity_tol, grec, g, ifx, ify, pv.geom, g0, g1, g2, m0, m1, m2))
       ok = geometry_exact(gp.min_sq_dist, gp.rigidity_tol, grec, g, pv.geom, g0, g1, g2, m0, m1, m2, &T);
   }
-#ifdef SCR_FIN_DEBUG
-  printf("hypfin-cont a=%d slot=%d att=%d it=%d ok=%d\n", a, slot, att, it, ok ? 1 : 0);
-#endif
   if (ok) hyp[out] = T;
   hok[out] = ok ? 1 : 0;
   hiters[out] = it;  // ok: the passing attempt + 1; otherwise max_iters
