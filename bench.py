@@ -574,8 +574,8 @@ def run_ours(args, wl: Workload):
                for kk, v in sorted(per_bin.items())}
 
     # ---- e2e: pinned host frames through the C ABI (H2D + result D2H inside). Each call hands
-    # the library two batches, so it uploads the second while the first one's cascade runs.
-    CALL = 2 * B
+    # the library --e2e-batches batches, so it uploads batch j + 1 while batch j's cascade runs.
+    CALL = args.e2e_batches * B
     pins = {}
     for r in runs:
         nb = min(len(r.poses), CALL)
@@ -597,7 +597,7 @@ def run_ours(args, wl: Workload):
         e2e_step(li, 0)
     if dist is not None:
         dist.barrier()
-    e2e_calls = max(1, args.steps // 2)
+    e2e_calls = max(1, args.steps // args.e2e_batches)
     e2e_ms = max_over_ranks(run_lanes(e2e_step, e2e_calls), dist, dev_t)
     e2e_value = sum_over_ranks(float(e2e_calls * CALL * L), dist, dev_t) / (e2e_ms / 1e3)
     h2d = B * L * (k.width * k.height * 4 + k.width * k.height * 3)
@@ -998,6 +998,7 @@ def main(argv=None):
     ap.add_argument("--ref-batch", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--lanes", type=int, default=0, help="relocalisation lanes (streams + host threads) per GPU")
+    ap.add_argument("--e2e-batches", type=int, default=4, help="lane batches per scr_cascade_batch call in the e2e leg")
     ap.add_argument("--profile-window", action="store_true",
                     help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
     args = ap.parse_args(argv)
