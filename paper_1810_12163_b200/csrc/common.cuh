@@ -798,6 +798,27 @@ SCR_DEV double warp_sum_xor(double v) {
   for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, off);
   return v;
 }
+// warp_sum_xor of N <= 32 values at once ("transpose" reduction): at offset o every lane
+// keeps one half of its remaining values and sends the other half to lane ^ o, so each value
+// is combined with the same partner partial at every level as in its own xor butterfly (the
+// pairs are identical and IEEE addition is commutative): bit-identical sums, 31 shuffles of
+// a double instead of 5 N. On return lane k holds the sum of value k (for k < N) in v[0].
+template <int N>
+SCR_DEV void warp_sum_xor_many(double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = N; k < 32; ++k) v[k] = 0.0;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const double send = upper ? v[i] : v[i + o];
+      const double keep = upper ? v[i + o] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
 SCR_DEV int warp_isum(int v) {
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);

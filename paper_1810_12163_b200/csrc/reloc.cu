@@ -1648,10 +1648,12 @@ __global__ void __launch_bounds__(kLmThreads, SCR_LM_STEP_MINB) k_lm_step(FrameR
   }
   if (work) work_add(work, W_LM_TERMS, static_cast<unsigned>(terms));
   // canonical 128-lane reduction: xor butterfly inside each warp, then (W0 + W1) + (W2 + W3)
+  {
+    double v[32];
 #pragma unroll
-  for (int k = 0; k < 28; ++k) {
-    const double v = warp_sum_xor(acc[k]);
-    if (lane == 0) s_red[wid][k] = v;
+    for (int k = 0; k < 28; ++k) v[k] = acc[k];
+    warp_sum_xor_many<28>(v);
+    if (lane < 28) s_red[wid][lane] = v[0];
   }
   __syncthreads();
   if (tid < 28) s_tot[tid] = (s_red[0][tid] + s_red[1][tid]) + (s_red[2][tid] + s_red[3][tid]);
