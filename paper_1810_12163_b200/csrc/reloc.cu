@@ -415,7 +415,10 @@ SCR_DEV int attempt_exact(Rng& rng, const GenParams& gp, const FrameRefs& fr, co
 #endif
 constexpr int kGenWarps = SCR_GEN_WARPS;  // warps per generation CTA
 constexpr int kGenQ = 64;
-constexpr int kMaxSuspects = 64;  // per frame: triplets whose Kabsch may be degenerate
+#ifndef SCR_MAX_SUSPECTS
+#define SCR_MAX_SUSPECTS 256  // 64 overflowed on the Default profile: slots then replayed their attempts serially in k_hypfin
+#endif
+constexpr int kMaxSuspects = SCR_MAX_SUSPECTS;  // per frame: triplets whose Kabsch may be degenerate
 // A queued colour-check survivor. Fast-path entries carry the three raw mode draws and are
 // resolved to mode indices in the evaluation phase (at full SIMD width, instead of by the
 // few passing lanes of every attempt round); exact-path entries carry resolved modes.
