@@ -300,3 +300,26 @@ def test_multi_chunk_calls_match_single_chunk(oracle, gpu_device, world):
         assert a.stage_used == b.stage_used and a.has_pose == b.has_pose
         assert bytes(a.pose) == bytes(b.pose) and (a.score == b.score or (np.isinf(a.score) and np.isinf(b.score)))
     small.close()
+
+
+def test_relocalise_at_an_untiled_resolution(oracle, gpu_device):
+    """400 x 300: no pyramid level's width (400, 200, 100) is a multiple of the 32-pixel ray-cast
+    tile, so ICP and ranking cast through the untiled primitive lists; all three modes stay
+    bit-exact with the oracle."""
+    import paper_1810_12163_b200 as P
+
+    k = of.intrinsics(400, 300, 365.0, 365.0)
+    w = OracleWorld(oracle, scene_seed=2, n_adapt=12, n_test=3, k=k)
+    s = gpu_scene(gpu_device, w)
+    s.integrate_frames(list(w.D), list(w.RGB), w.adapt_poses)
+    s.update_leaves_round_robin(s.total_leaves)
+    for mode in (0, 1, 2):
+        res = s.relocalise_batch(w.Dt, w.RGBt, P.ransac_params("default"), mode, [2000 + i for i in range(3)])
+        for i, r in enumerate(res):
+            ref = oracle.relocalise(w.forest, w.state, w.scene, w.Dt[i], w.RGBt[i], k, of.ransac_params("default"),
+                                    mode, 2000 + i)
+            assert r.has_pose == ref.has_pose and r.status == ref.status, (mode, i)
+            if r.has_pose:
+                assert bytes(r.pose) == bytes(ref.pose), f"mode {mode} frame {i}"
+                assert r.score == ref.score or (np.isinf(r.score) and np.isinf(ref.score))
+    s.close()
