@@ -323,3 +323,26 @@ def test_relocalise_at_an_untiled_resolution(oracle, gpu_device):
                 assert bytes(r.pose) == bytes(ref.pose), f"mode {mode} frame {i}"
                 assert r.score == ref.score or (np.isinf(r.score) and np.isinf(ref.score))
     s.close()
+
+
+@pytest.mark.parametrize("prof,over", [
+    ("fast", dict(n_max=37)),                   # fewer slots than one warp's lanes
+    ("fast", dict(n_max=1000, max_gen_iters=77)),
+    ("default", dict(n_max=333, n_cull=17, n_out=3)),
+])
+def test_ransac_odd_slot_counts(oracle, world, gscene, prof, over):
+    """Slot counts that fill no warp or CTA evenly (slots are pulled from a per-frame counter;
+    survivors compacted in slot order) stay bit-exact with the sequential reference."""
+    import paper_1810_12163_b200 as P
+
+    p = of.ransac_params(prof, **over)
+    gp = P.ransac_params(prof, **over)
+    for i in range(2):
+        st, gs, gpz, ss, sp, se = gscene.debug_ransac(world.Dt[i], world.RGBt[i], gp, 500 + i)
+        rc, ogs, ogp, oss, osp, ose = oracle.ransac(world.forest, world.state, world.Dt[i], world.RGBt[i], K, p,
+                                                    500 + i)
+        assert np.array_equal(gs, ogs)
+        assert all(bytes(a) == bytes(b) for a, b in zip(gpz, ogp))
+        assert np.array_equal(ss, oss)
+        assert np.array_equal(se.view(np.uint32), ose.view(np.uint32))
+        assert all(bytes(a) == bytes(b) for a, b in zip(sp, osp))
